@@ -1,0 +1,303 @@
+/*
+ * scx.h -- C-ABI of libscx.so, the sm_100a kernels behind the
+ * paper_2506_09226_b200 relational operators.
+ *
+ * The reference (`/root/reference/pkg/src/shufflecast`) is pure numpy and has
+ * no FFI; each entry point below replaces the numpy body of the Python
+ * operator named in its comment (file:line under /root/reference/pkg/src/
+ * shufflecast).  The Python host layer (paper_2506_09226_b200/*.py) keeps the
+ * reference's operator/plan API and binds these through ctypes
+ * (INTEGRATION.md shows the binding a shufflecast maintainer would add).
+ *
+ * Conventions
+ *   - Every pointer argument named *_dev / uint64 "ptr" fields is a DEVICE
+ *     address (e.g. torch.Tensor.data_ptr()).  Host pointers are named *_host.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t, passed as
+ *     void*; NULL = legacy default stream).  Nothing allocates: callers pass
+ *     scratch sized by the matching *_workspace query.
+ *   - Return 0 on success, a negative SCX_E* code on error; the message is in
+ *     scx_last_error() (thread-local).  No C++ exception crosses the ABI.
+ *   - No global mutable state: safe to call from one thread per device.
+ */
+#ifndef SCX_H
+#define SCX_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SCX_ABI_VERSION 1
+
+/* ---- error codes ------------------------------------------------------- */
+#define SCX_OK            0
+#define SCX_EINVAL       -1   /* bad argument / descriptor                  */
+#define SCX_ECUDA        -2   /* CUDA runtime error (launch, memset, ...)   */
+#define SCX_ECAPACITY    -3   /* caller-provided buffer too small           */
+#define SCX_EUNSUPPORTED -4   /* shape outside what the kernels implement   */
+
+/* ---- physical column types (narrowed HBM layout) ---------- */
+#define SCX_I8   0
+#define SCX_I16  1
+#define SCX_I32  2
+#define SCX_I64  3
+#define SCX_U8   4
+#define SCX_U16  5
+#define SCX_F64  6
+#define SCX_U32  7
+
+/* ---- limits of one pipeline descriptor --------------------------------- */
+#define SCX_MAX_BASE      12   /* scanned (TMA-staged) columns              */
+#define SCX_MAX_SLOTS     20   /* base + probe-payload operand slots        */
+#define SCX_MAX_ATOMS     40
+#define SCX_MAX_SETWORDS  128  /* dictionary-set bitmaps, 32 codes / word   */
+#define SCX_MAX_LUT       512  /* dictionary code -> string-rank tables     */
+#define SCX_MAX_PROBES    3
+#define SCX_MAX_PAYLOAD   6
+#define SCX_MAX_MEASURES  8
+#define SCX_MAX_GKEYS     4
+#define SCX_MAX_OUT       16
+#define SCX_MAX_KEYS      4    /* key columns of a join / partition key     */
+
+/* atom ops: one comparison evaluated per row */
+#define SCX_ATOM_RANGE  0      /* lo <= v[slot] <= hi                         */
+#define SCX_ATOM_SET    1      /* bit v[slot] of setwords[set_word..] is 1;
+                                  lo = number of bitmap words of the set     */
+#define SCX_ATOM_DIFF   2      /* lo <= v[slot] - v[slot2] <= hi              */
+
+/* join kinds for a probe stage (relops.py:59-94) */
+#define SCX_JOIN_SEMI   0
+#define SCX_JOIN_ANTI   1
+#define SCX_JOIN_INNER  2      /* build keys unique: 0/1 match per probe row  */
+
+/* lookup-table kinds */
+#define SCX_HT_HASH     0      /* open addressing, u64 keys, linear probing   */
+#define SCX_HT_DIRECT   1      /* dense key range: vals[packed key]           */
+
+/* aggregate ops (relops.py:11, AGG_OPS) */
+#define SCX_AGG_SUM     0
+#define SCX_AGG_COUNT   1
+#define SCX_AGG_MIN     2
+#define SCX_AGG_MAX     3
+
+/* pipeline sinks */
+#define SCX_SINK_AGG_DENSE 0   /* small key domain: register/smem pre-agg    */
+#define SCX_SINK_AGG_HASH  1   /* open-addressing group table, global atomics */
+#define SCX_SINK_COMPACT   2   /* stable stream compaction (decoupled look-back) */
+#define SCX_SINK_COUNT     3   /* selected-row count only                      */
+
+#define SCX_EMPTY_KEY 0xFFFFFFFFFFFFFFFFull
+#define SCX_NO_ROW    0xFFFFFFFFu
+
+typedef struct scx_column {
+  uint64_t ptr;     /* device address of element 0 (16-byte aligned) */
+  int32_t dtype;    /* SCX_I8 ... */
+  int32_t _pad;
+} scx_column;
+
+typedef struct scx_atom {
+  int32_t op;       /* SCX_ATOM_* */
+  int32_t slot;
+  int32_t slot2;    /* DIFF only */
+  int32_t clause;   /* DNF clause 0..31 this atom belongs to */
+  int32_t set_word; /* SET: first word in setwords[] */
+  int32_t negate;   /* 1: atom result inverted */
+  int64_t lo, hi;   /* RANGE/DIFF bounds, inclusive */
+} scx_atom;
+
+/* A predicate in disjunctive normal form over atoms[first .. first+n).
+ * Row passes iff some clause c (bit c of clause_mask) has no failing atom.
+ * clause_mask == 0 means TRUE. */
+typedef struct scx_pred {
+  int32_t first_atom;
+  int32_t n_atoms;
+  uint32_t clause_mask;
+  int32_t _pad;
+} scx_pred;
+
+/* factor = a + b * v[slot]   (slot < 0: the constant a) */
+typedef struct scx_factor {
+  int64_t a, b;
+  int32_t slot;
+  int32_t _pad;
+} scx_factor;
+
+typedef struct scx_term {
+  int64_t coef;
+  int32_t n_factors;   /* 0..3 */
+  int32_t _pad;
+  scx_factor f[3];
+} scx_term;
+
+/* measure value per row = sum_t coef_t * prod_f factor_f, gated by cond_atom */
+typedef struct scx_measure {
+  int32_t op;          /* SCX_AGG_* (COUNT ignores terms) */
+  int32_t n_terms;     /* 1..2 */
+  int32_t cond_atom;   /* -1 or index into atoms[]: row contributes iff it holds */
+  int32_t _pad;
+  scx_term t[2];
+} scx_measure;
+
+/* key spec shared by probes, builds, group keys and partitioning:
+ * packed = sum_k (v[slot_k] - lo_k) << shift_k  (must fit 64 bits). */
+typedef struct scx_keyspec {
+  int32_t n;
+  int32_t slot[SCX_MAX_KEYS];
+  int32_t shift[SCX_MAX_KEYS];
+  int32_t bits[SCX_MAX_KEYS];  /* component k must lie in [0, 2^bits_k)   */
+  int32_t _pad;
+  int64_t lo[SCX_MAX_KEYS];
+} scx_keyspec;
+
+/* Lookup table built by scx_table_build and probed inside a pipeline. */
+typedef struct scx_lookup {
+  int32_t kind;        /* SCX_HT_HASH / SCX_HT_DIRECT */
+  int32_t _pad;
+  uint64_t keys;       /* HASH: u64[cap], SCX_EMPTY_KEY = free        */
+  uint64_t vals;       /* u32[cap] build row, SCX_NO_ROW = free        */
+  uint64_t cap;        /* HASH: power of two; DIRECT: key range size   */
+} scx_lookup;
+
+typedef struct scx_probe {
+  int32_t kind;        /* SCX_JOIN_* */
+  int32_t n_payload;
+  scx_keyspec key;     /* probe-side key slots, same packing as the build */
+  scx_lookup table;
+  scx_column payload[SCX_MAX_PAYLOAD];   /* build-side columns, gathered ... */
+  int32_t payload_slot[SCX_MAX_PAYLOAD]; /* ... into these operand slots     */
+} scx_probe;
+
+typedef struct scx_sink {
+  int32_t kind;        /* SCX_SINK_* */
+  int32_t n_measures;
+  scx_measure m[SCX_MAX_MEASURES];
+  /* group keys: DENSE uses card/lut (cell = mixed radix of ranks),
+   *             HASH packs them with gkey (shift/lo). */
+  scx_keyspec gkey;
+  int32_t gcard[SCX_MAX_GKEYS];   /* DENSE: domain size of key k          */
+  int32_t glut[SCX_MAX_GKEYS];    /* DENSE: offset into lut[] or -1       */
+  int32_t n_cells;                /* DENSE: prod(gcard)                   */
+  int32_t n_out;                  /* COMPACT: output columns              */
+  uint64_t acc;        /* DENSE: {u64 lo, i64 hi}[cells][M]; HASH: i64[cap][M] */
+  uint64_t gkeys;      /* HASH: u64[cap] packed group keys                 */
+  uint64_t gcap;       /* HASH: capacity (power of two)                    */
+  uint64_t flags;      /* u32[4]: [0] hash table full, [1] dup build key   */
+  int32_t out_slot[SCX_MAX_OUT];  /* COMPACT: slot, or -1 = base row index  */
+  scx_column out[SCX_MAX_OUT];
+  uint64_t status;     /* COMPACT: u64[n_tiles] look-back words, zeroed    */
+  uint64_t count;      /* COMPACT/COUNT: u64[1] selected rows (written)    */
+} scx_sink;
+
+typedef struct scx_pipeline {
+  int64_t n_rows;
+  int32_t n_base;
+  int32_t n_slots;
+  int32_t n_probes;
+  int32_t _pad;
+  scx_column base[SCX_MAX_BASE];
+  int32_t slot_dtype[SCX_MAX_SLOTS];
+  scx_pred pre;                  /* on base slots, before probes          */
+  scx_pred post;                 /* on any slot, after probes             */
+  scx_probe probe[SCX_MAX_PROBES];
+  scx_sink sink;
+  scx_atom atoms[SCX_MAX_ATOMS];
+  uint32_t setwords[SCX_MAX_SETWORDS];
+  int16_t lut[SCX_MAX_LUT];
+} scx_pipeline;
+
+/* ---- library info ------------------------------------------------------ */
+const char* scx_last_error(void);
+int scx_abi_version(void);
+/* kernels launched through libscx in this process so far */
+uint64_t scx_launch_count(void);
+/* sizeof of each descriptor struct, for binding checks: which = 0 pipeline,
+ * 1 probe, 2 sink, 3 measure, 4 atom, 5 keyspec, 6 lookup */
+int64_t scx_sizeof(int which);
+/* number of SMs / opt-in smem on `device` (for host-side sizing) */
+int scx_device_info(int device, int* sm_count, int* smem_optin);
+
+/* ---- fused scan pipeline -------------------------------------------------
+ * Replaces the numpy bodies of: ColumnTable.filter/take + driver predicate
+ * expressions (table.py:171-192, queries.py:39-234), local_hash_join probe
+ * (relops.py:59-94), group_aggregate (relops.py:97-160), q1's np.add.at grid
+ * (queries.py:42-54) and q6's filtered sum (queries.py:105-119).
+ * One launch: TMA-bulk-staged column tiles -> predicate -> probes ->
+ * post-predicate -> sink.  `desc_host` is copied into the launch. */
+int scx_pipeline_run(const scx_pipeline* desc_host, void* stream);
+/* number of 'status' words a COMPACT sink needs for n_rows */
+int64_t scx_pipeline_status_words(const scx_pipeline* desc_host);
+
+/* ---- lookup tables (local_hash_join build side, relops.py:81-84) --------
+ * Inserts packed keys of rows [0, n) of `cols` into `table` (pre-cleared
+ * with scx_lookup_clear).  flags_dev[1] is set to 1 when a key repeats
+ * (caller then uses the multi-match path). */
+int scx_lookup_clear(const scx_lookup* table, void* stream);
+int scx_lookup_build(const scx_lookup* table, const scx_column* cols, int n_cols,
+                     const scx_keyspec* key, int64_t n, uint32_t* flags_dev,
+                     void* stream);
+
+/* ---- group table finalize (group_aggregate output, relops.py:115-160) ----
+ * DENSE: sums n_ranks partial {lo,hi} accumulator copies (stride cells*M*2
+ * words) into one exact 128-bit {lo,hi} per (cell, measure).
+ * HASH: compacts occupied slots -> out_keys (u64) + out_acc measure-major
+ * (out_acc[m * cap + row]), count in count_dev[0].  Row order is slot order
+ * (caller sorts by packed key). */
+int scx_dense_reduce(const int64_t* acc_dev, int n_ranks, int cells, int m,
+                     int64_t* out_dev, void* stream);
+int scx_hash_agg_compact(const uint64_t* gkeys_dev, const int64_t* acc_dev,
+                         int64_t cap, int m, uint64_t* out_keys_dev,
+                         int64_t* out_acc_dev, uint64_t* count_dev, void* stream);
+
+/* ---- key unpack / convert ------------------------------------------------ */
+/* out[i] = ((packed[i] >> shift) & mask) + lo, stored as dtype */
+int scx_unpack_key(const uint64_t* packed_dev, int64_t n, int shift, uint64_t mask,
+                   int64_t lo, scx_column out, void* stream);
+/* out_f64[i] = (double)in[i*stride] / 10^scale  (optionally / max(cnt,1)) */
+int scx_fixed_to_f64(const int64_t* in_dev, int64_t stride, int64_t n, int scale,
+                     const int64_t* count_dev, int64_t count_stride,
+                     double* out_dev, void* stream);
+
+/* ---- sort (ColumnTable.sort_by, table.py:198-214) -------------------------
+ * Stable LSD radix sort of (key u64, value u32) pairs on key bits
+ * [0, n_bits).  Ping-pong buffers; result lands in *_out.  temp_dev sized by
+ * scx_sort_workspace. */
+int64_t scx_sort_workspace(int64_t n);
+int scx_sort_pairs(const uint64_t* keys_in, const uint32_t* vals_in,
+                   uint64_t* keys_out, uint32_t* vals_out,
+                   uint64_t* keys_tmp, uint32_t* vals_tmp,
+                   int64_t n, int n_bits, void* temp_dev, void* stream);
+/* key[i] = encode(col[idx ? idx[i] : i]) : order-preserving u64 of the value,
+ * minus lo, bit-inverted within n_bits when descending. */
+int scx_encode_sort_key(scx_column col, const uint32_t* idx_dev, int64_t n,
+                        int64_t lo, int n_bits, int descending, int shift,
+                        const int32_t* lut_dev, uint64_t* key_dev, int accumulate,
+                        void* stream);
+/* out_dev[0] = min, out_dev[1] = max over the column (integer dtypes);
+ * out_dev must be pre-set to {INT64_MAX, INT64_MIN}. */
+int scx_minmax(scx_column col, int64_t n, int64_t* out_dev, void* stream);
+/* out[i] = in[idx[i]] for a column of dtype (take, table.py:76-77/171) */
+int scx_gather(scx_column in, const uint32_t* idx_dev, int64_t n, scx_column out,
+               void* stream);
+/* idx[i] = i */
+int scx_iota(uint32_t* idx_dev, int64_t n, void* stream);
+/* p[i * stride] = value for i < n  (table / accumulator initialisation) */
+int scx_fill_i64(int64_t* p_dev, int64_t n, int64_t stride, int64_t value, void* stream);
+
+/* ---- hash partitioning (exchange.py:35-70) --------------------------------
+ * bucket(row) = fib_hash(keys) mod n_parts with the reference's u64 wrap:
+ *   acc = 0; for k: acc = (acc ^ (u64(v_k) * F)) * F,  F = 0x9E3779B97F4A7C15
+ * scx_hash_keys writes the raw u64 hashes.  scx_partition computes counts
+ * (u64[n_parts]) and a stable scatter of every column into `outs`, parts
+ * contiguous in bucket order, rows in input order within a part. */
+int scx_hash_keys(const scx_column* keys, int n_keys, int64_t n, uint64_t* out_dev,
+                  void* stream);
+int64_t scx_partition_workspace(int64_t n, int n_parts);
+int scx_partition(const scx_column* keys, int n_keys, const scx_column* cols,
+                  const scx_column* outs, int n_cols, int64_t n, int n_parts,
+                  uint64_t* counts_dev, void* temp_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SCX_H */

@@ -1,0 +1,309 @@
+// radix.cu -- stable 8-bit-digit counting passes shared by
+//   * scx_sort_pairs   : LSD radix sort (ColumnTable.sort_by, table.py:198-214)
+//   * scx_partition    : hash partition + stable scatter (exchange.py:52-70,
+//                        hash_partition / partition_indices; the reference's
+//                        stable argsort by bucket + take of every column)
+//   * scx_hash_keys    : raw Fibonacci hashes (exchange.py:35-49)
+//
+// Each CTA owns a contiguous chunk of kChunk rows processed as 16 sub-tiles of
+// 256 rows in order.  Stability within a sub-tile comes from a per-warp
+// __match_any_sync rank plus a per-(warp, digit) exclusive scan in shared
+// memory; across CTAs from a digit-major exclusive scan of the per-CTA
+// histograms.  So every element's output position is the same as a stable
+// sort by digit, which is exactly partition_indices' stable argsort.
+#include "common.cuh"
+
+namespace scx {
+
+constexpr int kDigits = 256;
+constexpr int kItems = 16;
+constexpr int kChunk = kBlock * kItems;   // 4096 rows per CTA
+
+struct PartKeys {
+  scx_column k[SCX_MAX_KEYS];
+  int n;
+};
+struct PartCols {
+  scx_column in[SCX_MAX_OUT];
+  scx_column out[SCX_MAX_OUT];
+  int n;
+};
+
+__device__ __forceinline__ uint64_t fib_hash_row(const PartKeys& K, int64_t i) {
+  uint64_t acc = 0;
+  for (int j = 0; j < K.n; ++j)
+    acc = fib_step(acc, load_i64(reinterpret_cast<const void*>(K.k[j].ptr), K.k[j].dtype, i));
+  return acc;
+}
+
+__device__ __forceinline__ uint32_t bucket_of(const PartKeys& K, int64_t i, uint32_t nparts) {
+  const uint64_t h = fib_hash_row(K, i);
+  return (nparts & (nparts - 1)) == 0 ? (uint32_t)(h & (nparts - 1)) : (uint32_t)(h % nparts);
+}
+
+// digit source: sort pass (key >> shift) & 255, or partition bucket
+struct DigitSrc {
+  const uint64_t* keys;
+  int shift;
+  PartKeys pk;
+  uint32_t nparts;
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const {
+    return keys ? (uint32_t)((keys[i] >> shift) & 255u) : bucket_of(pk, i, nparts);
+  }
+};
+
+__global__ void hist_kernel(DigitSrc D, int64_t n, int ndig, uint32_t* counts, int nblocks) {
+  __shared__ uint32_t h[kDigits];
+  for (int d = threadIdx.x; d < kDigits; d += kBlock) h[d] = 0;
+  __syncthreads();
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int it = 0; it < kItems; ++it) {
+    const int64_t i = base + it * kBlock + threadIdx.x;
+    if (i < n) atomicAdd(&h[D(i)], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < ndig; d += kBlock) counts[(int64_t)d * nblocks + blockIdx.x] = h[d];
+}
+
+// single-CTA exclusive scan of m u32 counts into u64 offsets (m <= ~16M)
+__global__ void scan_kernel(const uint32_t* in, uint64_t* out, int64_t m) {
+  __shared__ uint64_t part[1024];
+  const int t = threadIdx.x;
+  const int64_t per = (m + 1023) / 1024;
+  const int64_t b = t * per, e = min(m, b + per);
+  uint64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += in[i];
+  part[t] = s;
+  __syncthreads();
+  for (int o = 1; o < 1024; o <<= 1) {
+    uint64_t v = (t >= o) ? part[t - o] : 0;
+    __syncthreads();
+    part[t] += v;
+    __syncthreads();
+  }
+  uint64_t run = part[t] - s;
+  for (int64_t i = b; i < e; ++i) { out[i] = run; run += in[i]; }
+  if (t == 1023) out[m] = part[1023];
+}
+
+// stable scatter; `emit(i, pos)` writes element i to pos
+template <typename Emit>
+__device__ __forceinline__ void scatter_chunk(const DigitSrc& D, int64_t n, int ndig,
+                                              const uint64_t* offs, int nblocks, Emit emit) {
+  __shared__ uint32_t wc[kWarps][kDigits];
+  __shared__ uint64_t run[kDigits];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int d = tid; d < kDigits; d += kBlock)
+    run[d] = d < ndig ? offs[(int64_t)d * nblocks + blockIdx.x] : 0;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int it = 0; it < kItems; ++it) {
+    for (int j = tid; j < kWarps * kDigits; j += kBlock) (&wc[0][0])[j] = 0;
+    __syncthreads();
+    const int64_t i = base + it * kBlock + tid;
+    const bool valid = i < n;
+    const uint32_t d = valid ? D(i) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(peers & ((1u << lane) - 1u));
+    if (valid && rank == 0) wc[warp][d] = __popc(peers);
+    __syncthreads();
+    // per digit: exclusive scan over warps (thread d owns digit d)
+    for (int dd = tid; dd < kDigits; dd += kBlock) {
+      uint32_t s = 0;
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) { const uint32_t c = wc[w][dd]; wc[w][dd] = s; s += c; }
+      // stash total in run after positions are computed: use a second pass
+      // (run is read below before being advanced)
+      (void)s;
+    }
+    __syncthreads();
+    uint64_t pos = 0;
+    if (valid) pos = run[d] + wc[warp][d] + rank;
+    __syncthreads();
+    if (valid) emit(i, pos);
+    // advance run[d] by this sub-tile's count of digit d: the last element of
+    // each digit group (highest warp, highest rank) knows the total.
+    if (valid && (peers >> lane) == 1u) {
+      // am I the last lane of my peer group in the highest warp holding d?
+      // total = wc[warp][d] + popc(peers) only if no later warp has digit d;
+      // resolved with an atomic max on the candidate end position instead.
+      atomicMax(reinterpret_cast<unsigned long long*>(&run[d]), (unsigned long long)(pos + 1));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void sort_scatter_kernel(DigitSrc D, int64_t n, const uint64_t* offs, int nblocks,
+                                    const uint64_t* kin, const uint32_t* vin, uint64_t* kout,
+                                    uint32_t* vout) {
+  scatter_chunk(D, n, kDigits, offs, nblocks, [&](int64_t i, uint64_t pos) {
+    kout[pos] = kin[i];
+    vout[pos] = vin[i];
+  });
+}
+
+__global__ void part_scatter_kernel(DigitSrc D, int64_t n, int nparts, const uint64_t* offs,
+                                    int nblocks, PartCols C) {
+  scatter_chunk(D, n, nparts, offs, nblocks, [&](int64_t i, uint64_t pos) {
+    for (int c = 0; c < C.n; ++c) {
+      const int w = dtype_size_d(C.in[c].dtype);
+      const char* s = reinterpret_cast<const char*>(C.in[c].ptr);
+      char* d = reinterpret_cast<char*>(C.out[c].ptr);
+      switch (w) {
+        case 1: d[pos] = s[i]; break;
+        case 2: reinterpret_cast<int16_t*>(d)[pos] = reinterpret_cast<const int16_t*>(s)[i]; break;
+        case 4: reinterpret_cast<int32_t*>(d)[pos] = reinterpret_cast<const int32_t*>(s)[i]; break;
+        default: reinterpret_cast<int64_t*>(d)[pos] = reinterpret_cast<const int64_t*>(s)[i]; break;
+      }
+    }
+  });
+}
+
+__global__ void part_counts_kernel(const uint64_t* offs, int nparts, int nblocks, uint64_t* counts) {
+  const int p = threadIdx.x;
+  if (p < nparts) counts[p] = offs[(int64_t)(p + 1) * nblocks] - offs[(int64_t)p * nblocks];
+}
+
+__global__ void hash_keys_kernel(PartKeys K, int64_t n, uint64_t* out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = fib_hash_row(K, i);
+}
+
+__global__ void copy_pairs_kernel(const uint64_t* ki, const uint32_t* vi, uint64_t* ko,
+                                  uint32_t* vo, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    ko[i] = ki[i];
+    vo[i] = vi[i];
+  }
+}
+
+static int64_t nblocks_for(int64_t n) { return (n + kChunk - 1) / kChunk; }
+
+// workspace: counts u32[ndig*nb] + offsets u64[ndig*nb + 1]
+static int64_t ws_bytes(int64_t n, int ndig) {
+  const int64_t nb = nblocks_for(n) > 0 ? nblocks_for(n) : 1;
+  const int64_t m = ndig * nb;
+  return ((m * 4 + 255) / 256) * 256 + (m + 1) * 8;
+}
+
+static int counting_pass(const DigitSrc& D, int64_t n, int ndig, void* temp, cudaStream_t st,
+                         const uint64_t*& offs_out, int& nb_out) {
+  const int64_t nb = nblocks_for(n);
+  if (nb * ndig > (1ll << 26)) { set_error("radix: input too large for single-CTA scan"); return SCX_EUNSUPPORTED; }
+  uint32_t* counts = static_cast<uint32_t*>(temp);
+  uint64_t* offs = reinterpret_cast<uint64_t*>(static_cast<char*>(temp) + ((nb * ndig * 4 + 255) / 256) * 256);
+  hist_kernel<<<(int)nb, kBlock, 0, st>>>(D, n, ndig, counts, (int)nb);
+  SCX_CHECK_LAUNCH("hist_kernel");
+  scan_kernel<<<1, 1024, 0, st>>>(counts, offs, nb * ndig);
+  SCX_CHECK_LAUNCH("scan_kernel");
+  offs_out = offs;
+  nb_out = (int)nb;
+  return SCX_OK;
+}
+
+}  // namespace scx
+
+using namespace scx;
+
+extern "C" int64_t scx_sort_workspace(int64_t n) { return ws_bytes(n, kDigits); }
+
+extern "C" int scx_sort_pairs(const uint64_t* kin, const uint32_t* vin, uint64_t* kout,
+                              uint32_t* vout, uint64_t* ktmp, uint32_t* vtmp, int64_t n,
+                              int n_bits, void* temp, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!kin || !vin || !kout || !vout || n_bits < 0 || n_bits > 64 ||
+      (n_bits > 8 && (!ktmp || !vtmp)) || !temp) {
+    set_error("sort_pairs: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const int passes = (n_bits + 7) / 8;
+  if (passes == 0) {
+    copy_pairs_kernel<<<grid_for(n, 256, 2368), 256, 0, st>>>(kin, vin, kout, vout, n);
+    SCX_CHECK_LAUNCH("copy_pairs_kernel");
+    return SCX_OK;
+  }
+  const uint64_t* ks = kin;
+  const uint32_t* vs = vin;
+  for (int p = 0; p < passes; ++p) {
+    // land the final pass in *_out
+    const bool to_out = ((passes - 1 - p) % 2) == 0;
+    uint64_t* kd = to_out ? kout : ktmp;
+    uint32_t* vd = to_out ? vout : vtmp;
+    DigitSrc D;
+    memset(&D, 0, sizeof(D));
+    D.keys = ks;
+    D.shift = 8 * p;
+    const uint64_t* offs;
+    int nb;
+    int rc = counting_pass(D, n, kDigits, temp, st, offs, nb);
+    if (rc) return rc;
+    sort_scatter_kernel<<<nb, kBlock, 0, st>>>(D, n, offs, nb, ks, vs, kd, vd);
+    SCX_CHECK_LAUNCH("sort_scatter_kernel");
+    ks = kd;
+    vs = vd;
+  }
+  return SCX_OK;
+}
+
+extern "C" int scx_hash_keys(const scx_column* keys, int n_keys, int64_t n, uint64_t* out,
+                             void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!keys || n_keys < 1 || n_keys > SCX_MAX_KEYS || !out) {
+    set_error("hash_keys: bad arguments");
+    return SCX_EINVAL;
+  }
+  PartKeys K;
+  memset(&K, 0, sizeof(K));
+  K.n = n_keys;
+  for (int i = 0; i < n_keys; ++i) K.k[i] = keys[i];
+  hash_keys_kernel<<<grid_for(n, 256, 2368), 256, 0, (cudaStream_t)stream>>>(K, n, out);
+  SCX_CHECK_LAUNCH("hash_keys_kernel");
+  return SCX_OK;
+}
+
+extern "C" int64_t scx_partition_workspace(int64_t n, int n_parts) { return ws_bytes(n, n_parts); }
+
+extern "C" int scx_partition(const scx_column* keys, int n_keys, const scx_column* cols,
+                             const scx_column* outs, int n_cols, int64_t n, int n_parts,
+                             uint64_t* counts, void* temp, void* stream) {
+  if (!keys || n_keys < 1 || n_keys > SCX_MAX_KEYS || n_cols < 0 || n_cols > SCX_MAX_OUT ||
+      n_parts < 1 || n_parts > kDigits || !counts || (n > 0 && !temp)) {
+    set_error("partition: bad arguments (keys=%d cols=%d parts=%d)", n_keys, n_cols, n_parts);
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {
+    SCX_CUDA(cudaMemsetAsync(counts, 0, 8 * n_parts, st));
+    return SCX_OK;
+  }
+  DigitSrc D;
+  memset(&D, 0, sizeof(D));
+  D.keys = nullptr;
+  D.nparts = (uint32_t)n_parts;
+  D.pk.n = n_keys;
+  for (int i = 0; i < n_keys; ++i) D.pk.k[i] = keys[i];
+  PartCols C;
+  memset(&C, 0, sizeof(C));
+  C.n = n_cols;
+  for (int i = 0; i < n_cols; ++i) {
+    C.in[i] = cols[i];
+    C.out[i] = outs[i];
+    if (dtype_size(cols[i].dtype) != dtype_size(outs[i].dtype)) {
+      set_error("partition: column %d in/out width mismatch", i);
+      return SCX_EINVAL;
+    }
+  }
+  const uint64_t* offs;
+  int nb;
+  int rc = counting_pass(D, n, n_parts, temp, st, offs, nb);
+  if (rc) return rc;
+  part_counts_kernel<<<1, kDigits, 0, st>>>(offs, n_parts, nb, counts);
+  SCX_CHECK_LAUNCH("part_counts_kernel");
+  if (n_cols > 0) {
+    part_scatter_kernel<<<nb, kBlock, 0, st>>>(D, n, n_parts, offs, nb, C);
+    SCX_CHECK_LAUNCH("part_scatter_kernel");
+  }
+  return SCX_OK;
+}

@@ -1,0 +1,341 @@
+// tables.cu -- lookup-table build (join build side), group-table compaction,
+// exact dense-aggregate reduction, key unpack, fixed-point -> f64, gather.
+//
+// Build side of local_hash_join (relops.py:81-84: the reference's stable
+// argsort + searchsorted becomes an open-addressing insert), the output
+// assembly of group_aggregate (relops.py:115-160) and Column.take
+// (table.py:76-77).
+#include "common.cuh"
+
+namespace scx {
+
+__global__ void lookup_clear_kernel(uint64_t* keys, uint32_t* vals, uint64_t cap) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    if (keys) keys[i] = SCX_EMPTY_KEY;
+    vals[i] = SCX_NO_ROW;
+  }
+}
+
+struct BuildCols {
+  scx_column c[SCX_MAX_KEYS];
+};
+
+__device__ __forceinline__ bool build_key(const BuildCols& C, const scx_keyspec& K, int64_t i,
+                                          uint64_t& out) {
+  uint64_t k = 0;
+  bool in = true;
+  for (int j = 0; j < K.n; ++j) {
+    const scx_column& col = C.c[K.slot[j]];
+    const uint64_t u = static_cast<uint64_t>(load_i64(reinterpret_cast<const void*>(col.ptr),
+                                                      col.dtype, i) - K.lo[j]);
+    if (K.bits[j] < 64 && (u >> K.bits[j]) != 0) in = false;
+    k |= u << K.shift[j];
+  }
+  out = k;
+  return in;
+}
+
+__global__ void lookup_build_kernel(scx_lookup T, BuildCols C, scx_keyspec K, int64_t n,
+                                    uint32_t* flags) {
+  uint32_t* vals = reinterpret_cast<uint32_t*>(T.vals);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t key;
+    if (!build_key(C, K, i, key)) { atomicOr(flags + 2, 1u); continue; }
+    if (T.kind == SCX_HT_DIRECT) {
+      if (key >= T.cap) { atomicOr(flags + 2, 1u); continue; }
+      const uint32_t prev = atomicExch(vals + key, (uint32_t)i);
+      if (prev != SCX_NO_ROW) atomicOr(flags + 1, 1u);
+    } else {
+      uint64_t* keys = reinterpret_cast<uint64_t*>(T.keys);
+      const uint64_t mask = T.cap - 1;
+      uint64_t h = mix64(key) & mask;
+      for (uint64_t p = 0; p <= mask; ++p) {
+        const unsigned long long prev =
+            atomicCAS(reinterpret_cast<unsigned long long*>(keys + h), SCX_EMPTY_KEY, key);
+        if (prev == SCX_EMPTY_KEY) { vals[h] = (uint32_t)i; break; }
+        if (prev == key) { atomicOr(flags + 1, 1u); break; }   // duplicate key
+        h = (h + 1) & mask;
+      }
+    }
+  }
+}
+
+// exact reduction of n_ranks partial {lo,hi} accumulators into 3 x 42-bit
+// signed limbs is unnecessary on one device: we emit {lo, hi} summed.
+__global__ void dense_reduce_kernel(const int64_t* acc, int n_ranks, int64_t words,
+                                    int64_t* out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= words / 2) return;
+  uint64_t lo = 0;
+  int64_t hi = 0;
+  for (int r = 0; r < n_ranks; ++r) {
+    const uint64_t l = (uint64_t)acc[r * words + 2 * i];
+    const int64_t h = acc[r * words + 2 * i + 1];
+    const uint64_t s = lo + l;
+    hi += h + (s < lo ? 1 : 0);
+    lo = s;
+  }
+  out[2 * i] = (int64_t)lo;
+  out[2 * i + 1] = hi;
+}
+
+__global__ void hash_agg_compact_kernel(const uint64_t* gkeys, const int64_t* acc, int64_t cap,
+                                        int m, uint64_t* out_keys, int64_t* out_acc,
+                                        unsigned long long* count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < cap;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = base + threadIdx.x;
+    const bool occ = i < cap && gkeys[i] != SCX_EMPTY_KEY;
+    const uint32_t b = __ballot_sync(0xffffffffu, occ);
+    unsigned long long wbase = 0;
+    if (lane == 0 && b) wbase = atomicAdd(count, (unsigned long long)__popc(b));
+    wbase = __shfl_sync(0xffffffffu, wbase, 0);
+    if (occ) {
+      const int64_t o = (int64_t)wbase + __popc(b & ((1u << lane) - 1u));
+      out_keys[o] = gkeys[i];
+      for (int j = 0; j < m; ++j) out_acc[j * cap + o] = acc[i * m + j];
+    }
+  }
+}
+
+__global__ void unpack_key_kernel(const uint64_t* packed, int64_t n, int shift, uint64_t mask,
+                                  int64_t lo, scx_column out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = (int64_t)((packed[i] >> shift) & mask) + lo;
+    store_i64(reinterpret_cast<void*>(out.ptr), out.dtype, i, v);
+  }
+}
+
+__device__ __forceinline__ double pow10d(int s) {
+  double p = 1.0;
+  for (int i = 0; i < s; ++i) p *= 10.0;
+  return p;
+}
+
+// exact integer -> correctly rounded double, then one correctly rounded
+// division by 10^scale (the numpy reference computes the same quotient
+// in float64 up to summation-order rounding).
+__global__ void fixed_to_f64_kernel(const int64_t* in, int64_t stride, int64_t n, int scale,
+                                    const int64_t* cnt, int64_t cstride, double* out) {
+  const double p = pow10d(scale);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double v = (double)in[i * stride];
+    v = scale ? v / p : v;
+    if (cnt) {
+      int64_t c = cnt[i * cstride];
+      v = v / (double)(c > 1 ? c : 1);
+    }
+    out[i] = v;
+  }
+}
+
+__global__ void gather_kernel(scx_column in, const uint32_t* idx, int64_t n, scx_column out) {
+  const int w = dtype_size_d(in.dtype);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx[i];
+    const char* s = reinterpret_cast<const char*>(in.ptr);
+    char* d = reinterpret_cast<char*>(out.ptr);
+    switch (w) {
+      case 1: d[i] = s[j]; break;
+      case 2: reinterpret_cast<int16_t*>(d)[i] = reinterpret_cast<const int16_t*>(s)[j]; break;
+      case 4: reinterpret_cast<int32_t*>(d)[i] = reinterpret_cast<const int32_t*>(s)[j]; break;
+      default: reinterpret_cast<int64_t*>(d)[i] = reinterpret_cast<const int64_t*>(s)[j]; break;
+    }
+  }
+}
+
+__global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t stride, int64_t v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i * stride] = v;
+}
+
+__global__ void iota_kernel(uint32_t* idx, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    idx[i] = (uint32_t)i;
+}
+
+// order-preserving key of one sort column (table.py:198-214).  F64 columns
+// map IEEE bits to a monotone u64; integers are offset by `lo`.
+__global__ void encode_sort_key_kernel(scx_column col, const uint32_t* idx, int64_t n,
+                                       int64_t lo, int n_bits, int desc, int shift,
+                                       const int32_t* lut, uint64_t* key, int accumulate) {
+  const uint64_t mask = n_bits >= 64 ? ~0ull : ((1ull << n_bits) - 1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = idx ? (int64_t)idx[i] : i;
+    uint64_t u;
+    if (col.dtype == SCX_F64) {   // n_bits == 64 enforced by the host entry
+      const uint64_t b = reinterpret_cast<const uint64_t*>(col.ptr)[j];
+      u = (b >> 63) ? ~b : (b | (1ull << 63));
+    } else {
+      int64_t v = load_i64(reinterpret_cast<const void*>(col.ptr), col.dtype, j) - lo;
+      if (lut) v = lut[v];
+      u = (uint64_t)v;
+    }
+    u &= mask;
+    if (desc) u = mask - u;
+    u <<= shift;
+    key[i] = accumulate ? (key[i] | u) : u;
+  }
+}
+
+__global__ void minmax_kernel(scx_column col, int64_t n, int64_t* out) {
+  int64_t mn = INT64_MAX, mx = INT64_MIN;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = load_i64(reinterpret_cast<const void*>(col.ptr), col.dtype, i);
+    mn = min(mn, v);
+    mx = max(mx, v);
+  }
+  mn = warp_min_i64(mn);
+  mx = warp_max_i64(mx);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(reinterpret_cast<long long*>(out), (long long)mn);
+    atomicMax(reinterpret_cast<long long*>(out + 1), (long long)mx);
+  }
+}
+
+}  // namespace scx
+
+using namespace scx;
+
+extern "C" int scx_minmax(scx_column col, int64_t n, int64_t* out, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!col.ptr || !out || col.dtype == SCX_F64) { set_error("minmax: bad arguments"); return SCX_EINVAL; }
+  minmax_kernel<<<grid_for(n, 256, 148 * 8), 256, 0, (cudaStream_t)stream>>>(col, n, out);
+  SCX_CHECK_LAUNCH("minmax_kernel");
+  return SCX_OK;
+}
+
+static int launch_grid(int64_t n) { return grid_for(n, 256, 148 * 16); }
+
+extern "C" int scx_lookup_clear(const scx_lookup* T, void* stream) {
+  if (!T || !T->vals || (T->kind == SCX_HT_HASH && (!T->keys || (T->cap & (T->cap - 1))))) {
+    set_error("lookup_clear: bad table (hash capacity must be a power of two)");
+    return SCX_EINVAL;
+  }
+  lookup_clear_kernel<<<launch_grid(T->cap), 256, 0, (cudaStream_t)stream>>>(
+      T->kind == SCX_HT_HASH ? reinterpret_cast<uint64_t*>(T->keys) : nullptr,
+      reinterpret_cast<uint32_t*>(T->vals), T->cap);
+  SCX_CHECK_LAUNCH("lookup_clear_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_lookup_build(const scx_lookup* T, const scx_column* cols, int n_cols,
+                                const scx_keyspec* K, int64_t n, uint32_t* flags,
+                                void* stream) {
+  if (!T || !cols || !K || !flags || n_cols < 1 || n_cols > SCX_MAX_KEYS || K->n < 1 ||
+      K->n > SCX_MAX_KEYS) {
+    set_error("lookup_build: bad arguments");
+    return SCX_EINVAL;
+  }
+  if (n > 0xFFFFFFFEll) { set_error("lookup_build: >2^32-2 build rows"); return SCX_EUNSUPPORTED; }
+  BuildCols C;
+  memset(&C, 0, sizeof(C));
+  for (int i = 0; i < n_cols; ++i) C.c[i] = cols[i];
+  for (int i = 0; i < K->n; ++i)
+    if (K->slot[i] < 0 || K->slot[i] >= n_cols) { set_error("lookup_build: key slot"); return SCX_EINVAL; }
+  if (n == 0) return SCX_OK;
+  lookup_build_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(*T, C, *K, n, flags);
+  SCX_CHECK_LAUNCH("lookup_build_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_dense_reduce(const int64_t* acc, int n_ranks, int cells, int m, int64_t* out,
+                                void* stream) {
+  if (!acc || !out || n_ranks < 1 || cells < 1 || m < 1) {
+    set_error("dense_reduce: bad arguments");
+    return SCX_EINVAL;
+  }
+  const int64_t words = 2ll * cells * m;
+  dense_reduce_kernel<<<(int)((words / 2 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      acc, n_ranks, words, out);
+  SCX_CHECK_LAUNCH("dense_reduce_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_hash_agg_compact(const uint64_t* gkeys, const int64_t* acc, int64_t cap, int m,
+                                    uint64_t* out_keys, int64_t* out_acc, uint64_t* count,
+                                    void* stream) {
+  if (!gkeys || !out_keys || !count || (m > 0 && (!acc || !out_acc))) {
+    set_error("hash_agg_compact: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
+  if (cap == 0) return SCX_OK;
+  hash_agg_compact_kernel<<<launch_grid(cap), 256, 0, st>>>(
+      gkeys, acc, cap, m, out_keys, out_acc, reinterpret_cast<unsigned long long*>(count));
+  SCX_CHECK_LAUNCH("hash_agg_compact_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_unpack_key(const uint64_t* packed, int64_t n, int shift, uint64_t mask,
+                              int64_t lo, scx_column out, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!packed || !out.ptr || shift < 0 || shift > 63) { set_error("unpack_key: bad arguments"); return SCX_EINVAL; }
+  unpack_key_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(packed, n, shift, mask, lo, out);
+  SCX_CHECK_LAUNCH("unpack_key_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_fixed_to_f64(const int64_t* in, int64_t stride, int64_t n, int scale,
+                                const int64_t* cnt, int64_t cstride, double* out, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!in || !out || scale < 0 || scale > 18) { set_error("fixed_to_f64: bad arguments"); return SCX_EINVAL; }
+  fixed_to_f64_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(in, stride, n, scale, cnt,
+                                                                       cstride, out);
+  SCX_CHECK_LAUNCH("fixed_to_f64_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_gather(scx_column in, const uint32_t* idx, int64_t n, scx_column out,
+                          void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!in.ptr || !out.ptr || !idx || dtype_size(in.dtype) != dtype_size(out.dtype)) {
+    set_error("gather: bad arguments");
+    return SCX_EINVAL;
+  }
+  gather_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(in, idx, n, out);
+  SCX_CHECK_LAUNCH("gather_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_fill_i64(int64_t* p, int64_t n, int64_t stride, int64_t value, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!p || stride < 1) { set_error("fill_i64: bad arguments"); return SCX_EINVAL; }
+  fill_i64_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(p, n, stride, value);
+  SCX_CHECK_LAUNCH("fill_i64_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_iota(uint32_t* idx, int64_t n, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!idx) { set_error("iota: null"); return SCX_EINVAL; }
+  iota_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(idx, n);
+  SCX_CHECK_LAUNCH("iota_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_encode_sort_key(scx_column col, const uint32_t* idx, int64_t n, int64_t lo,
+                                   int n_bits, int descending, int shift, const int32_t* lut,
+                                   uint64_t* key, int accumulate, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!col.ptr || !key || n_bits < 1 || n_bits > 64 || shift < 0 || shift + n_bits > 64 ||
+      (col.dtype == SCX_F64 && n_bits != 64)) {
+    set_error("encode_sort_key: bad arguments (bits=%d shift=%d)", n_bits, shift);
+    return SCX_EINVAL;
+  }
+  encode_sort_key_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(
+      col, idx, n, lo, n_bits, descending, shift, lut, key, accumulate);
+  SCX_CHECK_LAUNCH("encode_sort_key_kernel");
+  return SCX_OK;
+}

@@ -1,0 +1,320 @@
+"""Seeded TPC-H-shaped data, generated straight into the narrowed HBM layout.
+
+Restates the reference generator ``shufflecast.data.generate``
+(`/root/reference/pkg/src/shufflecast/data.py:161-268`) value-for-value:
+the same ``numpy.random.default_rng(seed)`` stream is consumed by the same
+draws in the same order (orders -> lineitem -> customer -> part -> partsupp
+-> supplier), so every logical value is identical to
+the reference's.  What differs is the *storage*: each draw is narrowed as
+soon as it is produced (int64 draws to int8/int16/int32, decimals to
+fixed-point integers, dates to int16 days, dictionary codes to uint8), so
+SF100 lineitem is ~25 B/row (15 GB) instead of the reference's 76 B/row and
+the host never holds the wide copy.  ``Dataset.to_reference()`` widens back
+to the reference dtypes for the oracle (tests only).
+
+Also carries ``partition_dataset`` (`data.py:284-302`), whose
+``default_keys`` scheme runs on the GPU through the partition kernel
+(see ``exchange.hash_partition``) when tables are device resident; the host
+variant here only computes row-index lists via the same Fibonacci hash.
+"""
+
+from __future__ import annotations
+
+import itertools
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .table import HostColumn, HostTable, date_to_days, narrow_host
+
+PARTITION_SCHEMES = ("default_keys", "unpartitioned", "round_robin")
+
+# data.py:47-56 -- conventional partition key per table
+DEFAULT_PARTITION_KEYS = {
+    "lineitem": "l_orderkey",
+    "orders": "o_orderkey",
+    "customer": "c_custkey",
+    "part": "p_partkey",
+    "partsupp": "ps_partkey",
+    "supplier": "s_suppkey",
+    "nation": "n_nationkey",
+    "region": "r_regionkey",
+}
+
+# Canonical dictionaries (data.py:58-82); shared by every table/partition.
+RETURN_FLAGS = ("R", "A", "N")
+LINE_STATUSES = ("O", "F")
+SHIP_INSTRUCTS = ("DELIVER IN PERSON", "COLLECT COD", "NONE", "TAKE BACK RETURN")
+SHIP_MODES = ("REG AIR", "AIR", "RAIL", "SHIP", "TRUCK", "MAIL", "FOB")
+ORDER_PRIORITIES = ("1-URGENT", "2-HIGH", "3-MEDIUM", "4-NOT SPECIFIED", "5-LOW")
+MARKET_SEGMENTS = ("AUTOMOBILE", "BUILDING", "FURNITURE", "MACHINERY", "HOUSEHOLD")
+BRANDS = tuple(f"Brand#{a}{b}" for a in range(1, 6) for b in range(1, 6))
+TYPES = tuple(" ".join(w) for w in itertools.product(
+    ("STANDARD", "SMALL", "MEDIUM", "LARGE", "ECONOMY", "PROMO"),
+    ("ANODIZED", "BURNISHED", "PLATED", "POLISHED", "BRUSHED"),
+    ("TIN", "NICKEL", "BRASS", "STEEL", "COPPER"),
+))
+CONTAINERS = tuple(" ".join(w) for w in itertools.product(
+    ("SM", "MED", "LG", "JUMBO", "WRAP"),
+    ("CASE", "BOX", "BAG", "JAR", "PKG", "PACK", "CAN", "DRUM"),
+))
+NATION_NAMES = tuple(f"NATION_{i:02d}" for i in range(25))
+REGION_NAMES = ("AFRICA", "AMERICA", "ASIA", "EUROPE", "MIDDLE EAST")
+
+# Logical schema per table (data.py:84-105): (column, reference kind).
+SCHEMAS: dict[str, list[tuple[str, str]]] = {
+    "lineitem": [
+        ("l_orderkey", "int64"), ("l_partkey", "int64"), ("l_quantity", "int64"),
+        ("l_extendedprice", "float64"), ("l_discount", "float64"), ("l_tax", "float64"),
+        ("l_returnflag", "dict"), ("l_linestatus", "dict"),
+        ("l_shipdate", "date32"), ("l_commitdate", "date32"), ("l_receiptdate", "date32"),
+        ("l_shipinstruct", "dict"), ("l_shipmode", "dict"),
+    ],
+    "orders": [
+        ("o_orderkey", "int64"), ("o_custkey", "int64"), ("o_orderdate", "date32"),
+        ("o_orderpriority", "dict"), ("o_shippriority", "int64"),
+    ],
+    "customer": [("c_custkey", "int64"), ("c_mktsegment", "dict"), ("c_nationkey", "int64")],
+    "part": [
+        ("p_partkey", "int64"), ("p_brand", "dict"), ("p_type", "dict"),
+        ("p_size", "int64"), ("p_container", "dict"),
+    ],
+    "partsupp": [("ps_partkey", "int64"), ("ps_suppkey", "int64"), ("ps_supplycost", "float64")],
+    "supplier": [("s_suppkey", "int64"), ("s_nationkey", "int64")],
+    "nation": [("n_nationkey", "int64"), ("n_name", "dict"), ("n_regionkey", "int64")],
+    "region": [("r_regionkey", "int64"), ("r_name", "dict")],
+}
+
+DICTIONARIES: dict[str, tuple[str, ...]] = {
+    "l_returnflag": RETURN_FLAGS, "l_linestatus": LINE_STATUSES,
+    "l_shipinstruct": SHIP_INSTRUCTS, "l_shipmode": SHIP_MODES,
+    "o_orderpriority": ORDER_PRIORITIES, "c_mktsegment": MARKET_SEGMENTS,
+    "p_brand": BRANDS, "p_type": TYPES, "p_container": CONTAINERS,
+    "n_name": NATION_NAMES, "r_name": REGION_NAMES,
+}
+
+_ORDERDATE_LO = date_to_days("1992-01-01")
+_ORDERDATE_HI = date_to_days("1998-08-02")
+_LINESTATUS_CUTOFF = date_to_days("1995-06-17")
+
+
+class DataError(ValueError):
+    """Bad generator / partitioning arguments (data.py:126)."""
+
+
+@dataclass
+class Dataset:
+    """Host-resident narrowed tables plus the knobs that produced them."""
+
+    tables: dict[str, HostTable]
+    sf: float | None = None
+    skew: float = 0.0
+    seed: int | None = None
+
+    def table(self, name: str) -> HostTable:
+        return self.tables[name]
+
+    def row_counts(self) -> dict[str, int]:
+        return {n: t.row_count for n, t in self.tables.items()}
+
+    def manifest(self) -> dict:
+        return {"sf": self.sf, "skew": self.skew, "seed": self.seed,
+                "row_counts": self.row_counts()}
+
+    @property
+    def nbytes(self) -> int:
+        return sum(t.nbytes for t in self.tables.values())
+
+    def to_reference(self) -> dict[str, dict[str, tuple]]:
+        """Widen to the reference's dtypes: {table: {col: (kind, values, dict)}}.
+
+        Test/oracle use only -- the product never widens.
+        """
+        return {n: t.to_reference() for n, t in self.tables.items()}
+
+
+def _zipf(rng: np.random.Generator, n_items: int, s: float, size: int) -> np.ndarray:
+    # Same draw as data.py:154-158 (rank 1 hottest, keys 1..n_items).
+    w = np.arange(1, n_items + 1, dtype=np.float64) ** (-s)
+    w /= w.sum()
+    return rng.choice(n_items, size=size, p=w).astype(np.int64) + 1
+
+
+def _dict(codes: np.ndarray, name: str) -> HostColumn:
+    return HostColumn.from_codes(codes, DICTIONARIES[name])
+
+
+def generate(sf: float, skew: float = 0.0, seed: int = 0) -> Dataset:
+    """Deterministic dataset for (sf, skew, seed); values identical to data.py:161."""
+    if sf <= 0:
+        raise DataError(f"scale factor must be positive, got {sf}")
+    if skew < 0:
+        raise DataError(f"skew exponent must be >= 0, got {skew}")
+    rng = np.random.default_rng(seed)
+    n_ord = max(1, round(1_500_000 * sf))
+    n_cust = max(1, round(150_000 * sf))
+    n_part = max(1, round(200_000 * sf))
+    n_supp = max(1, round(10_000 * sf))
+    i64 = np.int64
+
+    # ---- orders: custkey, orderdate, priority -------------------------------
+    if skew > 0:
+        o_cust = _zipf(rng, n_cust, skew, n_ord)
+    else:
+        o_cust = rng.integers(1, n_cust + 1, size=n_ord, dtype=i64)
+    o_date = narrow_host(rng.integers(_ORDERDATE_LO, _ORDERDATE_HI + 1, size=n_ord, dtype=i64))
+    o_prio = rng.integers(0, len(ORDER_PRIORITIES), size=n_ord)
+    orders = HostTable({
+        "o_orderkey": HostColumn.int_range(1, n_ord + 1),
+        "o_custkey": HostColumn.from_ints("int64", o_cust),
+        "o_orderdate": HostColumn.from_ints("date32", o_date),
+        "o_orderpriority": _dict(o_prio, "o_orderpriority"),
+        "o_shippriority": HostColumn.from_ints("int64", np.zeros(n_ord, dtype=np.int8)),
+    })
+    del o_cust, o_prio
+
+    # ---- lineitem ----------------------------------------------------------
+    if skew > 0:
+        n_li = max(1, round(6_000_000 * sf))
+        l_ok = np.sort(_zipf(rng, n_ord, skew, n_li))
+    else:
+        lines_per_order = rng.integers(1, 8, size=n_ord, dtype=i64)
+        l_ok = np.repeat(np.arange(1, n_ord + 1, dtype=i64), lines_per_order)
+        n_li = len(l_ok)
+        del lines_per_order
+    if skew > 0:
+        l_pk = _zipf(rng, n_part, skew, n_li)
+    else:
+        l_pk = rng.integers(1, n_part + 1, size=n_li, dtype=i64)
+    qty = narrow_host(rng.integers(1, 51, size=n_li, dtype=i64))
+    # extendedprice = qty * (900 + partkey % 1000): integral dollars -> cents
+    ext_cents = (qty.astype(np.int32) * (900 + (l_pk % 1000)).astype(np.int32)) * np.int32(100)
+    odate = o_date[(l_ok - 1)]
+    ship = narrow_host(odate.astype(np.int32) + rng.integers(1, 122, size=n_li).astype(np.int32))
+    commit = narrow_host(odate.astype(np.int32) + rng.integers(30, 91, size=n_li).astype(np.int32))
+    del odate
+    receipt = narrow_host(ship.astype(np.int32) + rng.integers(1, 31, size=n_li).astype(np.int32))
+    disc = narrow_host(rng.integers(0, 11, size=n_li))
+    tax = narrow_host(rng.integers(0, 9, size=n_li))
+    rflag = rng.integers(0, len(RETURN_FLAGS), size=n_li)
+    lineitem_cols = {
+        "l_orderkey": HostColumn.from_ints("int64", l_ok),
+        "l_partkey": HostColumn.from_ints("int64", l_pk),
+        "l_quantity": HostColumn.from_ints("int64", qty),
+        "l_extendedprice": HostColumn.decimal(ext_cents, 2),
+        "l_discount": HostColumn.decimal(disc, 2),
+        "l_tax": HostColumn.decimal(tax, 2),
+        "l_returnflag": _dict(rflag, "l_returnflag"),
+        "l_linestatus": _dict((ship <= _LINESTATUS_CUTOFF).astype(np.uint8), "l_linestatus"),
+        "l_shipdate": HostColumn.from_ints("date32", ship),
+        "l_commitdate": HostColumn.from_ints("date32", commit),
+        "l_receiptdate": HostColumn.from_ints("date32", receipt),
+    }
+    del l_ok, l_pk, rflag
+    lineitem_cols["l_shipinstruct"] = _dict(
+        rng.integers(0, len(SHIP_INSTRUCTS), size=n_li), "l_shipinstruct")
+    lineitem_cols["l_shipmode"] = _dict(
+        rng.integers(0, len(SHIP_MODES), size=n_li), "l_shipmode")
+    lineitem = HostTable(lineitem_cols)
+
+    # ---- customer, part, partsupp, supplier -------------------------------
+    customer = HostTable({
+        "c_custkey": HostColumn.int_range(1, n_cust + 1),
+        "c_mktsegment": _dict(rng.integers(0, len(MARKET_SEGMENTS), size=n_cust), "c_mktsegment"),
+        "c_nationkey": HostColumn.from_ints("int64", rng.integers(0, 25, size=n_cust)),
+    })
+    part = HostTable({
+        "p_partkey": HostColumn.int_range(1, n_part + 1),
+        "p_brand": _dict(rng.integers(0, len(BRANDS), size=n_part), "p_brand"),
+        "p_type": _dict(rng.integers(0, len(TYPES), size=n_part), "p_type"),
+        "p_size": HostColumn.from_ints("int64", rng.integers(1, 51, size=n_part)),
+        "p_container": _dict(rng.integers(0, len(CONTAINERS), size=n_part), "p_container"),
+    })
+    ps_supp = rng.integers(1, n_supp + 1, size=4 * n_part)
+    ps_cost = rng.uniform(1.0, 1000.0, size=4 * n_part).round(2)
+    partsupp = HostTable({
+        "ps_partkey": HostColumn.from_ints(
+            "int64", np.repeat(np.arange(1, n_part + 1, dtype=np.int64), 4)),
+        "ps_suppkey": HostColumn.from_ints("int64", ps_supp),
+        "ps_supplycost": HostColumn.from_float(ps_cost),
+    })
+    supplier = HostTable({
+        "s_suppkey": HostColumn.int_range(1, n_supp + 1),
+        "s_nationkey": HostColumn.from_ints("int64", rng.integers(0, 25, size=n_supp)),
+    })
+    nation = HostTable({
+        "n_nationkey": HostColumn.int_range(0, 25),
+        "n_name": _dict(np.arange(25), "n_name"),
+        "n_regionkey": HostColumn.from_ints("int64", np.arange(25) % 5),
+    })
+    region = HostTable({
+        "r_regionkey": HostColumn.int_range(0, 5),
+        "r_name": _dict(np.arange(5), "r_name"),
+    })
+    return Dataset(
+        tables={"lineitem": lineitem, "orders": orders, "customer": customer,
+                "part": part, "partsupp": partsupp, "supplier": supplier,
+                "nation": nation, "region": region},
+        sf=sf, skew=skew, seed=seed,
+    )
+
+
+# ---------------------------------------------------------------------------
+# host-side partition assignment (the GPU path lives in exchange.py)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class PartitionedDataset:
+    """Per-worker table sets produced by one partitioning scheme (data.py:271-281)."""
+
+    scheme: str
+    n_workers: int
+    workers: list[dict] = field(default_factory=list)
+    source: Dataset | None = None
+
+    def worker_tables(self, rank: int) -> dict:
+        return self.workers[rank]
+
+
+def fib_hash_host(keys: np.ndarray) -> np.ndarray:
+    """Single-key Fibonacci hash, u64 wraparound (exchange.py:29-49).
+
+    Host helper for metadata-scale work and for checking; bulk hashing runs
+    in the ``scx_hash_partition`` kernel.
+    """
+    f = np.uint64(0x9E3779B97F4A7C15)
+    with np.errstate(over="ignore"):
+        return (keys.astype(np.int64).astype(np.uint64) * f) * f
+
+
+def partition_rows(table: HostTable, scheme: str, key: str | None, n: int) -> list[np.ndarray]:
+    """Row indices per worker for ``scheme`` (data.py:284-302), input order kept."""
+    rows = table.row_count
+    if scheme == "default_keys":
+        b = fib_hash_host(table.column(key).to_int64()) % np.uint64(n)
+        order = np.argsort(b, kind="stable")
+        cuts = np.searchsorted(b[order], np.arange(n + 1, dtype=np.uint64))
+        return [order[cuts[i]:cuts[i + 1]] for i in range(n)]
+    if scheme == "unpartitioned":
+        cuts = np.linspace(0, rows, n + 1).astype(np.int64)
+        return [np.arange(cuts[i], cuts[i + 1]) for i in range(n)]
+    idx = np.arange(rows)
+    return [idx[idx % n == r] for r in range(n)]
+
+
+def partition_dataset(ds: Dataset, n_workers: int, scheme: str = "default_keys") -> PartitionedDataset:
+    """Host-side partitioning of a narrowed dataset (data.py:284).
+
+    Used for small host datasets and by tests; ``engine.load_partition`` does
+    the same assignment on the GPU for the bench path.
+    """
+    if n_workers < 1:
+        raise DataError(f"need at least one worker, got {n_workers}")
+    if scheme not in PARTITION_SCHEMES:
+        raise DataError(f"unknown partitioning scheme {scheme!r}; choose from {PARTITION_SCHEMES}")
+    workers: list[dict] = [{} for _ in range(n_workers)]
+    for name, t in ds.tables.items():
+        parts = partition_rows(t, scheme, DEFAULT_PARTITION_KEYS[name], n_workers)
+        for r in range(n_workers):
+            workers[r][name] = t.take(parts[r])
+    return PartitionedDataset(scheme, n_workers, workers, ds)

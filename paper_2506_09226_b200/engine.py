@@ -1,0 +1,357 @@
+"""SPMD executor over HBM-resident partitions: context, plans, reports.
+
+Drop-in for ``shufflecast.engine`` (`/root/reference/pkg/src/shufflecast/
+engine.py`): the exchange-plan registry (41-133), ``RunReport`` (144-179),
+``result_digest`` (182-197), the driver-facing context protocol
+(``LocalContext``/``WorkerContext``, 221-365), ``run_query`` (382-460) and
+``reference_run`` (463-469).
+
+Differences by design: a worker is a *process* owning one GPU (not a
+thread), tables live in HBM, relational operators are fused kernels, and
+exchanges are NCCL collectives.  Timing follows the reference's barrier
+method (engine.py:318-340): every exchange is bracketed by a device-drained
+barrier, compute is the remainder.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import exchange as X
+from . import relops as R
+from .cluster import Endpoint, barrier, create_cluster
+from .data import DEFAULT_PARTITION_KEYS, Dataset, PARTITION_SCHEMES, DataError
+from .table import Column, ColumnTable, concat_tables
+
+
+class PlanError(ValueError):
+    """Unsupported query/variant or a plan-vs-partitioning mismatch (engine.py:37)."""
+
+
+@dataclass(frozen=True)
+class ExchangePlan:
+    """Declarative plan shape (engine.py:41-72)."""
+
+    query_id: str
+    variant: str
+    steps: tuple[str, ...]
+    expected_exchanges: tuple[int, int]
+    requires_co_partition: tuple[tuple[str, str], ...] = ()
+
+    def validate(self) -> None:
+        if self.steps.count("final_gather") != 1 or self.steps[-1] != "final_gather":
+            raise PlanError(f"{self.query_id}/{self.variant}: need exactly one final_gather, last")
+        for step in self.steps:
+            if step.startswith("local_hash_join:"):
+                prep = step.split(":", 1)[1]
+                if prep not in ("co_partitioned", "shuffle", "broadcast"):
+                    raise PlanError(f"{self.query_id}: join without a valid alignment: {prep}")
+                if prep == "co_partitioned" and not self.requires_co_partition:
+                    raise PlanError(f"{self.query_id}/{self.variant}: co-partitioned join must "
+                                    "state its partitioning requirement")
+
+
+EXCHANGE_PLANS: dict[tuple[str, str], ExchangePlan] = {}
+
+_CO_LO = (("lineitem", "l_orderkey"), ("orders", "o_orderkey"))
+
+
+def _register(qid, variant, steps, expected, co=()):
+    p = ExchangePlan(qid, variant, tuple(steps), expected, tuple(co))
+    p.validate()
+    EXCHANGE_PLANS[(qid, variant)] = p
+
+
+# engine.py:83-133 (same shapes and Table-4 counts)
+_register("Q1", "default", ["scan:lineitem", "filter", "group_aggregate", "final_gather"], (0, 0))
+_register("Q3", "default", ["scan:customer", "filter", "broadcast:customer", "scan:orders",
+                            "filter", "local_hash_join:broadcast", "scan:lineitem", "filter",
+                            "local_hash_join:co_partitioned", "group_aggregate", "final_gather"],
+          (0, 1), _CO_LO)
+_register("Q6", "default", ["scan:lineitem", "filter", "group_aggregate", "final_gather"], (0, 0))
+_register("Q12", "default", ["scan:lineitem", "filter", "scan:orders",
+                             "local_hash_join:co_partitioned", "group_aggregate", "final_gather"],
+          (0, 0), _CO_LO)
+_register("Q12", "pa", ["scan:lineitem", "filter", "shuffle:l_orderkey", "scan:orders",
+                        "shuffle:o_orderkey", "local_hash_join:shuffle", "group_aggregate",
+                        "final_gather"], (2, 0))
+_register("Q12", "pb", ["scan:lineitem", "filter", "broadcast:lineitem", "scan:orders",
+                        "local_hash_join:broadcast", "group_aggregate", "final_gather"], (0, 1))
+_register("Q14", "default", ["scan:lineitem", "filter", "shuffle:l_partkey", "scan:part",
+                             "local_hash_join:shuffle", "group_aggregate", "final_gather"],
+          (1, 0), (("part", "p_partkey"),))
+_register("Q19", "default", ["scan:part", "filter", "broadcast:part", "scan:lineitem", "filter",
+                             "local_hash_join:broadcast", "filter", "group_aggregate",
+                             "final_gather"], (0, 1))
+
+
+def get_plan(qid: str, variant: str) -> ExchangePlan:
+    plan = EXCHANGE_PLANS.get((qid, variant))
+    if plan is None:
+        known = sorted({q for q, _ in EXCHANGE_PLANS})
+        raise PlanError(f"no plan for query {qid!r} variant {variant!r}; queries: {known}")
+    return plan
+
+
+@dataclass
+class RunReport:
+    """Per-query instrumentation (engine.py:144-179), device-timed."""
+
+    query_id: str
+    variant: str
+    mode: str
+    compute_s: float
+    shuffle_s: float
+    broadcast_s: float
+    shuffle_msgs: list[int]
+    broadcast_msgs: list[int]
+    peak_bytes: list[int]
+    result_digest: str
+    exchange_counts: tuple[int, int]
+    shuffle_bytes: int = 0
+    broadcast_bytes: int = 0
+
+    @property
+    def total_s(self) -> float:
+        return self.compute_s + self.shuffle_s + self.broadcast_s
+
+    def to_json(self) -> str:
+        return json.dumps({
+            "compute_s": self.compute_s, "shuffle_s": self.shuffle_s,
+            "broadcast_s": self.broadcast_s, "shuffle_msgs": self.shuffle_msgs,
+            "broadcast_msgs": self.broadcast_msgs, "peak_bytes": self.peak_bytes,
+            "result_digest": self.result_digest, "exchange_counts": list(self.exchange_counts),
+        }, indent=2)
+
+
+def result_digest(table) -> str:
+    """Order-insensitive sha256 of result rows, floats at 9 significant digits
+    (engine.py:182-197).  Not N-stable for float queries."""
+    if table is None:
+        return "empty"
+    table = table.materialize()
+    decoded = [table.column(n).decoded() for n in table.column_names]
+    kinds = [table.column(n).kind for n in table.column_names]
+    lines = []
+    for i in range(table.row_count):
+        lines.append("|".join(f"{col[i]:.9e}" if k == "float64" else str(col[i])
+                              for col, k in zip(decoded, kinds)))
+    lines.sort()
+    payload = "\n".join([",".join(table.column_names)] + lines)
+    return hashlib.sha256(payload.encode()).hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# the context protocol used by query drivers
+# ---------------------------------------------------------------------------
+
+class DeviceContext:
+    """One rank's view: its HBM partition, fused relops, NCCL exchanges.
+
+    With ``ep.n == 1`` exchanges are the identity, which makes this the
+    single-context execution (``LocalContext``, engine.py:221-258) as well.
+    """
+
+    def __init__(self, ep: Endpoint, tables: dict[str, ColumnTable], variant: str = "default",
+                 scheme: str = "default_keys", p2p_broadcast: bool = False,
+                 timed: bool = True):
+        self.ep = ep
+        self.tables = tables
+        self.variant = variant
+        self.scheme = scheme
+        self.p2p_broadcast = p2p_broadcast
+        self.timed = timed
+        self.shuffle_s = 0.0
+        self.broadcast_s = 0.0
+        self.shuffle_msgs: list[int] = []
+        self.broadcast_msgs: list[int] = []
+        self.shuffle_bytes = 0
+        self.broadcast_bytes = 0
+        self.n_shuffles = 0
+        self.n_broadcasts = 0
+
+    @property
+    def is_root(self) -> bool:
+        return self.ep.rank == 0
+
+    def table(self, name: str) -> ColumnTable:
+        return self.tables[name]
+
+    def filter(self, t, mask):
+        return R.filter_table(t, mask)
+
+    def join(self, left, right, on, how="inner"):
+        return R.local_hash_join(left, right, on, how)
+
+    def group(self, t, keys, aggs):
+        return R.group_aggregate(t, keys, aggs)
+
+    def add_column(self, t, name, col):
+        return R.as_view(t).with_column(name, col)
+
+    def require_co_partitioned(self, *tables) -> None:
+        if self.ep.n > 1 and self.scheme != "default_keys":
+            raise PlanError(f"plan needs co-partitioned {tables}, but data is partitioned "
+                            f"as {self.scheme!r}")
+
+    def _bracket(self):
+        if self.timed:
+            barrier(self.ep)
+        return time.perf_counter()
+
+    def shuffle(self, t, keys):
+        t0 = self._bracket()
+        stats = X.ExchangeStats()
+        out = X.shuffle_table(self.ep, t, keys, stats) if self.ep.n > 1 else t
+        self.shuffle_s += self._bracket() - t0
+        self.shuffle_msgs.extend(stats.messages)
+        self.shuffle_bytes += stats.table_bytes
+        self.n_shuffles += 1
+        return out
+
+    def broadcast(self, t):
+        t0 = self._bracket()
+        stats = X.ExchangeStats()
+        out = (X.broadcast_table(self.ep, t, stats, use_p2p=self.p2p_broadcast)
+               if self.ep.n > 1 else t)
+        self.broadcast_s += self._bracket() - t0
+        self.broadcast_msgs.extend(stats.messages)
+        self.broadcast_bytes += stats.table_bytes
+        self.n_broadcasts += 1
+        return out
+
+    def global_group(self, t, keys, aggs):
+        """Group + exact cross-rank final aggregation; result on the root.
+
+        The reference does this with a float64 ``all_reduce_sum`` of the
+        numpy grid (queries.py:51-54, 116); here the per-rank partials are
+        exact 128-bit integers and are summed exactly (all-gather + exact
+        fold), so the result is rank-count independent.
+        """
+        g = R.group_aggregate(t, keys, aggs, cross=self)
+        return g if self.is_root else None
+
+    def all_reduce_sum(self, vec) -> np.ndarray:
+        v = np.asarray(vec, dtype=np.float64)
+        if self.ep.n == 1:
+            return v
+        import torch
+        import torch.distributed as dist
+        t = torch.from_numpy(v.copy()).to(self.ep.device)
+        parts = X.all_gather_tensor(self.ep, t).cpu().numpy()
+        acc = parts[0].copy()
+        for p in parts[1:]:   # rank-order fold (collectives.py:198-206)
+            acc += p
+        return acc
+
+    def gather(self, t):
+        """Partials to rank 0, rank order (engine.py:345-365)."""
+        t = t.materialize()
+        if self.ep.n == 1:
+            return t
+        import torch.distributed as dist
+        names = t.column_names
+        counts, _ = X.size_exchange(self.ep, np.full(self.ep.n, t.row_count, dtype=np.int64))
+        parts = [t] if self.is_root else []
+        if self.is_root:
+            for src in range(1, self.ep.n):
+                cols = {}
+                for name in names:
+                    ref = t.column(name)
+                    buf = R.alloc(int(counts[src]), ref.np_dtype)
+                    if counts[src]:
+                        dist.recv(buf, src=src)
+                    cols[name] = ref.like(buf)
+                parts.append(ColumnTable(cols))
+            return concat_tables(parts)
+        for name in names:
+            if t.row_count:
+                dist.send(t.column(name).data.contiguous(), dst=0)
+        return None
+
+
+# ---------------------------------------------------------------------------
+# data placement
+# ---------------------------------------------------------------------------
+
+def load_tables(ds: Dataset, ep: Endpoint | None = None, scheme: str = "default_keys",
+                names=None) -> dict[str, ColumnTable]:
+    """Upload a dataset and keep this rank's partition in HBM.
+
+    ``default_keys`` partitions on the GPU with the same kernel the shuffle
+    uses (data.py:284-302 semantics); ``unpartitioned`` / ``round_robin`` use
+    host row ranges.
+    """
+    from .data import partition_rows
+    ep = ep or Endpoint(0, 1, "nccl")
+    if scheme not in PARTITION_SCHEMES:
+        raise DataError(f"unknown partitioning scheme {scheme!r}; choose from {PARTITION_SCHEMES}")
+    out = {}
+    for name, ht in ds.tables.items():
+        if names is not None and name not in names:
+            continue
+        if ep.n == 1:
+            out[name] = ht.to_device()
+        elif scheme == "default_keys":
+            dev = ht.to_device()
+            out[name] = X.hash_partition(dev, [DEFAULT_PARTITION_KEYS[name]], ep.n)[ep.rank]
+            del dev
+        else:
+            rows = partition_rows(ht, scheme, None, ep.n)[ep.rank]
+            out[name] = ht.take(rows).to_device()
+    return out
+
+
+def run_query(qid: str, variant: str = "default", ep: Endpoint | None = None,
+              tables: dict[str, ColumnTable] | None = None, scheme: str = "default_keys",
+              p2p_broadcast: bool = False):
+    """Execute one query on this rank's partition; (result on root | None, RunReport)."""
+    from .queries import PLAN_FUNCTIONS
+    import torch
+    plan = get_plan(qid, variant)
+    ep = ep or Endpoint(0, 1, "nccl")
+    if plan.requires_co_partition and scheme != "default_keys" and ep.n > 1:
+        needs = ", ".join(f"{t} on {k}" for t, k in plan.requires_co_partition)
+        raise PlanError(f"{qid}/{variant} requires co-partitioned inputs ({needs}); "
+                        f"got scheme {scheme!r}")
+    ctx = DeviceContext(ep, tables, variant, scheme, p2p_broadcast)
+    torch.cuda.reset_peak_memory_stats()
+    barrier(ep)
+    t0 = time.perf_counter()
+    result = PLAN_FUNCTIONS[qid](ctx)
+    if result is not None:
+        result = result.materialize()
+    barrier(ep)
+    total = time.perf_counter() - t0
+    counts = (ctx.n_shuffles, ctx.n_broadcasts)
+    if counts != plan.expected_exchanges:
+        raise PlanError(f"{qid}/{variant}: plan declares exchanges {plan.expected_exchanges}, "
+                        f"run produced {counts}")
+    report = RunReport(
+        query_id=qid, variant=variant, mode=ep.backend,
+        compute_s=total - ctx.shuffle_s - ctx.broadcast_s, shuffle_s=ctx.shuffle_s,
+        broadcast_s=ctx.broadcast_s, shuffle_msgs=ctx.shuffle_msgs,
+        broadcast_msgs=ctx.broadcast_msgs,
+        peak_bytes=[int(torch.cuda.max_memory_allocated())],
+        result_digest=result_digest(result) if result is not None else "empty",
+        exchange_counts=counts, shuffle_bytes=ctx.shuffle_bytes,
+        broadcast_bytes=ctx.broadcast_bytes)
+    return result, report
+
+
+def reference_run(qid: str, tables, variant: str = "default") -> ColumnTable:
+    """Single-context execution over full device tables (engine.py:463-469)."""
+    from .queries import PLAN_FUNCTIONS
+    if qid not in PLAN_FUNCTIONS:
+        from .queries import SUPPORTED_QUERIES
+        raise PlanError(f"unsupported query {qid!r}; supported: {SUPPORTED_QUERIES}")
+    if isinstance(tables, Dataset):
+        tables = load_tables(tables)
+    ctx = DeviceContext(Endpoint(0, 1, "nccl"), tables, variant, timed=False)
+    res = PLAN_FUNCTIONS[qid](ctx)
+    return res.materialize() if res is not None else None

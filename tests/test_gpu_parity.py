@@ -1,0 +1,203 @@
+"""GPU parity: the CUDA path vs the oracle / golden reference outputs.
+
+Bar: keys, counts, integer/date/dict columns and row order
+bit-exact; float64 columns within rtol 1e-9 (the tolerance north_star
+states).  Fixed-point aggregates are additionally checked bit-exact against
+an exact integer restatement.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, parse_key
+from oracle import ref as O
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-9
+
+
+def _dev():
+    import paper_2506_09226_b200 as P
+    return P
+
+
+def assert_table_matches(got, expected: dict, ctx=""):
+    """got: device ColumnTable; expected: oracle-jsonable dict."""
+    got = got.materialize()
+    assert got.column_names == list(expected), (ctx, got.column_names, list(expected))
+    for name, exp in expected.items():
+        c = got.column(name)
+        assert c.kind == exp["kind"], (ctx, name, c.kind, exp["kind"])
+        v = c.values
+        if exp["kind"] == "float64":
+            e = np.asarray([float.fromhex(x) for x in exp["hex"]])
+            assert len(v) == len(e), (ctx, name, len(v), len(e))
+            np.testing.assert_allclose(v, e, rtol=RTOL, atol=0, err_msg=f"{ctx}:{name}")
+        else:
+            e = np.asarray(exp["values"])
+            assert len(v) == len(e), (ctx, name, len(v), len(e))
+            assert np.array_equal(v.astype(np.int64), e.astype(np.int64)), (ctx, name, v[:10], e[:10])
+            if "dictionary" in exp:
+                assert list(c.dictionary) == exp["dictionary"]
+
+
+RES = load_golden("query_results.json")
+_DS = {}
+
+
+def device_tables(key):
+    if key not in _DS:
+        from paper_2506_09226_b200.data import generate
+        from paper_2506_09226_b200.engine import load_tables
+        sf, skew = parse_key(key)
+        _DS.clear()
+        _DS[key] = load_tables(generate(sf, skew, 0))
+    return _DS[key]
+
+
+@pytest.mark.parametrize("key", sorted(RES))
+@pytest.mark.parametrize("qid", ["Q1", "Q3", "Q6", "Q12", "Q14", "Q19"])
+def test_query_matches_reference(key, qid):
+    P = _dev()
+    tables = device_tables(key)
+    got = P.reference_run(qid, tables)
+    assert_table_matches(got, RES[key][qid], f"{key}/{qid}")
+
+
+@pytest.mark.parametrize("variant", ["default", "pa", "pb"])
+def test_q12_variants_single_gpu(variant):
+    P = _dev()
+    key = "sf0.01_skew0.0"
+    res, rep = P.run_query("Q12", variant, tables=device_tables(key),
+                           scheme="default_keys" if variant == "default" else "unpartitioned")
+    assert_table_matches(res, RES[key]["Q12"], variant)
+    assert rep.exchange_counts == P.get_plan("Q12", variant).expected_exchanges
+
+
+def test_q6_fixed_point_exact():
+    """Q6 revenue as an exact integer (cents x percent) == integer restatement."""
+    from paper_2506_09226_b200.data import generate
+    from paper_2506_09226_b200.engine import load_tables
+    import paper_2506_09226_b200.relops as R
+    from paper_2506_09226_b200.table import date_to_days as d
+    ds = generate(0.1, 0.0, 0)
+    li = ds.tables["lineitem"]
+    sd = li.column("l_shipdate").to_int64()
+    dc = li.column("l_discount").to_int64()
+    qt = li.column("l_quantity").to_int64()
+    ex = li.column("l_extendedprice").to_int64()
+    m = (sd >= d("1994-01-01")) & (sd < d("1995-01-01")) & (dc >= 5) & (dc <= 7) & (qt < 24)
+    exact = int((ex[m] * dc[m]).sum())                 # units of 1e-4 dollars
+    t = load_tables(ds)["lineitem"]
+    f = R.filter_table(t, (t["l_shipdate"] >= d("1994-01-01")) & (t["l_shipdate"] < d("1995-01-01"))
+                       & (t["l_discount"] >= 0.05) & (t["l_discount"] <= 0.07)
+                       & (t["l_quantity"] < 24))
+    f = f.with_column("rev", f["l_extendedprice"] * f["l_discount"])
+    g = R.group_aggregate(f, [], {"revenue": ("sum", "rev")})
+    c = g.column("revenue")
+    assert c.scale == 4
+    assert int(c.host()[0]) == exact
+
+
+REL = load_golden("relops.json")
+
+
+def _rel_tables():
+    from paper_2506_09226_b200.table import Column, ColumnTable
+
+    def up(j):
+        t = O.from_jsonable(j)
+        return ColumnTable({n: Column.from_numpy(k, v, d) for n, (k, v, d) in t.items()})
+    return up(REL["left"]), up(REL["right_unique"]), up(REL["right_dup"])
+
+
+@pytest.mark.parametrize("how", ["inner", "semi", "anti"])
+def test_join_semantics(how):
+    P = _dev()
+    left, ru, rd = _rel_tables()
+    assert_table_matches(P.local_hash_join(left, ru, [("lk", "rk")], how), REL[f"join_unique_{how}"], how)
+    if how != "inner":
+        assert_table_matches(P.local_hash_join(left, rd, [("lk", "rk")], how), REL[f"join_dup_{how}"],
+                             how + "_dup")
+
+
+AGGS = {"n": ("count", None), "s_f": ("sum", "lv"), "s_i": ("sum", "li"), "a_f": ("avg", "lv"),
+        "mn_i": ("min", "li"), "mx_i": ("max", "li"), "mn_f": ("min", "lv"),
+        "mx_d": ("max", "ld"), "s_d": ("sum", "ld")}
+
+
+@pytest.mark.parametrize("keys,name", [(["lc"], "group_lc"), (["lc", "ld"], "group_lc_ld"),
+                                       (["lk"], "group_lk"), ([], "group_none")])
+def test_group_semantics(keys, name):
+    P = _dev()
+    left, _, _ = _rel_tables()
+    assert_table_matches(P.group_aggregate(left, keys, AGGS), REL[name], name)
+
+
+def test_sort_semantics():
+    left, _, _ = _rel_tables()
+    assert_table_matches(left.sort_by(["lc", "lv"], {"lv"}), REL["sort_lc_desc_lv"], "sort1")
+    assert_table_matches(left.sort_by(["li", "ld"], {"li"}), REL["sort_li_ld"], "sort2")
+
+
+def test_filter_then_materialize_keeps_order():
+    P = _dev()
+    left, _, _ = _rel_tables()
+    ref = O.from_jsonable(REL["left"])
+    m = (ref["li"][1] > 3) & (ref["lv"][1] <= 500.0)
+    got = P.filter_table(left, (left["li"] > 3) & (left["lv"] <= 500.0)).materialize()
+    assert_table_matches(got, O.to_jsonable(O.filter_(ref, m)), "filter")
+    # numpy-mask filtering (reference spelling) goes through the same kernel
+    got2 = P.filter_table(left, m).materialize()
+    assert np.array_equal(got2.column("lk").values, ref["lk"][1][m])
+
+
+def test_hash_keys_and_partition_match_reference():
+    P = _dev()
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    k = load_golden("hash_kats.json")
+    t = ColumnTable({"k": Column.from_numpy("int64", np.asarray(k["keys"], dtype=np.int64))})
+    h = P.hash_keys(t, ["k"]).cpu().numpy()
+    assert [str(int(x)) for x in h] == k["hash_single"]
+    rng = np.random.default_rng(k["partition_input_seed"])
+    a = rng.integers(-(1 << 40), 1 << 40, size=2000)
+    b = rng.integers(0, 50, size=2000).astype(np.int32)
+    t2 = ColumnTable({"a": Column.from_numpy("int64", a), "b": Column.from_numpy("date32", b)})
+    for n, exp in k["partitions"].items():
+        parts = P.hash_partition(t2, ["a"], int(n))
+        assert [[int(x) for x in p.column("a").values] for p in parts] == exp["single"], n
+        parts2 = P.hash_partition(t2, ["a", "b"], int(n))
+        assert [p.row_count for p in parts2] == exp["multi_sizes"], n
+        assert [[int(x) for x in p.column("a").values[:5]] for p in parts2] == exp["multi_first"]
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 16])
+def test_partition_large_stable(n):
+    """Partition of SF1 lineitem on l_orderkey == oracle stable partition."""
+    P = _dev()
+    from paper_2506_09226_b200.data import generate
+    ds = generate(1.0, 0.0, 0)
+    t = ds.tables["lineitem"].select(["l_orderkey", "l_partkey", "l_shipdate"]).to_device()
+    parts = P.hash_partition(t, ["l_orderkey"], n)
+    ref = ds.tables["lineitem"].select(["l_orderkey", "l_partkey", "l_shipdate"]).to_reference()
+    oparts = O.hash_partition(ref, ["l_orderkey"], n)
+    assert sum(p.row_count for p in parts) == t.row_count
+    for p, o in zip(parts, oparts):
+        for c in ("l_orderkey", "l_partkey", "l_shipdate"):
+            assert np.array_equal(p.column(c).values, o[c][1])
+
+
+def test_radix_sort_large_and_edge_cases():
+    P = _dev()
+    import torch
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(3)
+    for n in (0, 1, 5, 4097, 300_000):
+        a = rng.integers(-1000, 1000, size=n)
+        b = rng.integers(0, 3, size=n)
+        t = ColumnTable({"a": Column.from_numpy("int64", a), "b": Column.from_numpy("int64", b)})
+        s = t.sort_by(["b", "a"], {"a"})
+        idx = np.lexsort([-a, b]) if n else np.arange(0)
+        assert np.array_equal(s.column("a").values, a[idx])
+        assert np.array_equal(s.column("b").values, b[idx])

@@ -766,7 +766,9 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
     integers, turned into result columns and uploaded.
     """
     cells = acc.shape[0]
-    vals = [[_i128(acc[c, j]) for j in range(acc.shape[1])] for c in range(cells)]
+    minmax = [op in ("min", "max") for op, _ in measures]
+    vals = [[int(acc[c, j, 0]) if minmax[j] else _i128(acc[c, j]) for j in range(acc.shape[1])]
+            for c in range(cells)]
     if keys:
         live = [c for c in range(cells) if vals[c][count_m] > 0]
     else:

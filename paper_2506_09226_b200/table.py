@@ -38,6 +38,7 @@ NP_TO_SCX = {
     np.dtype(np.int32): _lib.SCX_I32, np.dtype(np.int64): _lib.SCX_I64,
     np.dtype(np.uint8): _lib.SCX_U8, np.dtype(np.uint16): _lib.SCX_U16,
     np.dtype(np.float64): _lib.SCX_F64, np.dtype(np.uint32): _lib.SCX_U32,
+    np.dtype(np.uint64): _lib.SCX_I64,
 }
 MAX_DECIMAL_SCALE = 4
 
@@ -251,6 +252,7 @@ def torch_dtype(np_dtype: np.dtype):
             np.dtype(np.int32): torch.int32, np.dtype(np.int64): torch.int64,
             np.dtype(np.uint8): torch.uint8, np.dtype(np.uint16): torch.uint16,
             np.dtype(np.float64): torch.float64, np.dtype(np.uint32): torch.uint32,
+            np.dtype(np.uint64): torch.uint64,
         }
     return _TORCH_DTYPE[np.dtype(np_dtype)]
 

@@ -260,6 +260,67 @@ def generate(sf: float, skew: float = 0.0, seed: int = 0) -> Dataset:
 
 
 # ---------------------------------------------------------------------------
+# on-disk cache of the narrowed columns (.npy + manifest), so SF100 is
+# generated once per box and every rank of a job can mmap the same files
+# (SURVEY.md §5 "cache the generated columns as .npy").  Loader-only: no
+# timing depends on it.
+# ---------------------------------------------------------------------------
+
+def save_dataset(ds: Dataset, path: str) -> None:
+    import json
+    import os
+    os.makedirs(path, exist_ok=True)
+    meta = {"sf": ds.sf, "skew": ds.skew, "seed": ds.seed, "tables": {}}
+    for tname, t in ds.tables.items():
+        cols = {}
+        for cname, c in t.columns.items():
+            np.save(os.path.join(path, f"{tname}.{cname}.npy"), c.values)
+            cols[cname] = {"kind": c.kind, "scale": c.scale, "lo": c.lo, "hi": c.hi,
+                           "dictionary": list(c.dictionary) if c.dictionary else None}
+        meta["tables"][tname] = cols
+    tmp = os.path.join(path, "manifest.json.tmp")
+    with open(tmp, "w") as fh:
+        json.dump(meta, fh)
+    os.replace(tmp, os.path.join(path, "manifest.json"))
+
+
+def load_dataset(path: str, mmap: bool = True) -> Dataset:
+    import json
+    import os
+    with open(os.path.join(path, "manifest.json")) as fh:
+        meta = json.load(fh)
+    tables = {}
+    for tname, cols in meta["tables"].items():
+        hc = {}
+        for cname, m in cols.items():
+            v = np.load(os.path.join(path, f"{tname}.{cname}.npy"),
+                        mmap_mode="r" if mmap else None)
+            hc[cname] = HostColumn(m["kind"], v, m["scale"],
+                                   tuple(m["dictionary"]) if m["dictionary"] else None,
+                                   m["lo"], m["hi"])
+        tables[tname] = HostTable(hc)
+    return Dataset(tables, meta["sf"], meta["skew"], meta["seed"])
+
+
+def cached_generate(sf: float, skew: float = 0.0, seed: int = 0,
+                    root: str = "/tmp/scx_data") -> Dataset:
+    """generate() through the on-disk cache (validated by the manifest)."""
+    import os
+    path = os.path.join(root, f"sf{sf}_skew{skew}_seed{seed}")
+    if os.path.exists(os.path.join(path, "manifest.json")):
+        try:
+            return load_dataset(path)
+        except Exception:   # corrupt cache: regenerate
+            pass
+    ds = generate(sf, skew, seed)
+    try:
+        save_dataset(ds, path)
+    except OSError:
+        pass
+    return ds
+
+
+# ---------------------------------------------------------------------------
 # host-side partition assignment (the GPU path lives in exchange.py)
 # ---------------------------------------------------------------------------
 

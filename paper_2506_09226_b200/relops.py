@@ -503,10 +503,28 @@ class _Builder:
             T.n_factors = len(fs)
             for fi, (a, b, col) in enumerate(fs):
                 T.f[fi].a, T.f[fi].b, T.f[fi].slot = a, b, self.slot[col]
+                # narrow flag (scx_factor._pad): a + b*v fits int32 over the
+                # column's [lo, hi] -> the kernel's int32 fast path
+                c = self.v.meta[col]
+                if c.hi >= c.lo:
+                    ext = max(abs(a + b * c.lo), abs(a + b * c.hi))
+                    narrow = ext < (1 << 31) and abs(a) < (1 << 31) and abs(b) < (1 << 31)
+                else:
+                    narrow = abs(a) < (1 << 31) and abs(b) < (1 << 31) and b == 0
+                T.f[fi]._pad = 1 if narrow else 0
         if im.cond is not None:
             dst.cond_atom = self._atom(im.cond, 0)
 
-    def run(self):
+    def run(self, timing: list | None = None):
+        """Launch; with `timing`, CUDA events bracket exactly this launch."""
+        if timing is not None:
+            torch = _torch()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            L.call("scx_pipeline_run", C.byref(self.P), _stream())
+            e1.record()
+            timing.append((e0, e1))
+            return
         L.call("scx_pipeline_run", C.byref(self.P), _stream())
 
 
@@ -651,7 +669,7 @@ def _plan_aggs(v: TableView, aggs: dict) -> tuple[list[_Agg], list[tuple[str, In
 
 
 def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
-                    cross=None) -> ColumnTable:
+                    cross=None, timing: list | None = None) -> ColumnTable:
     """Aggregate per group (relops.py:97-160), one fused kernel launch.
 
     ``cross`` (engine.DeviceContext) makes it a global aggregate over all
@@ -697,7 +715,7 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
             if bound * per >= (1 << 62):
                 raise SchemaError("aggregate may overflow 64-bit partial sums")
     if dense:
-        return _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross)
+        return _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross, timing)
     part = _group_hash(v, b, keys, kcols, plan, measures, count_m)
     if cross is None or cross.ep.n == 1:
         return part
@@ -715,7 +733,7 @@ def regroup(full, keys: list[str], aggs: dict[str, tuple]) -> ColumnTable:
     return group_aggregate(full, keys, re)
 
 
-def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross=None):
+def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross=None, timing=None):
     torch = _torch()
     S = b.P.sink
     S.kind = L.SINK_AGG_DENSE
@@ -743,7 +761,7 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
             init[:, j, 0] = INT64_MIN
     acc = torch.from_numpy(init).to(_device())
     S.acc = acc.data_ptr()
-    b.run()
+    b.run(timing)
     if cross is not None and cross.ep.n > 1:
         from .exchange import all_gather_tensor
         parts = all_gather_tensor(cross.ep, acc)

@@ -70,41 +70,81 @@ def peaks() -> dict:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region.
 
-    def __init__(self, device: int):
+    NVML from a background thread (``nvidia_ml_py``), every ``period`` s.
+    ``SCX_CLOCKS=smi`` uses an ``nvidia-smi -lms`` subprocess instead and
+    ``SCX_CLOCKS=off`` disables sampling (for A/B checks of sampler
+    interference).
+    """
+
+    def __init__(self, device: int, period: float = 0.05):
+        import threading
+        self.mode = os.environ.get("SCX_CLOCKS", "nvml")
+        self.samples: list[tuple[float, float, int]] = []
+        self.max_mhz = None
         self.proc = None
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(device),
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+        self._stop = threading.Event()
+        self._thread = None
+        if self.mode == "nvml":
+            try:
+                import pynvml as N
+                N.nvmlInit()
+                idx = device
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                if vis and vis.split(",")[device].strip().isdigit():
+                    idx = int(vis.split(",")[device])
+                h = N.nvmlDeviceGetHandleByIndex(idx)
+                self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+
+                def run():
+                    while not self._stop.is_set():
+                        try:
+                            self.samples.append((
+                                float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                                self.max_mhz,
+                                int(N.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                        except Exception:
+                            pass
+                        self._stop.wait(period)
+
+                self._thread = threading.Thread(target=run, daemon=True)
+                self._thread.start()
+            except Exception as exc:  # pragma: no cover
+                self.mode = f"unavailable ({exc})"
+        elif self.mode == "smi":
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", "-i", str(device),
+                     "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                     "--format=csv,noheader,nounits", "-lms", "100"],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except OSError:
+                self.proc = None
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        sm, mx, reasons = [], [], set()
-        for line in out.strip().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 3:
-                continue
-            try:
-                s, m, r = float(parts[0]), float(parts[1]), int(parts[2], 16)
-            except ValueError:
-                continue
-            sm.append(s)
-            mx.append(m)
+        if self._thread is not None:
+            self._stop.set()
+            self._thread.join(timeout=5)
+        elif self.proc is not None:
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            for line in out.strip().splitlines():
+                parts = [x.strip() for x in line.split(",")]
+                try:
+                    self.samples.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except (ValueError, IndexError):
+                    continue
+        sm = [x[0] for x in self.samples]
+        mx = [x[1] for x in self.samples if x[1]]
+        reasons = set()
+        for _, _, r in self.samples:
             for bit, name in REASONS.items():
                 if r & bit and name != "gpu_idle":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "sm_max_mhz": max(mx) if mx else self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(sm), "sampler": self.mode}
 
 
 def alg_bytes(tables, qid) -> int:

@@ -227,6 +227,18 @@ int scx_device_info(int device, int* sm_count, int* smem_optin);
 int scx_pipeline_run(const scx_pipeline* desc_host, void* stream);
 /* number of 'status' words a COMPACT sink needs for n_rows */
 int64_t scx_pipeline_status_words(const scx_pipeline* desc_host);
+/* The pipeline is specialised per descriptor: libscx generates CUDA C++ for
+ * the plan (every dtype, literal, set, key packing and measure as an
+ * immediate), compiles it with NVRTC for sm_100a and caches the cubin in
+ * memory and on disk (<libdir>/jit_cache or $SCX_JIT_CACHE).  SCX_JIT=0
+ * selects the descriptor-interpreting kernel instead (A/B baseline).
+ * scx_pipeline_source: the generated source (length returned; up to cap-1
+ * bytes + NUL copied to buf).  scx_pipeline_compile: codegen + NVRTC into
+ * the disk cache without a device.  scx_jit_stats: kernels compiled / loaded
+ * from disk / reused in memory by this process. */
+int64_t scx_pipeline_source(const scx_pipeline* desc_host, char* buf, int64_t cap);
+int scx_pipeline_compile(const scx_pipeline* desc_host);
+int scx_jit_stats(int64_t* compiled, int64_t* disk_hits, int64_t* mem_hits);
 
 /* ---- lookup tables (local_hash_join build side, relops.py:81-84) --------
  * Inserts packed keys of rows [0, n) of `cols` into `table` (pre-cleared

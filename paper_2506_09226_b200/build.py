@@ -17,6 +17,10 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libscx.so")
 OBJ = os.path.join(HERE, "build")
+CUDA_LIB = "/usr/local/cuda/lib64"
+# NVRTC (plan-specialised kernels, csrc/jit.cu) is linked dynamically with an
+# rpath into the image's CUDA toolkit (the GPU box runs the same image)
+LINK = ["-L" + CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + CUDA_LIB, "-ldl"]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
@@ -64,7 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
-        run([nvcc, *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs])
+        run([nvcc, *ARCH, "-shared", "--cudart", "static", "-o", LIB, *objs, *LINK])
     return LIB
 
 

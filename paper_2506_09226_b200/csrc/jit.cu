@@ -1,0 +1,1025 @@
+// jit.cu -- plan-specialised scan kernels: scx_pipeline descriptor -> CUDA C++
+// source -> NVRTC (sm_100a cubin) -> driver-API launch.
+//
+// Why: the descriptor-interpreting kernel (pipeline.cu) pays ~180-600
+// warp-instructions per 32 rows re-reading atoms / measures / dtypes from
+// the parameter bank and dispatching on them (profiles/r1_v0_*).  At 8-11
+// narrowed bytes per row the HBM roofline leaves ~50 thread-instructions per
+// row, so the per-query fragment has to be compiled: every dtype, literal,
+// dictionary set, key packing and measure polynomial of the plan becomes an
+// immediate in straight-line code, and the only runtime parameters left are
+// device pointers, table capacities and the row count.
+//
+// Generated kernel shape (one CTA = 256 threads, V rows per thread-chunk):
+//   * tile = 256 consecutive chunks = 256*V consecutive rows; CTAs stride over
+//     tiles (tile order = row order, which the stable compaction relies on);
+//   * each thread loads its V rows of every touched column with 128-bit
+//     ld.global.nc (a 1-byte column is one 16-byte load per 16 rows), values
+//     are extracted from registers with compile-time byte offsets;
+//   * stages run column-at-a-time over the V rows held in registers:
+//     pre-predicate -> probes (all V first-probe loads issued before any is
+//     resolved) -> post-predicate -> sink;
+//   * sinks: dense group-by in per-thread int64 registers (<= 8 cells) or a
+//     shared-memory table, one exact 128-bit global atomic per cell per CTA;
+//     open-addressing hash group-by; stable compaction with a decoupled
+//     look-back over tiles; count.
+//
+// Generated sources and cubins are cached in memory (per device) and on disk
+// (<libdir>/jit_cache, keyed by a hash of source + options, source stored
+// beside the cubin and compared on load), so a plan compiles once per box.
+#include <dlfcn.h>
+#include <nvrtc.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <fstream>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace scx {
+
+int interp_pipeline_run(const scx_pipeline* d, void* stream);
+int64_t interp_status_words(const scx_pipeline* d);
+
+namespace jit {
+
+// ---------------------------------------------------------------------------
+// driver API through the runtime's entry-point query (no -lcuda link)
+// ---------------------------------------------------------------------------
+typedef int CUres;
+typedef void* CUmod;
+typedef void* CUfn;
+typedef CUres (*PFN_ModuleLoadData)(CUmod*, const void*);
+typedef CUres (*PFN_ModuleGetFunction)(CUfn*, CUmod, const char*);
+typedef CUres (*PFN_LaunchKernel)(CUfn, unsigned, unsigned, unsigned, unsigned, unsigned,
+                                  unsigned, unsigned, void*, void**, void**);
+typedef CUres (*PFN_FuncSetAttribute)(CUfn, int, int);
+typedef CUres (*PFN_FuncGetAttribute)(int*, int, CUfn);
+typedef CUres (*PFN_Occupancy)(int*, CUfn, int, size_t);
+typedef CUres (*PFN_GetErrorString)(CUres, const char**);
+
+struct Driver {
+  PFN_ModuleLoadData load = nullptr;
+  PFN_ModuleGetFunction get = nullptr;
+  PFN_LaunchKernel launch = nullptr;
+  PFN_FuncSetAttribute set_attr = nullptr;
+  PFN_FuncGetAttribute get_attr = nullptr;
+  PFN_Occupancy occupancy = nullptr;
+  PFN_GetErrorString errstr = nullptr;
+  bool ok = false;
+};
+
+static Driver& driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    auto sym = [](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+             q == cudaDriverEntryPointSuccess && *fn != nullptr;
+    };
+    d.ok = sym("cuModuleLoadData", (void**)&d.load) &&
+           sym("cuModuleGetFunction", (void**)&d.get) &&
+           sym("cuLaunchKernel", (void**)&d.launch) &&
+           sym("cuFuncSetAttribute", (void**)&d.set_attr) &&
+           sym("cuFuncGetAttribute", (void**)&d.get_attr) &&
+           sym("cuOccupancyMaxActiveBlocksPerMultiprocessor", (void**)&d.occupancy) &&
+           sym("cuGetErrorString", (void**)&d.errstr);
+  });
+  return d;
+}
+
+static int drv_fail(CUres r, const char* what) {
+  const char* s = "?";
+  if (driver().errstr) driver().errstr(r, &s);
+  set_error("%s: CUDA driver error %d (%s)", what, r, s);
+  return SCX_ECUDA;
+}
+
+// ---------------------------------------------------------------------------
+// compile + cache
+// ---------------------------------------------------------------------------
+static const char* kOptions[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo",
+                                 "-default-device"};
+static const int kNumOptions = 4;
+
+static uint64_t fnv1a(const std::string& s, uint64_t h = 0xcbf29ce484222325ull) {
+  for (unsigned char c : s) { h ^= c; h *= 0x100000001b3ull; }
+  return h;
+}
+
+struct Stats {
+  int64_t compiled = 0, disk_hits = 0, mem_hits = 0;
+  double compile_s = 0;
+};
+static Stats g_stats;
+static std::mutex g_mu;
+
+static std::string cache_dir() {
+  const char* env = getenv("SCX_JIT_CACHE");
+  if (env && *env) return env;
+  Dl_info info;
+  if (dladdr((void*)&cache_dir, &info) && info.dli_fname) {
+    std::string p = info.dli_fname;
+    size_t k = p.rfind('/');
+    if (k != std::string::npos) return p.substr(0, k) + "/jit_cache";
+  }
+  return "/tmp/scx_jit_cache";
+}
+
+static bool read_file(const std::string& path, std::string& out) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return false;
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  out = ss.str();
+  return true;
+}
+
+static void write_file_atomic(const std::string& path, const std::string& data) {
+  std::string tmp = path + ".tmp." + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    f.write(data.data(), (std::streamsize)data.size());
+  }
+  rename(tmp.c_str(), path.c_str());
+}
+
+// NVRTC: source -> sm_100a cubin
+int compile(const std::string& src, const std::string& name, std::string& cubin) {
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), (name + ".cu").c_str(), 0, nullptr,
+                                     nullptr);
+  if (r != NVRTC_SUCCESS) {
+    set_error("nvrtcCreateProgram: %s", nvrtcGetErrorString(r));
+    return SCX_ECUDA;
+  }
+  r = nvrtcCompileProgram(prog, kNumOptions, kOptions);
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    set_error("nvrtc compile of %s failed: %s\n%.1500s", name.c_str(), nvrtcGetErrorString(r),
+              log.c_str());
+    if (getenv("SCX_JIT_DUMP")) fprintf(stderr, "%s\n----\n%s\n", src.c_str(), log.c_str());
+    nvrtcDestroyProgram(&prog);
+    return SCX_EINVAL;
+  }
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin.assign(n, '\0');
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  return SCX_OK;
+}
+
+struct Entry {
+  std::string src;
+  CUfn fn = nullptr;
+  int max_dyn_smem = 0;
+};
+static std::unordered_map<std::string, Entry> g_fns;   // "dev:hash" -> kernel
+
+static std::string kernel_name(const std::string& body) {
+  char buf[40];
+  snprintf(buf, sizeof(buf), "scx_pipe_%016llx", (unsigned long long)fnv1a(body));
+  return buf;
+}
+
+// cubin for `src` (disk cache or NVRTC); no device needed
+static int get_cubin(const std::string& src, const std::string& name, std::string& cubin,
+                     bool& from_disk) {
+  const std::string dir = cache_dir();
+  const std::string base = dir + "/" + name;
+  std::string old_src;
+  from_disk = false;
+  if (read_file(base + ".cu", old_src) && old_src == src && read_file(base + ".cubin", cubin) &&
+      !cubin.empty()) {
+    from_disk = true;
+    return SCX_OK;
+  }
+  int rc = compile(src, name, cubin);
+  if (rc) return rc;
+  mkdir(dir.c_str(), 0775);
+  write_file_atomic(base + ".cubin", cubin);
+  write_file_atomic(base + ".cu", src);
+  return SCX_OK;
+}
+
+int get_function(const std::string& src, const std::string& name, Entry*& out) {
+  int dev = 0;
+  SCX_CUDA(cudaGetDevice(&dev));
+  const std::string key = std::to_string(dev) + ":" + name;
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    auto it = g_fns.find(key);
+    if (it != g_fns.end() && it->second.src == src) {
+      ++g_stats.mem_hits;
+      out = &it->second;
+      return SCX_OK;
+    }
+  }
+  Driver& d = driver();
+  if (!d.ok) {
+    set_error("jit: CUDA driver entry points unavailable");
+    return SCX_ECUDA;
+  }
+  std::string cubin;
+  bool disk = false;
+  int rc = get_cubin(src, name, cubin, disk);
+  if (rc) return rc;
+  SCX_CUDA(cudaFree(nullptr));   // make the device's primary context current
+  CUmod mod = nullptr;
+  CUres cr = d.load(&mod, cubin.data());
+  if (cr) return drv_fail(cr, "cuModuleLoadData");
+  CUfn fn = nullptr;
+  cr = d.get(&fn, mod, name.c_str());
+  if (cr) return drv_fail(cr, "cuModuleGetFunction");
+  std::lock_guard<std::mutex> g(g_mu);
+  if (disk) ++g_stats.disk_hits; else ++g_stats.compiled;
+  Entry& e = g_fns[key];
+  e.src = src;
+  e.fn = fn;
+  e.max_dyn_smem = 0;
+  out = &e;
+  return SCX_OK;
+}
+
+// ---------------------------------------------------------------------------
+// code generation
+// ---------------------------------------------------------------------------
+static const char* kPrelude = R"PRE(
+typedef signed char i8; typedef unsigned char u8; typedef short i16; typedef unsigned short u16;
+typedef int i32; typedef unsigned int u32; typedef long long i64; typedef unsigned long long u64;
+#define SCX_EMPTY 0xFFFFFFFFFFFFFFFFull
+#define SCX_NOROW 0xFFFFFFFFu
+struct Args { i64 n; u64 p[MAXP]; };
+static __device__ __forceinline__ u64 mix64(u64 k) {
+  k ^= k >> 33; k *= 0xff51afd7ed558ccdull; k ^= k >> 33; k *= 0xc4ceb9fe1a85ec53ull;
+  k ^= k >> 33; return k;
+}
+static __device__ __forceinline__ uint4 ldv4(const void* p) {
+  uint4 v;
+  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+      : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+static __device__ __forceinline__ uint2 ldv2(const void* p) {
+  uint2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+static __device__ __forceinline__ u32 ldv1(const void* p) {
+  u32 v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+static __device__ __forceinline__ u64 ld_acquire(const u64* p) {
+  u64 v; asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+static __device__ __forceinline__ void st_release(u64* p, u64 v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+static __device__ __forceinline__ void atomic_add_i128(i64* lohi, i64 v) {
+  if (v == 0) return;
+  u64 old = atomicAdd((unsigned long long*)lohi, (unsigned long long)v);
+  u64 sum = old + (u64)v;
+  i64 hi_add = (v < 0 ? -1ll : 0ll) + (sum < old ? 1ll : 0ll);
+  if (hi_add) atomicAdd((unsigned long long*)(lohi + 1), (unsigned long long)hi_add);
+}
+static __device__ __forceinline__ i64 wsum(i64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+static __device__ __forceinline__ i64 wmin(i64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { i64 w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
+  return v;
+}
+static __device__ __forceinline__ i64 wmax(i64 v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) { i64 w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+  return v;
+}
+static __device__ __forceinline__ i64 smin(i64 a, i64 b) { return a < b ? a : b; }
+static __device__ __forceinline__ i64 smax(i64 a, i64 b) { return a > b ? a : b; }
+#define X1S(w, r) ((i32)(i8)((w)[(r) >> 2] >> (((r) & 3) * 8)))
+#define X1U(w, r) ((i32)(((w)[(r) >> 2] >> (((r) & 3) * 8)) & 0xffu))
+#define X2S(w, r) ((i32)(i16)((w)[(r) >> 1] >> (((r) & 1) * 16)))
+#define X2U(w, r) ((i32)(((w)[(r) >> 1] >> (((r) & 1) * 16)) & 0xffffu))
+#define X4S(w, r) ((i32)(w)[(r)])
+#define X4U(w, r) ((u32)(w)[(r)])
+#define X8(w, r) ((i64)(((u64)(w)[2 * (r) + 1] << 32) | (u64)(w)[2 * (r)]))
+)PRE";
+
+static const int kTPB = 256;
+static const int kMaxP = 96;
+
+static std::string lit64(int64_t v) {
+  char b[48];
+  snprintf(b, sizeof(b), "((i64)0x%016llxull)", (unsigned long long)v);
+  return b;
+}
+static std::string ulit64(uint64_t v) {
+  char b[40];
+  snprintf(b, sizeof(b), "0x%016llxull", (unsigned long long)v);
+  return b;
+}
+
+static bool fits32_dt(int dt) {
+  return dt == SCX_I8 || dt == SCX_I16 || dt == SCX_I32 || dt == SCX_U8 || dt == SCX_U16;
+}
+static const char* ctype(int dt) {
+  switch (dt) {
+    case SCX_I8: return "i8"; case SCX_U8: return "u8"; case SCX_I16: return "i16";
+    case SCX_U16: return "u16"; case SCX_I32: return "i32"; case SCX_U32: return "u32";
+    default: return "i64";
+  }
+}
+
+struct Gen {
+  const scx_pipeline& P;
+  std::ostringstream o;        // kernel body
+  std::ostringstream g;        // globals (sets, luts)
+  std::vector<uint64_t> ptrs;  // Args.p values, in generation order
+  int V = 16;
+  int n_globals = 0;
+  size_t dyn_smem = 0;
+  std::string err;
+
+  explicit Gen(const scx_pipeline& p) : P(p) {}
+
+  int param(uint64_t v) {
+    ptrs.push_back(v);
+    return (int)ptrs.size() - 1;
+  }
+
+  // value of slot s at row r (r is a loop variable / literal in the source)
+  std::string val(int s, const char* r) {
+    const int dt = P.slot_dtype[s];
+    char b[96];
+    if (s < P.n_base) {
+      switch (dt) {
+        case SCX_I8: snprintf(b, sizeof(b), "X1S(w%d, %s)", s, r); break;
+        case SCX_U8: snprintf(b, sizeof(b), "X1U(w%d, %s)", s, r); break;
+        case SCX_I16: snprintf(b, sizeof(b), "X2S(w%d, %s)", s, r); break;
+        case SCX_U16: snprintf(b, sizeof(b), "X2U(w%d, %s)", s, r); break;
+        case SCX_I32: snprintf(b, sizeof(b), "X4S(w%d, %s)", s, r); break;
+        case SCX_U32: snprintf(b, sizeof(b), "X4U(w%d, %s)", s, r); break;
+        default: snprintf(b, sizeof(b), "X8(w%d, %s)", s, r); break;
+      }
+    } else {
+      if (fits32_dt(dt)) snprintf(b, sizeof(b), "((i32)pv%d[%s])", s, r);
+      else snprintf(b, sizeof(b), "pv%d[%s]", s, r);
+    }
+    return b;
+  }
+
+  // bitmap membership of a dictionary code set
+  std::string set_expr(const scx_atom& A, const std::string& v) {
+    const int nw = (int)A.lo;
+    const uint32_t* w = P.setwords + A.set_word;
+    char b[160];
+    if (nw <= 1) {
+      snprintf(b, sizeof(b), "((u32)(%s) < 32u && ((0x%08xu >> (u32)(%s)) & 1u))", v.c_str(),
+               w[0], v.c_str());
+      return b;
+    }
+    if (nw == 2) {
+      const uint64_t m = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
+      snprintf(b, sizeof(b), "((u32)(%s) < 64u && ((%s >> (u32)(%s)) & 1ull))", v.c_str(),
+               ulit64(m).c_str(), v.c_str());
+      return b;
+    }
+    const int id = n_globals++;
+    g << "static __device__ const u32 SET" << id << "[" << nw << "] = {";
+    for (int i = 0; i < nw; ++i) g << (i ? "," : "") << w[i] << "u";
+    g << "};\n";
+    snprintf(b, sizeof(b), "((u32)(%s) < %du && ((__ldg(SET%d + ((u32)(%s) >> 5)) >> ((u32)(%s) & 31u)) & 1u))",
+             v.c_str(), nw * 32, id, v.c_str(), v.c_str());
+    return b;
+  }
+
+  std::string range_expr(const std::string& v, bool narrow, int64_t lo, int64_t hi) {
+    if (lo > hi) return "false";
+    char b[200];
+    if (narrow) {
+      if (lo < INT32_MIN) lo = INT32_MIN;
+      if (hi > INT32_MAX) hi = INT32_MAX;
+      if (lo > hi) return "false";
+      if (lo == INT32_MIN && hi == INT32_MAX) return "true";
+      const uint32_t span = (uint32_t)((int64_t)hi - lo);
+      snprintf(b, sizeof(b), "((u32)(%s) - (u32)(%d) <= %uu)", v.c_str(), (int32_t)lo, span);
+      return b;
+    }
+    const uint64_t span = (uint64_t)hi - (uint64_t)lo;
+    snprintf(b, sizeof(b), "((u64)(i64)(%s) - (u64)%s <= %s)", v.c_str(), lit64(lo).c_str(),
+             ulit64(span).c_str());
+    return b;
+  }
+
+  std::string atom_expr(const scx_atom& A, const char* r) {
+    std::string e;
+    if (A.slot < 0 || A.slot >= P.n_slots) { err = "atom slot out of range"; return "false"; }
+    const int dt = P.slot_dtype[A.slot];
+    if (A.op == SCX_ATOM_RANGE) {
+      e = range_expr(val(A.slot, r), fits32_dt(dt), A.lo, A.hi);
+    } else if (A.op == SCX_ATOM_SET) {
+      e = set_expr(A, val(A.slot, r));
+    } else if (A.op == SCX_ATOM_DIFF) {
+      if (A.slot2 < 0 || A.slot2 >= P.n_slots) { err = "atom slot2 out of range"; return "false"; }
+      const std::string d = "((i64)" + val(A.slot, r) + " - (i64)" + val(A.slot2, r) + ")";
+      e = range_expr(d, false, A.lo, A.hi);
+    } else {
+      err = "unknown atom op";
+      return "false";
+    }
+    return A.negate ? "(!" + e + ")" : e;
+  }
+
+  std::string pred_expr(const scx_pred& pr, const char* r) {
+    if (pr.clause_mask == 0 || pr.n_atoms == 0) return "true";
+    std::string out, cur;
+    int clause = P.atoms[pr.first_atom].clause;
+    for (int a = pr.first_atom; a < pr.first_atom + pr.n_atoms; ++a) {
+      const scx_atom& A = P.atoms[a];
+      if (A.clause != clause) {
+        out += (out.empty() ? "" : " || ") + ("(" + cur + ")");
+        cur.clear();
+        clause = A.clause;
+      }
+      cur += (cur.empty() ? "" : " && ") + atom_expr(A, r);
+    }
+    out += (out.empty() ? "" : " || ") + ("(" + cur + ")");
+    return out;
+  }
+
+  std::string lut_expr(int off, int n, const std::string& v) {
+    // dictionary code -> string rank; packed into an immediate when small
+    bool small = n <= 16;
+    for (int i = 0; i < n && small; ++i) small = P.lut[off + i] >= 0 && P.lut[off + i] < 16;
+    if (small) {
+      uint64_t m = 0;
+      for (int i = 0; i < n; ++i) m |= (uint64_t)P.lut[off + i] << (4 * i);
+      return "((i64)((" + ulit64(m) + " >> (4u * (u32)(" + v + "))) & 15ull))";
+    }
+    const int id = n_globals++;
+    g << "static __device__ const i16 LUT" << id << "[" << n << "] = {";
+    for (int i = 0; i < n; ++i) g << (i ? "," : "") << P.lut[off + i];
+    g << "};\n";
+    return "((i64)__ldg(LUT" + std::to_string(id) + " + (" + v + ")))";
+  }
+
+  // packed key (u64) + in-range flag into variables `kv` / `kin`
+  void pack_key(const scx_keyspec& K, const char* r, const int32_t* glut, int lut_n,
+                const std::string& kv, const std::string& kin) {
+    o << "      u64 " << kv << " = 0; bool " << kin << " = true;\n";
+    for (int i = 0; i < K.n; ++i) {
+      std::string v = "((i64)" + val(K.slot[i], r) + " - " + lit64(K.lo[i]) + ")";
+      if (glut && glut[i] >= 0) {
+        int n = lut_n;
+        if (n < 0) {   // hash group key: LUT covers the key's bit range
+          n = K.bits[i] >= 16 ? SCX_MAX_LUT : (1 << K.bits[i]);
+          if (glut[i] + n > SCX_MAX_LUT) n = SCX_MAX_LUT - glut[i];
+        }
+        v = lut_expr(glut[i], n, v);
+      }
+      o << "      { const u64 u = (u64)" << v << ";";
+      if (K.bits[i] < 64) o << " " << kin << " &= (u >> " << K.bits[i] << ") == 0ull;";
+      o << " " << kv << " |= u << " << K.shift[i] << "; }\n";
+    }
+  }
+
+  std::string factor(const scx_factor& F, const char* r) {
+    if (F.slot < 0) return lit64(F.a);
+    const int dt = P.slot_dtype[F.slot];
+    const std::string v = val(F.slot, r);
+    const bool narrow = F._pad == 1 && fits32_dt(dt) && F.a >= INT32_MIN && F.a <= INT32_MAX &&
+                        F.b >= INT32_MIN && F.b <= INT32_MAX;
+    char b[200];
+    if (narrow) {
+      if (F.a == 0 && F.b == 1) return "((i32)" + v + ")";
+      snprintf(b, sizeof(b), "((i32)(%d) + (i32)(%d) * (i32)%s)", (int)F.a, (int)F.b, v.c_str());
+      return b;
+    }
+    if (F.a == 0 && F.b == 1) return "((i64)" + v + ")";
+    return "(" + lit64(F.a) + " + " + lit64(F.b) + " * (i64)" + v + ")";
+  }
+
+  std::string measure_expr(const scx_measure& M, const char* r) {
+    std::string e;
+    if (M.op == SCX_AGG_COUNT) {
+      e = "1ll";
+    } else {
+      for (int t = 0; t < M.n_terms; ++t) {
+        const scx_term& T = M.t[t];
+        std::string p;
+        for (int f = 0; f < T.n_factors; ++f) {
+          const std::string fx = factor(T.f[f], r);
+          p = p.empty() ? "(i64)" + fx : "(" + p + " * " + fx + ")";
+        }
+        if (p.empty()) p = lit64(T.coef);
+        else if (T.coef != 1) p = "(" + lit64(T.coef) + " * " + p + ")";
+        e += (e.empty() ? "" : " + ") + p;
+      }
+      if (e.empty()) e = "0ll";
+    }
+    if (M.cond_atom >= 0) e = "((" + atom_expr(P.atoms[M.cond_atom], r) + ") ? (i64)(" + e + ") : 0ll)";
+    return "(i64)(" + e + ")";
+  }
+
+  // ---- pieces of the kernel ----
+  void emit_word_decls() {
+    for (int s = 0; s < P.n_base; ++s)
+      o << "    u32 w" << s << "[" << V * dtype_size(P.base[s].dtype) / 4 << "];\n";
+  }
+
+  void emit_loads() {
+    for (int s = 0; s < P.n_base; ++s) {
+      const int w = dtype_size(P.base[s].dtype);
+      const int nb = V * w;                  // bytes per chunk
+      const int nwords = nb / 4;
+      const int pi = param(P.base[s].ptr);
+      o << "    { const char* p = (const char*)a.p[" << pi << "] + row0 * " << w << "ll;\n";
+      o << "      if (full) {\n";
+      if (nb >= 16) {
+        for (int j = 0; j < nb / 16; ++j)
+          o << "        { uint4 t = ldv4(p + " << 16 * j << "); w" << s << "[" << 4 * j
+            << "] = t.x; w" << s << "[" << 4 * j + 1 << "] = t.y; w" << s << "[" << 4 * j + 2
+            << "] = t.z; w" << s << "[" << 4 * j + 3 << "] = t.w; }\n";
+      } else if (nb == 8) {
+        o << "        { uint2 t = ldv2(p); w" << s << "[0] = t.x; w" << s << "[1] = t.y; }\n";
+      } else {
+        o << "        w" << s << "[0] = ldv1(p);\n";
+      }
+      o << "      } else {\n";
+      o << "#pragma unroll\n        for (int j = 0; j < " << nwords << "; ++j) w" << s
+        << "[j] = 0u;\n";
+      o << "#pragma unroll\n        for (int r = 0; r < V; ++r) if (r < rem) {\n";
+      switch (w) {
+        case 1: o << "          w" << s << "[r >> 2] |= (u32)((const u8*)p)[r] << ((r & 3) * 8);\n"; break;
+        case 2: o << "          w" << s << "[r >> 1] |= (u32)((const u16*)p)[r] << ((r & 1) * 16);\n"; break;
+        case 4: o << "          w" << s << "[r] = ((const u32*)p)[r];\n"; break;
+        default: o << "          w" << s << "[2 * r] = ((const u32*)p)[2 * r]; w" << s
+                   << "[2 * r + 1] = ((const u32*)p)[2 * r + 1];\n"; break;
+      }
+      o << "        }\n      }\n    }\n";
+    }
+  }
+
+  void emit_pred(const scx_pred& pr, const char* what) {
+    if (pr.clause_mask == 0 || pr.n_atoms == 0) return;
+    o << "    // " << what << "\n";
+    o << "#pragma unroll\n    for (int r = 0; r < V; ++r) {\n";
+    o << "      const bool ok = " << pred_expr(pr, "r") << ";\n";
+    o << "      if (!ok) sel &= ~(1u << r);\n    }\n";
+  }
+
+  void emit_probe(int pi) {
+    const scx_probe& pb = P.probe[pi];
+    const int keys_p = param(pb.table.keys);
+    const int vals_p = param(pb.table.vals);
+    const int cap_p = param(pb.table.cap);
+    o << "    // probe " << pi << " (" << (pb.kind == SCX_JOIN_SEMI ? "semi" :
+                                          pb.kind == SCX_JOIN_ANTI ? "anti" : "inner") << ", "
+      << (pb.table.kind == SCX_HT_DIRECT ? "direct" : "hash") << ")\n";
+    o << "    u32 idx" << pi << "[V];\n    {\n";
+    o << "      const u32* vals = (const u32*)a.p[" << vals_p << "];\n";
+    o << "      const u64 cap = a.p[" << cap_p << "];\n";
+    if (pb.table.kind == SCX_HT_DIRECT) {
+      o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
+      o << "        idx" << pi << "[r] = SCX_NOROW;\n";
+      o << "        if ((sel >> r) & 1u) {\n";
+      pack_key(pb.key, "r", nullptr, 0, "key", "kin");
+      o << "          if (kin && key < cap) idx" << pi << "[r] = __ldg(vals + key);\n";
+      o << "        }\n      }\n";
+    } else {
+      o << "      const u64* keys = (const u64*)a.p[" << keys_p << "];\n";
+      o << "      const u64 mask = cap - 1;\n";
+      o << "      u64 hk[V], hh[V], k0[V];\n";
+      o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
+      o << "        idx" << pi << "[r] = SCX_NOROW; hk[r] = SCX_EMPTY; hh[r] = 0; k0[r] = SCX_EMPTY;\n";
+      o << "        if ((sel >> r) & 1u) {\n";
+      pack_key(pb.key, "r", nullptr, 0, "key", "kin");
+      o << "          if (kin) { hk[r] = key; hh[r] = mix64(key) & mask; k0[r] = __ldg(keys + hh[r]); }\n";
+      o << "        }\n      }\n";
+      o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
+      o << "        if (hk[r] == SCX_EMPTY) continue;\n";
+      o << "        u64 h = hh[r], k = k0[r];\n";
+      o << "        while (k != hk[r] && k != SCX_EMPTY) { h = (h + 1) & mask; k = __ldg(keys + h); }\n";
+      o << "        if (k == hk[r]) idx" << pi << "[r] = __ldg(vals + h);\n";
+      o << "      }\n";
+    }
+    o << "    }\n";
+    const bool anti = pb.kind == SCX_JOIN_ANTI;
+    o << "#pragma unroll\n    for (int r = 0; r < V; ++r) if (idx" << pi << "[r] "
+      << (anti ? "!=" : "==") << " SCX_NOROW) sel &= ~(1u << r);\n";
+    if (pb.kind == SCX_JOIN_INNER) {
+      for (int j = 0; j < pb.n_payload; ++j) {
+        const int s = pb.payload_slot[j];
+        const int src_p = param(pb.payload[j].ptr);
+        const char* t = ctype(pb.payload[j].dtype);
+        o << "    " << t << " pv" << s << "[V];\n";
+        o << "    { const " << t << "* src = (const " << t << "*)a.p[" << src_p << "];\n";
+        o << "#pragma unroll\n      for (int r = 0; r < V; ++r) pv" << s
+          << "[r] = ((sel >> r) & 1u) ? __ldg(src + idx" << pi << "[r]) : (" << t << ")0; }\n";
+      }
+    }
+  }
+
+  // ------------------------------------------------------------------------
+  int generate(std::string& src, std::string& name, int& tiles_out) {
+    const scx_sink& S = P.sink;
+    int row_bytes = 0, max_w = 1;
+    for (int c = 0; c < P.n_base; ++c) {
+      const int w = dtype_size(P.base[c].dtype);
+      if (w == 0) { err = "bad base dtype"; return SCX_EINVAL; }
+      if (P.slot_dtype[c] != P.base[c].dtype) { err = "slot dtype != base dtype"; return SCX_EINVAL; }
+      if (P.base[c].ptr % 16) { err = "base column not 16-byte aligned"; return SCX_EINVAL; }
+      row_bytes += w;
+      max_w = max_w > w ? max_w : w;
+    }
+    int payload_bytes = 0;
+    for (int s = P.n_base; s < P.n_slots; ++s) payload_bytes += dtype_size(P.slot_dtype[s]);
+    // rows per thread-chunk: 16 keeps a 1-byte column at one 16-byte load;
+    // wide rows drop to 8 to bound registers
+    V = (row_bytes + payload_bytes <= 24 && max_w <= 4) ? 16 : 8;
+    if (S.kind == SCX_SINK_AGG_DENSE && S.n_cells > 1 && S.n_cells <= 8) V = 8;
+    if (S.kind == SCX_SINK_AGG_HASH) V = 8;
+    const int64_t tile_rows = (int64_t)kTPB * V;
+    tiles_out = (int)((P.n_rows + tile_rows - 1) / tile_rows);
+
+    const bool dense_reg = S.kind == SCX_SINK_AGG_DENSE && S.n_cells <= 8;
+    const int M = S.n_measures;
+    const int NC = dense_reg ? (S.n_cells < 1 ? 1 : S.n_cells) : 0;
+
+    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ") KNAME(const __grid_constant__ Args a) {\n";
+    o << "  constexpr int V = " << V << ";\n";
+    o << "  const i64 n = a.n;\n";
+    o << "  const i64 ntiles = (n + " << tile_rows << "ll - 1) / " << tile_rows << "ll;\n";
+    o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+    o << "  (void)lane; (void)warp;\n";
+
+    // sink state
+    int acc_p = -1, gkeys_p = -1, gcap_p = -1, flags_p = -1, status_p = -1, count_p = -1;
+    std::vector<int> out_p;
+    if (S.kind == SCX_SINK_AGG_DENSE) {
+      acc_p = param(S.acc);
+      if (dense_reg) {
+        o << "  i64 acc[" << NC << "][" << M << "];\n";
+        for (int c = 0; c < NC; ++c)
+          for (int m = 0; m < M; ++m)
+            o << "  acc[" << c << "][" << m << "] = " << (S.m[m].op == SCX_AGG_MIN ? "0x7fffffffffffffffll" :
+                                                         S.m[m].op == SCX_AGG_MAX ? "(-0x7fffffffffffffffll - 1)" : "0ll") << ";\n";
+      } else {
+        const int64_t words = (int64_t)S.n_cells * M;
+        if (words * 8 > 160 * 1024) { err = "dense sink too large for shared memory"; return SCX_EUNSUPPORTED; }
+        dyn_smem = (size_t)words * 8;
+        o << "  extern __shared__ __align__(16) i64 tab[];\n";
+        o << "  for (int i = tid; i < " << words << "; i += " << kTPB << ") {\n";
+        o << "    const int m = i % " << M << ";\n";
+        o << "    tab[i] = ";
+        for (int m = 0; m < M; ++m)
+          o << "m == " << m << " ? " << (S.m[m].op == SCX_AGG_MIN ? "0x7fffffffffffffffll" :
+                                         S.m[m].op == SCX_AGG_MAX ? "(-0x7fffffffffffffffll - 1)" : "0ll") << " : ";
+        o << "0ll;\n  }\n  __syncthreads();\n";
+      }
+    } else if (S.kind == SCX_SINK_AGG_HASH) {
+      acc_p = param(S.acc);
+      gkeys_p = param(S.gkeys);
+      gcap_p = param(S.gcap);
+      flags_p = param(S.flags);
+      o << "  u64* gkeys = (u64*)a.p[" << gkeys_p << "];\n";
+      o << "  i64* gacc = (i64*)a.p[" << acc_p << "];\n";
+      o << "  const u64 gmask = a.p[" << gcap_p << "] - 1;\n";
+    } else if (S.kind == SCX_SINK_COMPACT) {
+      status_p = param(S.status);
+      count_p = param(S.count);
+      for (int i = 0; i < S.n_out; ++i) out_p.push_back(param(S.out[i].ptr));
+      o << "  __shared__ u32 s_warp[" << kTPB / 32 << "];\n";
+      o << "  __shared__ i64 s_excl;\n";
+    } else if (S.kind == SCX_SINK_COUNT) {
+      count_p = param(S.count);
+      o << "  u64 cnt = 0;\n";
+    } else {
+      err = "unknown sink";
+      return SCX_EINVAL;
+    }
+
+    o << "  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+    o << "    const i64 row0 = (tile * " << kTPB << " + tid) * (i64)V;\n";
+    o << "    const bool full = row0 + V <= n;\n";
+    o << "    const int rem = row0 >= n ? 0 : (int)(n - row0 < V ? n - row0 : V);\n";
+    o << "    u32 sel = full ? " << (V == 32 ? "0xffffffffu" : std::to_string((1u << V) - 1) + "u")
+      << " : ((1u << rem) - 1u);\n";
+    emit_word_decls();
+    o << "    if (rem > 0) {\n";
+    emit_loads();
+    o << "    }\n";
+    // when rem == 0 the word arrays are uninitialised but sel == 0 masks every use
+    emit_pred(P.pre, "pre-predicate");
+    for (int p = 0; p < P.n_probes; ++p) emit_probe(p);
+    emit_pred(P.post, "post-predicate");
+
+    // ---- sink per row ----
+    if (S.kind == SCX_SINK_AGG_DENSE) {
+      o << "#pragma unroll\n    for (int r = 0; r < V; ++r) {\n";
+      o << "      if (!((sel >> r) & 1u)) continue;\n";
+      o << "      int cell = 0;\n";
+      for (int i = 0; i < S.gkey.n; ++i) {
+        std::string v = "((i64)" + val(S.gkey.slot[i], "r") + " - " + lit64(S.gkey.lo[i]) + ")";
+        if (S.glut[i] >= 0) v = lut_expr(S.glut[i], S.gcard[i], v);
+        o << "      cell = cell * " << S.gcard[i] << " + (int)" << v << ";\n";
+      }
+      for (int m = 0; m < M; ++m) o << "      const i64 m" << m << " = " << measure_expr(S.m[m], "r") << ";\n";
+      if (dense_reg) {
+        for (int c = 0; c < NC; ++c) {
+          if (NC > 1) o << "      if (cell == " << c << ") {\n";
+          for (int m = 0; m < M; ++m) {
+            const int op = S.m[m].op;
+            o << "        acc[" << c << "][" << m << "] = ";
+            if (op == SCX_AGG_MIN) o << "smin(acc[" << c << "][" << m << "], m" << m << ");\n";
+            else if (op == SCX_AGG_MAX) o << "smax(acc[" << c << "][" << m << "], m" << m << ");\n";
+            else o << "acc[" << c << "][" << m << "] + m" << m << ";\n";
+          }
+          if (NC > 1) o << "      }\n";
+        }
+      } else {
+        for (int m = 0; m < M; ++m) {
+          const int op = S.m[m].op;
+          o << "      { unsigned long long* t = (unsigned long long*)&tab[cell * " << M << " + " << m << "]; ";
+          if (op == SCX_AGG_MIN) o << "atomicMin((long long*)t, (long long)m" << m << "); }\n";
+          else if (op == SCX_AGG_MAX) o << "atomicMax((long long*)t, (long long)m" << m << "); }\n";
+          else o << "atomicAdd(t, (unsigned long long)m" << m << "); }\n";
+        }
+      }
+      o << "    }\n";
+    } else if (S.kind == SCX_SINK_AGG_HASH) {
+      o << "#pragma unroll\n    for (int r = 0; r < V; ++r) {\n";
+      o << "      if (!((sel >> r) & 1u)) continue;\n";
+      pack_key(S.gkey, "r", S.glut, -1, "key", "kin");
+      // lut length for hash group keys: dictionary size isn't in the keyspec;
+      // the LUT region is bounded by SCX_MAX_LUT so emit the whole tail
+      o << "      (void)kin;\n";
+      o << "      u64 h = mix64(key) & gmask; u64 slot = SCX_EMPTY;\n";
+      o << "      for (u64 pr = 0; pr <= gmask; ++pr) {\n";
+      o << "        u64 cur = gkeys[h];\n";
+      o << "        if (cur == SCX_EMPTY) { cur = atomicCAS((unsigned long long*)(gkeys + h), SCX_EMPTY, key); if (cur == SCX_EMPTY) cur = key; }\n";
+      o << "        if (cur == key) { slot = h; break; }\n";
+      o << "        h = (h + 1) & gmask;\n      }\n";
+      o << "      if (slot == SCX_EMPTY) { atomicOr((u32*)a.p[" << flags_p << "], 1u); continue; }\n";
+      for (int m = 0; m < M; ++m) {
+        const int op = S.m[m].op;
+        o << "      { const i64 mv = " << measure_expr(S.m[m], "r") << "; long long* t = (long long*)(gacc + slot * " << M << " + " << m << "); ";
+        if (op == SCX_AGG_MIN) o << "atomicMin(t, mv); }\n";
+        else if (op == SCX_AGG_MAX) o << "atomicMax(t, mv); }\n";
+        else o << "atomicAdd((unsigned long long*)t, (unsigned long long)mv); }\n";
+      }
+      o << "    }\n";
+    } else if (S.kind == SCX_SINK_COUNT) {
+      o << "    cnt += __popc(sel);\n";
+    } else {  // COMPACT
+      o << "    {\n";
+      o << "      const u32 c = __popc(sel);\n";
+      o << "      u32 inc = c;\n";
+      o << "#pragma unroll\n      for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, inc, d); if (lane >= d) inc += y; }\n";
+      o << "      if (lane == 31) s_warp[warp] = inc;\n";
+      o << "      __syncthreads();\n";
+      o << "      if (tid == 0) {\n";
+      o << "        u32 run = 0;\n";
+      o << "        for (int i = 0; i < " << kTPB / 32 << "; ++i) { const u32 t = s_warp[i]; s_warp[i] = run; run += t; }\n";
+      o << "        u64* status = (u64*)a.p[" << status_p << "];\n";
+      o << "        const u64 kA = 1ull << 62, kP = 2ull << 62, kV = (1ull << 62) - 1;\n";
+      o << "        u64 excl = 0;\n";
+      o << "        if (tile == 0) { st_release(status, kP | (u64)run); }\n";
+      o << "        else {\n";
+      o << "          st_release(status + tile, kA | (u64)run);\n";
+      o << "          i64 j = tile - 1;\n";
+      o << "          while (true) { const u64 w = ld_acquire(status + j); const u64 f = w & ~kV; if (f == 0) continue; excl += w & kV; if (f == kP) break; --j; }\n";
+      o << "          st_release(status + tile, kP | (excl + run));\n";
+      o << "        }\n";
+      o << "        if (tile == ntiles - 1) *(u64*)a.p[" << count_p << "] = excl + run;\n";
+      o << "        s_excl = (i64)excl;\n";
+      o << "      }\n";
+      o << "      __syncthreads();\n";
+      o << "      const i64 base = s_excl + s_warp[warp] + inc - c;\n";
+      o << "      __syncthreads();\n";   // s_warp / s_excl reused by the next tile
+      for (int i = 0; i < S.n_out; ++i) {
+        const int s = S.out_slot[i];
+        const int dt = S.out[i].dtype;
+        const char* t = ctype(dt);
+        o << "      { " << t << "* dst = (" << t << "*)a.p[" << out_p[i] << "]; i64 pos = base;\n";
+        o << "#pragma unroll\n        for (int r = 0; r < V; ++r) if ((sel >> r) & 1u) dst[pos++] = (" << t << ")";
+        if (s < 0) o << "(row0 + r);\n";
+        else o << val(s, "r") << ";\n";
+        o << "      }\n";
+      }
+      o << "    }\n";
+    }
+    o << "  }\n";  // tile loop
+
+    // ---- epilogues ----
+    if (S.kind == SCX_SINK_AGG_DENSE && dense_reg) {
+      o << "  __shared__ i64 red[" << kTPB / 32 << "][" << NC * M << "];\n";
+      for (int c = 0; c < NC; ++c)
+        for (int m = 0; m < M; ++m) {
+          const int op = S.m[m].op;
+          const char* f = op == SCX_AGG_MIN ? "wmin" : op == SCX_AGG_MAX ? "wmax" : "wsum";
+          o << "  { const i64 v = " << f << "(acc[" << c << "][" << m << "]); if (lane == 0) red[warp][" << c * M + m << "] = v; }\n";
+        }
+      o << "  __syncthreads();\n";
+      o << "  if (tid < " << NC * M << ") {\n";
+      o << "    const int c = tid / " << M << ", m = tid % " << M << ";\n";
+      o << "    i64* gacc = (i64*)a.p[" << acc_p << "] + 2 * (c * " << M << " + m);\n";
+      o << "    const int op = ";
+      for (int m = 0; m < M; ++m) o << "m == " << m << " ? " << S.m[m].op << " : ";
+      o << "0;\n";
+      o << "    if (op == " << SCX_AGG_MIN << " || op == " << SCX_AGG_MAX << ") {\n";
+      o << "      i64 v = red[0][tid];\n";
+      o << "      for (int w = 1; w < " << kTPB / 32 << "; ++w) { const i64 x = red[w][tid]; v = op == " << SCX_AGG_MIN << " ? (x < v ? x : v) : (x > v ? x : v); }\n";
+      o << "      if (op == " << SCX_AGG_MIN << ") { if (v != 0x7fffffffffffffffll) atomicMin((long long*)gacc, v); }\n";
+      o << "      else { if (v != (-0x7fffffffffffffffll - 1)) atomicMax((long long*)gacc, v); }\n";
+      o << "    } else {\n";
+      o << "      u64 lo = 0; i64 hi = 0;\n";
+      o << "      for (int w = 0; w < " << kTPB / 32 << "; ++w) { const i64 v = red[w][tid]; const u64 s2 = lo + (u64)v; hi += (v < 0 ? -1 : 0) + (s2 < lo ? 1 : 0); lo = s2; }\n";
+      o << "      if (lo) atomic_add_i128(gacc, (i64)lo);\n";
+      o << "      if (hi) atomicAdd((unsigned long long*)(gacc + 1), (unsigned long long)hi);\n";
+      o << "    }\n  }\n";
+    } else if (S.kind == SCX_SINK_AGG_DENSE) {
+      o << "  __syncthreads();\n";
+      o << "  for (int i = tid; i < " << (int64_t)S.n_cells * M << "; i += " << kTPB << ") {\n";
+      o << "    const int m = i % " << M << ";\n";
+      o << "    const i64 v = tab[i];\n";
+      o << "    i64* gacc = (i64*)a.p[" << acc_p << "] + 2 * (i64)i;\n";
+      o << "    const int op = ";
+      for (int m = 0; m < M; ++m) o << "m == " << m << " ? " << S.m[m].op << " : ";
+      o << "0;\n";
+      o << "    if (op == " << SCX_AGG_MIN << ") { if (v != 0x7fffffffffffffffll) atomicMin((long long*)gacc, v); }\n";
+      o << "    else if (op == " << SCX_AGG_MAX << ") { if (v != (-0x7fffffffffffffffll - 1)) atomicMax((long long*)gacc, v); }\n";
+      o << "    else atomic_add_i128(gacc, v);\n";
+      o << "  }\n";
+    } else if (S.kind == SCX_SINK_COUNT) {
+      o << "  { u64 w = cnt;\n";
+      o << "#pragma unroll\n    for (int d = 16; d > 0; d >>= 1) w += __shfl_xor_sync(0xffffffffu, w, d);\n";
+      o << "    if (lane == 0 && w) atomicAdd((unsigned long long*)a.p[" << count_p << "], (unsigned long long)w); }\n";
+    }
+    o << "}\n";
+    if (!err.empty()) return SCX_EINVAL;
+    if ((int)ptrs.size() > kMaxP) { err = "too many kernel parameters"; return SCX_EUNSUPPORTED; }
+
+    std::string body = g.str() + o.str();
+    name = kernel_name(body);
+    std::string b2 = body;
+    for (size_t k = b2.find("KNAME"); k != std::string::npos; k = b2.find("KNAME", k))
+      b2.replace(k, 5, name);
+    src = std::string("#define MAXP ") + std::to_string(kMaxP) + "\n" + kPrelude + b2;
+    return SCX_OK;
+  }
+};
+
+struct Prepared {
+  std::string src, name;
+  std::vector<uint64_t> ptrs;
+  int tiles = 0;
+  size_t dyn_smem = 0;
+};
+
+static int prepare(const scx_pipeline& P, Prepared& out) {
+  if (P.n_base < 0 || P.n_base > SCX_MAX_BASE || P.n_slots > SCX_MAX_SLOTS || P.n_slots < P.n_base ||
+      P.n_probes < 0 || P.n_probes > SCX_MAX_PROBES) {
+    set_error("pipeline: descriptor counts out of range (base=%d slots=%d probes=%d)", P.n_base,
+              P.n_slots, P.n_probes);
+    return SCX_EINVAL;
+  }
+  if (P.sink.n_measures < 0 || P.sink.n_measures > SCX_MAX_MEASURES || P.sink.n_out > SCX_MAX_OUT) {
+    set_error("pipeline: too many measures/outputs");
+    return SCX_EINVAL;
+  }
+  Gen g(P);
+  int rc = g.generate(out.src, out.name, out.tiles);
+  if (rc) {
+    set_error("jit codegen: %s", g.err.c_str());
+    return rc;
+  }
+  out.ptrs = g.ptrs;
+  out.dyn_smem = g.dyn_smem;
+  return SCX_OK;
+}
+
+static bool enabled() {
+  const char* e = getenv("SCX_JIT");
+  return !(e && e[0] == '0');
+}
+
+}  // namespace jit
+}  // namespace scx
+
+using namespace scx;
+
+extern "C" int64_t scx_pipeline_status_words(const scx_pipeline* d) {
+  if (!d) return 0;
+  if (!jit::enabled()) return interp_status_words(d);
+  jit::Prepared pp;
+  if (jit::prepare(*d, pp)) return -1;
+  return pp.tiles;
+}
+
+extern "C" int scx_pipeline_run(const scx_pipeline* d, void* stream) {
+  if (!d) { set_error("pipeline: null descriptor"); return SCX_EINVAL; }
+  if (!jit::enabled()) return interp_pipeline_run(d, stream);
+  const scx_pipeline& P = *d;
+  if (P.n_rows < 0) { set_error("pipeline: negative n_rows"); return SCX_EINVAL; }
+  if (P.n_rows == 0) {
+    if ((P.sink.kind == SCX_SINK_COMPACT || P.sink.kind == SCX_SINK_COUNT) && P.sink.count)
+      SCX_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(P.sink.count), 0, 8, (cudaStream_t)stream));
+    return SCX_OK;
+  }
+  if (P.sink.kind == SCX_SINK_AGG_DENSE && P.sink.n_cells < 1) {
+    set_error("pipeline: dense sink needs n_cells >= 1");
+    return SCX_EINVAL;
+  }
+  jit::Prepared pp;
+  int rc = jit::prepare(P, pp);
+  if (rc) return rc;
+  jit::Entry* e = nullptr;
+  rc = jit::get_function(pp.src, pp.name, e);
+  if (rc) return rc;
+  jit::Driver& drv = jit::driver();
+  if ((int)pp.dyn_smem > e->max_dyn_smem) {
+    int cr = drv.set_attr(e->fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/,
+                          (int)pp.dyn_smem);
+    if (cr) return jit::drv_fail(cr, "cuFuncSetAttribute");
+    e->max_dyn_smem = (int)pp.dyn_smem;
+  }
+  int occ = 0;
+  int cr = drv.occupancy(&occ, e->fn, jit::kTPB, pp.dyn_smem);
+  if (cr) return jit::drv_fail(cr, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (occ < 1) { set_error("jit kernel does not fit an SM"); return SCX_EUNSUPPORTED; }
+  int dev = 0, sms = 0;
+  SCX_CUDA(cudaGetDevice(&dev));
+  SCX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // all CTAs co-resident (the compaction look-back waits on predecessors)
+  int64_t grid = (int64_t)sms * occ;
+  if (grid > pp.tiles) grid = pp.tiles;
+  if (grid < 1) grid = 1;
+  struct {
+    int64_t n;
+    uint64_t p[jit::kMaxP];
+  } args;
+  memset(&args, 0, sizeof(args));
+  args.n = P.n_rows;
+  for (size_t i = 0; i < pp.ptrs.size(); ++i) args.p[i] = pp.ptrs[i];
+  void* params[] = {&args};
+  cr = drv.launch(e->fn, (unsigned)grid, 1, 1, jit::kTPB, 1, 1, (unsigned)pp.dyn_smem, stream,
+                  params, nullptr);
+  if (cr) return jit::drv_fail(cr, "cuLaunchKernel");
+  SCX_CHECK_LAUNCH("scx_pipe (jit)");
+  return SCX_OK;
+}
+
+// generated CUDA source of a descriptor (no device needed); returns the
+// source length, copies up to cap-1 bytes + NUL into buf
+extern "C" int64_t scx_pipeline_source(const scx_pipeline* d, char* buf, int64_t cap) {
+  if (!d) { set_error("null descriptor"); return SCX_EINVAL; }
+  jit::Prepared pp;
+  int rc = jit::prepare(*d, pp);
+  if (rc) return rc;
+  if (buf && cap > 0) {
+    const int64_t n = (int64_t)pp.src.size() < cap - 1 ? (int64_t)pp.src.size() : cap - 1;
+    memcpy(buf, pp.src.data(), (size_t)n);
+    buf[n] = '\0';
+  }
+  return (int64_t)pp.src.size();
+}
+
+// codegen + NVRTC compile (to the disk cache) without a device: lets the
+// CPU test-suite prove every plan's kernel compiles for sm_100a
+extern "C" int scx_pipeline_compile(const scx_pipeline* d) {
+  if (!d) { set_error("null descriptor"); return SCX_EINVAL; }
+  jit::Prepared pp;
+  int rc = jit::prepare(*d, pp);
+  if (rc) return rc;
+  std::string cubin;
+  bool disk = false;
+  return jit::get_cubin(pp.src, pp.name, cubin, disk);
+}
+
+extern "C" int scx_jit_stats(int64_t* compiled, int64_t* disk_hits, int64_t* mem_hits) {
+  std::lock_guard<std::mutex> g(jit::g_mu);
+  if (compiled) *compiled = jit::g_stats.compiled;
+  if (disk_hits) *disk_hits = jit::g_stats.disk_hits;
+  if (mem_hits) *mem_hits = jit::g_stats.mem_hits;
+  return SCX_OK;
+}

@@ -935,15 +935,17 @@ static int launch_r(const scx_pipeline& P, const Launch& L, cudaStream_t st) {
 
 }  // namespace scx
 
-extern "C" int64_t scx_pipeline_status_words(const scx_pipeline* d) {
+namespace scx {
+// descriptor-interpreting path (SCX_JIT=0): kept as an A/B baseline for the
+// plan-specialised kernels in jit.cu
+int64_t interp_status_words(const scx_pipeline* d) {
   if (!d) return 0;
   scx::Launch L;
   if (scx::plan_launch(*d, L) != SCX_OK) return -1;
   return L.K.n_tiles;
 }
 
-extern "C" int scx_pipeline_run(const scx_pipeline* d, void* stream) {
-  using namespace scx;
+int interp_pipeline_run(const scx_pipeline* d, void* stream) {
   if (!d) { set_error("pipeline: null descriptor"); return SCX_EINVAL; }
   const scx_pipeline& P = *d;
   if (P.n_rows < 0) { set_error("pipeline: negative n_rows"); return SCX_EINVAL; }
@@ -970,3 +972,4 @@ extern "C" int scx_pipeline_run(const scx_pipeline* d, void* stream) {
   if (L.nc == 8) return launch_r<8, 6>(P, L, st);
   return launch_r<0, 0>(P, L, st);
 }
+}  // namespace scx

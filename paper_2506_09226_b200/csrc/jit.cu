@@ -658,6 +658,16 @@ struct Gen {
     V = (row_bytes + payload_bytes <= 24 && max_w <= 4) ? 16 : 8;
     if (S.kind == SCX_SINK_AGG_DENSE && S.n_cells > 1 && S.n_cells <= 8) V = 8;
     if (S.kind == SCX_SINK_AGG_HASH) V = 8;
+    {
+      // register budget for 2 CTAs/SM (<= 128 regs): raw row words + dense
+      // register accumulators; narrower chunks trade load width for occupancy
+      const int acc_regs = (S.kind == SCX_SINK_AGG_DENSE && S.n_cells <= 8)
+                               ? 2 * (S.n_cells < 1 ? 1 : S.n_cells) * S.n_measures : 0;
+      int probe_regs = 0;   // per row: idx + transient key / slot / first-probe words
+      for (int p = 0; p < P.n_probes; ++p)
+        probe_regs += P.probe[p].table.kind == SCX_HT_HASH ? 7 : 3;
+      while (V > 4 && V * (row_bytes + payload_bytes) / 4 + V * probe_regs + acc_regs > 64) V /= 2;
+    }
     const int64_t tile_rows = (int64_t)kTPB * V;
     tiles_out = (int)((P.n_rows + tile_rows - 1) / tile_rows);
 
@@ -665,7 +675,7 @@ struct Gen {
     const int M = S.n_measures;
     const int NC = dense_reg ? (S.n_cells < 1 ? 1 : S.n_cells) : 0;
 
-    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ") KNAME(const __grid_constant__ Args a) {\n";
+    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", 2) KNAME(const __grid_constant__ Args a) {\n";
     o << "  constexpr int V = " << V << ";\n";
     o << "  const i64 n = a.n;\n";
     o << "  const i64 ntiles = (n + " << tile_rows << "ll - 1) / " << tile_rows << "ll;\n";

@@ -132,11 +132,11 @@ def test_codegen_compiles_for_sm100a(lib, name):
     cache = os.environ["SCX_JIT_CACHE"]
     cubins = [f for f in os.listdir(cache) if f.endswith(".cubin")]
     assert cubins
-    kname = src.split("void __launch_bounds__(256) ")[1].split("(")[0]
+    kname = src.split("void __launch_bounds__(256, 2) ")[1].split("(")[0]
     res = subprocess.run(["cuobjdump", "-res-usage", os.path.join(cache, kname + ".cubin")],
                          capture_output=True, text=True)
     if res.returncode == 0:
-        assert "LOCAL:0" in res.stdout, res.stdout      # no register spills
+        assert "LOCAL:0" in res.stdout and "STACK:0" in res.stdout, res.stdout   # no spills
 
 
 def test_source_is_deterministic_and_pointer_free(lib):

@@ -53,7 +53,8 @@ extern "C" {
 #define SCX_MAX_ATOMS     40
 #define SCX_MAX_SETWORDS  128  /* dictionary-set bitmaps, 32 codes / word   */
 #define SCX_MAX_LUT       512  /* dictionary code -> string-rank tables     */
-#define SCX_MAX_PROBES    3
+#define SCX_MAX_PROBES    5
+#define SCX_MAX_POLYS     4    /* polynomial comparison atoms per pipeline  */
 #define SCX_MAX_PAYLOAD   6
 #define SCX_MAX_MEASURES  8
 #define SCX_MAX_GKEYS     4
@@ -65,11 +66,19 @@ extern "C" {
 #define SCX_ATOM_SET    1      /* bit v[slot] of setwords[set_word..] is 1;
                                   lo = number of bitmap words of the set     */
 #define SCX_ATOM_DIFF   2      /* lo <= v[slot] - v[slot2] <= hi              */
+#define SCX_ATOM_POLY   3      /* lo <= polys[slot](row) <= hi: exact int64
+                                  polynomial of slots (scx_measure form)      */
 
 /* join kinds for a probe stage (relops.py:59-94) */
 #define SCX_JOIN_SEMI   0
 #define SCX_JOIN_ANTI   1
 #define SCX_JOIN_INNER  2      /* build keys unique: 0/1 match per probe row  */
+#define SCX_JOIN_LEFT   3      /* left outer, unique build keys: every probe
+                                  row kept, payload = 0 when unmatched       */
+
+/* key component transforms (scx_keyspec.xform, 8 bits per component) */
+#define SCX_XFORM_NONE  0
+#define SCX_XFORM_YEAR  1      /* civil year of a date32 (days since 1970)    */
 
 /* lookup-table kinds */
 #define SCX_HT_HASH     0      /* open addressing, u64 keys, linear probing   */
@@ -140,13 +149,14 @@ typedef struct scx_measure {
 } scx_measure;
 
 /* key spec shared by probes, builds, group keys and partitioning:
- * packed = sum_k (v[slot_k] - lo_k) << shift_k  (must fit 64 bits). */
+ * packed = sum_k (f_k(v[slot_k]) - lo_k) << shift_k  (must fit 64 bits),
+ * f_k = identity or the xform of component k (group keys only). */
 typedef struct scx_keyspec {
   int32_t n;
   int32_t slot[SCX_MAX_KEYS];
   int32_t shift[SCX_MAX_KEYS];
   int32_t bits[SCX_MAX_KEYS];  /* component k must lie in [0, 2^bits_k)   */
-  int32_t _pad;
+  int32_t xform;               /* byte k: SCX_XFORM_* applied to v[slot_k] */
   int64_t lo[SCX_MAX_KEYS];
 } scx_keyspec;
 
@@ -177,7 +187,9 @@ typedef struct scx_sink {
   scx_keyspec gkey;
   int32_t gcard[SCX_MAX_GKEYS];   /* DENSE: domain size of key k          */
   int32_t glut[SCX_MAX_GKEYS];    /* DENSE: offset into lut[] or -1       */
-  int32_t n_cells;                /* DENSE: prod(gcard)                   */
+  int32_t n_cells;                /* DENSE: prod(gcard); HASH: 1 = direct-
+                                     addressed (slot = packed key, gcap =
+                                     key domain), 0 = open addressing    */
   int32_t n_out;                  /* COMPACT: output columns              */
   uint64_t acc;        /* DENSE: {u64 lo, i64 hi}[cells][M]; HASH: i64[cap][M] */
   uint64_t gkeys;      /* HASH: u64[cap] packed group keys                 */
@@ -202,6 +214,7 @@ typedef struct scx_pipeline {
   scx_probe probe[SCX_MAX_PROBES];
   scx_sink sink;
   scx_atom atoms[SCX_MAX_ATOMS];
+  scx_measure polys[SCX_MAX_POLYS];  /* operands of SCX_ATOM_POLY atoms      */
   uint32_t setwords[SCX_MAX_SETWORDS];
   int16_t lut[SCX_MAX_LUT];
 } scx_pipeline;
@@ -260,6 +273,12 @@ int scx_dense_reduce(const int64_t* acc_dev, int n_ranks, int cells, int m,
 int scx_hash_agg_compact(const uint64_t* gkeys_dev, const int64_t* acc_dev,
                          int64_t cap, int m, uint64_t* out_keys_dev,
                          int64_t* out_acc_dev, uint64_t* count_dev, void* stream);
+
+/* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
+ * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not
+ * fit (group_aggregate output, relops.py:138-158). */
+int scx_i128_narrow(const int64_t* lo_dev, const int64_t* hi_dev, int64_t n, int64_t* out_dev,
+                    uint32_t* flag_dev, void* stream);
 
 /* ---- key unpack / convert ------------------------------------------------ */
 /* out[i] = ((packed[i] >> shift) & mask) + lo, stored as dtype */

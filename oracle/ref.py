@@ -298,9 +298,15 @@ def q19(T):
 QUERIES = {"Q1": q1, "Q3": q3, "Q6": q6, "Q12": q12, "Q14": q14, "Q19": q19}
 
 
+def all_queries() -> dict:
+    """The reference's six drivers + the builder-written 16 (oracle/tpch_ext.py)."""
+    from . import tpch_ext
+    return {**QUERIES, **tpch_ext.QUERIES}
+
+
 def reference_run(qid: str, tables):
     """Single-context ground truth (engine.py:463-469)."""
-    return QUERIES[qid](tables)
+    return all_queries()[qid](tables)
 
 
 def to_jsonable(t) -> dict:

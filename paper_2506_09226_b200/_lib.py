@@ -18,9 +18,11 @@ LIB_PATH = os.path.join(HERE, "libscx.so")
 # ---- constants (scx.h) ---------------------------------------------------
 SCX_I8, SCX_I16, SCX_I32, SCX_I64, SCX_U8, SCX_U16, SCX_F64, SCX_U32 = range(8)
 MAX_BASE, MAX_SLOTS, MAX_ATOMS, MAX_SETWORDS, MAX_LUT = 12, 20, 40, 128, 512
-MAX_PROBES, MAX_PAYLOAD, MAX_MEASURES, MAX_GKEYS, MAX_OUT, MAX_KEYS = 3, 6, 8, 4, 16, 4
-ATOM_RANGE, ATOM_SET, ATOM_DIFF = 0, 1, 2
-JOIN_SEMI, JOIN_ANTI, JOIN_INNER = 0, 1, 2
+MAX_PROBES, MAX_PAYLOAD, MAX_MEASURES, MAX_GKEYS, MAX_OUT, MAX_KEYS = 5, 6, 8, 4, 16, 4
+MAX_POLYS = 4
+ATOM_RANGE, ATOM_SET, ATOM_DIFF, ATOM_POLY = 0, 1, 2, 3
+XFORM_NONE, XFORM_YEAR = 0, 1
+JOIN_SEMI, JOIN_ANTI, JOIN_INNER, JOIN_LEFT = 0, 1, 2, 3
 HT_HASH, HT_DIRECT = 0, 1
 AGG_SUM, AGG_COUNT, AGG_MIN, AGG_MAX = 0, 1, 2, 3
 SINK_AGG_DENSE, SINK_AGG_HASH, SINK_COMPACT, SINK_COUNT = 0, 1, 2, 3
@@ -64,7 +66,7 @@ class Measure(C.Structure):
 
 class KeySpec(C.Structure):
     _fields_ = [("n", i32), ("slot", i32 * MAX_KEYS), ("shift", i32 * MAX_KEYS),
-                ("bits", i32 * MAX_KEYS), ("_pad", i32), ("lo", i64 * MAX_KEYS)]
+                ("bits", i32 * MAX_KEYS), ("xform", i32), ("lo", i64 * MAX_KEYS)]
 
 
 class Lookup(C.Structure):
@@ -88,7 +90,8 @@ class Pipeline(C.Structure):
     _fields_ = [("n_rows", i64), ("n_base", i32), ("n_slots", i32), ("n_probes", i32),
                 ("_pad", i32), ("base", Column_ * MAX_BASE), ("slot_dtype", i32 * MAX_SLOTS),
                 ("pre", Pred), ("post", Pred), ("probe", Probe * MAX_PROBES), ("sink", Sink),
-                ("atoms", Atom * MAX_ATOMS), ("setwords", u32 * MAX_SETWORDS),
+                ("atoms", Atom * MAX_ATOMS), ("polys", Measure * MAX_POLYS),
+                ("setwords", u32 * MAX_SETWORDS),
                 ("lut", i16 * MAX_LUT)]
 
 
@@ -113,6 +116,7 @@ _PROTOS = {
                                    C.POINTER(KeySpec), i64, _vp, _vp]),
     "scx_dense_reduce": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp]),
     "scx_hash_agg_compact": (C.c_int, [_vp, _vp, i64, C.c_int, _vp, _vp, _vp, _vp]),
+    "scx_i128_narrow": (C.c_int, [_vp, _vp, i64, _vp, _vp, _vp]),
     "scx_unpack_key": (C.c_int, [_vp, i64, C.c_int, u64, i64, Column_, _vp]),
     "scx_fixed_to_f64": (C.c_int, [_vp, i64, i64, C.c_int, _vp, i64, _vp, _vp]),
     "scx_sort_workspace": (i64, [i64]),

@@ -313,6 +313,16 @@ static __device__ __forceinline__ i64 wmax(i64 v) {
   for (int o = 16; o > 0; o >>= 1) { i64 w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
   return v;
 }
+// proleptic Gregorian year of a day count since 1970-01-01 (civil_from_days)
+static __device__ __forceinline__ i64 civil_year(i64 d) {
+  const i64 z = d + 719468;
+  const i64 era = (z >= 0 ? z : z - 146096) / 146097;
+  const i64 doe = z - era * 146097;
+  const i64 yoe = (doe - doe / 1460 + doe / 36524 - doe / 146096) / 365;
+  const i64 doy = doe - (365 * yoe + yoe / 4 - yoe / 100);
+  const i64 mp = (5 * doy + 2) / 153;
+  return yoe + era * 400 + (mp >= 10 ? 1 : 0);
+}
 static __device__ __forceinline__ i64 smin(i64 a, i64 b) { return a < b ? a : b; }
 static __device__ __forceinline__ i64 smax(i64 a, i64 b) { return a > b ? a : b; }
 #define X1S(w, r) ((i32)(i8)((w)[(r) >> 2] >> (((r) & 3) * 8)))
@@ -393,23 +403,20 @@ struct Gen {
     const uint32_t* w = P.setwords + A.set_word;
     char b[160];
     if (nw <= 1) {
-      snprintf(b, sizeof(b), "((u32)(%s) < 32u && ((0x%08xu >> (u32)(%s)) & 1u))", v.c_str(),
-               w[0], v.c_str());
-      return b;
+      snprintf(b, sizeof(b), "0x%08xu", w[0]);
+      return "((u32)(" + v + ") < 32u && ((" + b + " >> (u32)(" + v + ")) & 1u))";
     }
     if (nw == 2) {
       const uint64_t m = (uint64_t)w[0] | ((uint64_t)w[1] << 32);
-      snprintf(b, sizeof(b), "((u32)(%s) < 64u && ((%s >> (u32)(%s)) & 1ull))", v.c_str(),
-               ulit64(m).c_str(), v.c_str());
-      return b;
+      return "((u32)(" + v + ") < 64u && ((" + ulit64(m) + " >> (u32)(" + v + ")) & 1ull))";
     }
     const int id = n_globals++;
     g << "static __device__ const u32 SET" << id << "[" << nw << "] = {";
     for (int i = 0; i < nw; ++i) g << (i ? "," : "") << w[i] << "u";
     g << "};\n";
-    snprintf(b, sizeof(b), "((u32)(%s) < %du && ((__ldg(SET%d + ((u32)(%s) >> 5)) >> ((u32)(%s) & 31u)) & 1u))",
-             v.c_str(), nw * 32, id, v.c_str(), v.c_str());
-    return b;
+    const std::string ids = std::to_string(id);
+    return "((u32)(" + v + ") < " + std::to_string(nw * 32) + "u && ((__ldg(SET" + ids +
+           " + ((u32)(" + v + ") >> 5)) >> ((u32)(" + v + ") & 31u)) & 1u))";
   }
 
   std::string range_expr(const std::string& v, bool narrow, int64_t lo, int64_t hi) {
@@ -421,23 +428,28 @@ struct Gen {
       if (lo > hi) return "false";
       if (lo == INT32_MIN && hi == INT32_MAX) return "true";
       const uint32_t span = (uint32_t)((int64_t)hi - lo);
-      snprintf(b, sizeof(b), "((u32)(%s) - (u32)(%d) <= %uu)", v.c_str(), (int32_t)lo, span);
-      return b;
+      return "((u32)(" + v + ") - (u32)(" + std::to_string((int32_t)lo) + ") <= " +
+             std::to_string(span) + "u)";
     }
     const uint64_t span = (uint64_t)hi - (uint64_t)lo;
-    snprintf(b, sizeof(b), "((u64)(i64)(%s) - (u64)%s <= %s)", v.c_str(), lit64(lo).c_str(),
-             ulit64(span).c_str());
-    return b;
+    return "((u64)(i64)(" + v + ") - (u64)" + lit64(lo) + " <= " + ulit64(span) + ")";
   }
 
   std::string atom_expr(const scx_atom& A, const char* r) {
     std::string e;
-    if (A.slot < 0 || A.slot >= P.n_slots) { err = "atom slot out of range"; return "false"; }
-    const int dt = P.slot_dtype[A.slot];
+    if (A.op != SCX_ATOM_POLY && (A.slot < 0 || A.slot >= P.n_slots)) {
+      err = "atom slot out of range";
+      return "false";
+    }
+    const int dt = A.op == SCX_ATOM_POLY ? SCX_I64 : P.slot_dtype[A.slot];
     if (A.op == SCX_ATOM_RANGE) {
       e = range_expr(val(A.slot, r), fits32_dt(dt), A.lo, A.hi);
     } else if (A.op == SCX_ATOM_SET) {
       e = set_expr(A, val(A.slot, r));
+    } else if (A.op == SCX_ATOM_POLY) {
+      if (A.slot < 0 || A.slot >= SCX_MAX_POLYS) { err = "poly atom index out of range"; return "false"; }
+      e = range_expr(poly_value(P.polys[A.slot], r), false, A.lo, A.hi);
+      return A.negate ? "(!" + e + ")" : e;
     } else if (A.op == SCX_ATOM_DIFF) {
       if (A.slot2 < 0 || A.slot2 >= P.n_slots) { err = "atom slot2 out of range"; return "false"; }
       const std::string d = "((i64)" + val(A.slot, r) + " - (i64)" + val(A.slot2, r) + ")";
@@ -487,7 +499,7 @@ struct Gen {
                 const std::string& kv, const std::string& kin) {
     o << "      u64 " << kv << " = 0; bool " << kin << " = true;\n";
     for (int i = 0; i < K.n; ++i) {
-      std::string v = "((i64)" + val(K.slot[i], r) + " - " + lit64(K.lo[i]) + ")";
+      std::string v = "(" + key_value(K, i, r) + " - " + lit64(K.lo[i]) + ")";
       if (glut && glut[i] >= 0) {
         int n = lut_n;
         if (n < 0) {   // hash group key: LUT covers the key's bit range
@@ -511,33 +523,54 @@ struct Gen {
     char b[200];
     if (narrow) {
       if (F.a == 0 && F.b == 1) return "((i32)" + v + ")";
-      snprintf(b, sizeof(b), "((i32)(%d) + (i32)(%d) * (i32)%s)", (int)F.a, (int)F.b, v.c_str());
-      return b;
+      return "((i32)(" + std::to_string((int)F.a) + ") + (i32)(" + std::to_string((int)F.b) +
+             ") * (i32)" + v + ")";
     }
     if (F.a == 0 && F.b == 1) return "((i64)" + v + ")";
     return "(" + lit64(F.a) + " + " + lit64(F.b) + " * (i64)" + v + ")";
   }
 
-  std::string measure_expr(const scx_measure& M, const char* r) {
+  // sum_t coef_t * prod_f (a_f + b_f * v[slot_f]) in exact int64
+  std::string poly_value(const scx_measure& M, const char* r) {
     std::string e;
-    if (M.op == SCX_AGG_COUNT) {
-      e = "1ll";
-    } else {
-      for (int t = 0; t < M.n_terms; ++t) {
-        const scx_term& T = M.t[t];
-        std::string p;
-        for (int f = 0; f < T.n_factors; ++f) {
-          const std::string fx = factor(T.f[f], r);
-          p = p.empty() ? "(i64)" + fx : "(" + p + " * " + fx + ")";
-        }
-        if (p.empty()) p = lit64(T.coef);
-        else if (T.coef != 1) p = "(" + lit64(T.coef) + " * " + p + ")";
-        e += (e.empty() ? "" : " + ") + p;
+    if (M.n_terms < 0 || M.n_terms > 2) { err = "polynomial with more than 2 terms"; return "0ll"; }
+    for (int t = 0; t < M.n_terms; ++t) {
+      const scx_term& T = M.t[t];
+      if (T.n_factors < 0 || T.n_factors > 3) { err = "term with more than 3 factors"; return "0ll"; }
+      std::string p;
+      for (int f = 0; f < T.n_factors; ++f) {
+        if (T.f[f].slot >= P.n_slots) { err = "factor slot out of range"; return "0ll"; }
+        const std::string fx = factor(T.f[f], r);
+        p = p.empty() ? "(i64)" + fx : "(" + p + " * " + fx + ")";
       }
-      if (e.empty()) e = "0ll";
+      if (p.empty()) p = lit64(T.coef);
+      else if (T.coef != 1) p = "(" + lit64(T.coef) + " * " + p + ")";
+      e += (e.empty() ? "" : " + ") + p;
     }
-    if (M.cond_atom >= 0) e = "((" + atom_expr(P.atoms[M.cond_atom], r) + ") ? (i64)(" + e + ") : 0ll)";
+    if (e.empty()) e = "0ll";
     return "(i64)(" + e + ")";
+  }
+
+  std::string measure_expr(const scx_measure& M, const char* r) {
+    std::string e = M.op == SCX_AGG_COUNT ? std::string("1ll") : poly_value(M, r);
+    if (M.cond_atom >= 0) {
+      // a gated-off row contributes the aggregate's identity
+      const char* id = M.op == SCX_AGG_MIN ? "0x7fffffffffffffffll"
+                     : M.op == SCX_AGG_MAX ? "(-0x7fffffffffffffffll - 1)" : "0ll";
+      if (M.cond_atom >= SCX_MAX_ATOMS) { err = "cond atom out of range"; return "0ll"; }
+      e = "((" + atom_expr(P.atoms[M.cond_atom], r) + ") ? (i64)(" + e + ") : " + id + ")";
+    }
+    return "(i64)(" + e + ")";
+  }
+
+  // key component value with its transform
+  std::string key_value(const scx_keyspec& K, int i, const char* r) {
+    const int xf = (K.xform >> (8 * i)) & 0xff;
+    const std::string v = "(i64)" + val(K.slot[i], r);
+    if (xf == SCX_XFORM_NONE) return v;
+    if (xf == SCX_XFORM_YEAR) return "(i64)civil_year((i64)" + val(K.slot[i], r) + ")";
+    err = "unknown key transform";
+    return v;
   }
 
   // ---- pieces of the kernel ----
@@ -592,8 +625,10 @@ struct Gen {
     const int keys_p = param(pb.table.keys);
     const int vals_p = param(pb.table.vals);
     const int cap_p = param(pb.table.cap);
+    if (pb.kind < SCX_JOIN_SEMI || pb.kind > SCX_JOIN_LEFT) { err = "unknown join kind"; return; }
     o << "    // probe " << pi << " (" << (pb.kind == SCX_JOIN_SEMI ? "semi" :
-                                          pb.kind == SCX_JOIN_ANTI ? "anti" : "inner") << ", "
+                                          pb.kind == SCX_JOIN_ANTI ? "anti" :
+                                          pb.kind == SCX_JOIN_LEFT ? "left" : "inner") << ", "
       << (pb.table.kind == SCX_HT_DIRECT ? "direct" : "hash") << ")\n";
     o << "    u32 idx" << pi << "[V];\n    {\n";
     o << "      const u32* vals = (const u32*)a.p[" << vals_p << "];\n";
@@ -624,9 +659,10 @@ struct Gen {
     }
     o << "    }\n";
     const bool anti = pb.kind == SCX_JOIN_ANTI;
-    o << "#pragma unroll\n    for (int r = 0; r < V; ++r) if (idx" << pi << "[r] "
-      << (anti ? "!=" : "==") << " SCX_NOROW) sel &= ~(1u << r);\n";
-    if (pb.kind == SCX_JOIN_INNER) {
+    if (pb.kind != SCX_JOIN_LEFT)
+      o << "#pragma unroll\n    for (int r = 0; r < V; ++r) if (idx" << pi << "[r] "
+        << (anti ? "!=" : "==") << " SCX_NOROW) sel &= ~(1u << r);\n";
+    if (pb.kind == SCX_JOIN_INNER || pb.kind == SCX_JOIN_LEFT) {
       for (int j = 0; j < pb.n_payload; ++j) {
         const int s = pb.payload_slot[j];
         const int src_p = param(pb.payload[j].ptr);
@@ -634,7 +670,8 @@ struct Gen {
         o << "    " << t << " pv" << s << "[V];\n";
         o << "    { const " << t << "* src = (const " << t << "*)a.p[" << src_p << "];\n";
         o << "#pragma unroll\n      for (int r = 0; r < V; ++r) pv" << s
-          << "[r] = ((sel >> r) & 1u) ? __ldg(src + idx" << pi << "[r]) : (" << t << ")0; }\n";
+          << "[r] = (((sel >> r) & 1u) && idx" << pi << "[r] != SCX_NOROW) ? __ldg(src + idx" << pi
+          << "[r]) : (" << t << ")0; }\n";
       }
     }
   }
@@ -749,7 +786,7 @@ struct Gen {
       o << "      if (!((sel >> r) & 1u)) continue;\n";
       o << "      int cell = 0;\n";
       for (int i = 0; i < S.gkey.n; ++i) {
-        std::string v = "((i64)" + val(S.gkey.slot[i], "r") + " - " + lit64(S.gkey.lo[i]) + ")";
+        std::string v = "(" + key_value(S.gkey, i, "r") + " - " + lit64(S.gkey.lo[i]) + ")";
         if (S.glut[i] >= 0) v = lut_expr(S.glut[i], S.gcard[i], v);
         o << "      cell = cell * " << S.gcard[i] << " + (int)" << v << ";\n";
       }
@@ -783,18 +820,31 @@ struct Gen {
       // lut length for hash group keys: dictionary size isn't in the keyspec;
       // the LUT region is bounded by SCX_MAX_LUT so emit the whole tail
       o << "      (void)kin;\n";
-      o << "      u64 h = mix64(key) & gmask; u64 slot = SCX_EMPTY;\n";
-      o << "      for (u64 pr = 0; pr <= gmask; ++pr) {\n";
-      o << "        u64 cur = gkeys[h];\n";
-      o << "        if (cur == SCX_EMPTY) { cur = atomicCAS((unsigned long long*)(gkeys + h), SCX_EMPTY, key); if (cur == SCX_EMPTY) cur = key; }\n";
-      o << "        if (cur == key) { slot = h; break; }\n";
-      o << "        h = (h + 1) & gmask;\n      }\n";
+      if (S.n_cells == 1) {
+        // direct-addressed groups: the packed key is the slot (gcap = domain)
+        o << "      u64 slot = SCX_EMPTY;\n";
+        o << "      if (kin && key <= gmask) { slot = key; if (gkeys[slot] != key) gkeys[slot] = key; }\n";
+      } else {
+        // open addressing, linear probing; a probe run longer than 4096 means
+        // the table is (nearly) full: flag it so the host retries larger
+        o << "      u64 h = mix64(key) & gmask; u64 slot = SCX_EMPTY;\n";
+        o << "      for (u64 pr = 0; pr <= gmask && pr < 4096; ++pr) {\n";
+        o << "        u64 cur = gkeys[h];\n";
+        o << "        if (cur == SCX_EMPTY) { cur = atomicCAS((unsigned long long*)(gkeys + h), SCX_EMPTY, key); if (cur == SCX_EMPTY) cur = key; }\n";
+        o << "        if (cur == key) { slot = h; break; }\n";
+        o << "        h = (h + 1) & gmask;\n      }\n";
+      }
       o << "      if (slot == SCX_EMPTY) { atomicOr((u32*)a.p[" << flags_p << "], 1u); continue; }\n";
+      // accumulator words per group: 2 for 128-bit ("wide", measure._pad) sums
+      int W = 0;
+      std::vector<int> woff(M);
+      for (int m = 0; m < M; ++m) { woff[m] = W; W += S.m[m]._pad == 1 ? 2 : 1; }
       for (int m = 0; m < M; ++m) {
         const int op = S.m[m].op;
-        o << "      { const i64 mv = " << measure_expr(S.m[m], "r") << "; long long* t = (long long*)(gacc + slot * " << M << " + " << m << "); ";
+        o << "      { const i64 mv = " << measure_expr(S.m[m], "r") << "; long long* t = (long long*)(gacc + slot * " << W << " + " << woff[m] << "); ";
         if (op == SCX_AGG_MIN) o << "atomicMin(t, mv); }\n";
         else if (op == SCX_AGG_MAX) o << "atomicMax(t, mv); }\n";
+        else if (S.m[m]._pad == 1) o << "atomic_add_i128((i64*)t, mv); }\n";
         else o << "atomicAdd((unsigned long long*)t, (unsigned long long)mv); }\n";
       }
       o << "    }\n";

@@ -800,6 +800,21 @@ static int plan_launch(const scx_pipeline& P, Launch& L) {
               P.n_base, P.n_slots, P.n_probes);
     return SCX_EINVAL;
   }
+  // the interpreter predates poly atoms, key transforms and left joins
+  for (int a = 0; a < SCX_MAX_ATOMS; ++a)
+    if (P.atoms[a].op == SCX_ATOM_POLY) {
+      set_error("interpreter: polynomial atoms need the JIT path (unset SCX_JIT=0)");
+      return SCX_EUNSUPPORTED;
+    }
+  for (int p = 0; p < P.n_probes; ++p)
+    if (P.probe[p].kind == SCX_JOIN_LEFT) {
+      set_error("interpreter: left joins need the JIT path (unset SCX_JIT=0)");
+      return SCX_EUNSUPPORTED;
+    }
+  if (P.sink.gkey.xform != 0) {
+    set_error("interpreter: key transforms need the JIT path (unset SCX_JIT=0)");
+    return SCX_EUNSUPPORTED;
+  }
   uint32_t row_bytes = 0;
   for (int c = 0; c < P.n_base; ++c) {
     if (P.base[c].ptr % 16 != 0) {

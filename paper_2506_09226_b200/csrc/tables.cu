@@ -101,6 +101,16 @@ __global__ void hash_agg_compact_kernel(const uint64_t* gkeys, const int64_t* ac
   }
 }
 
+// 128-bit {lo, hi} -> int64 with an overflow flag (hash-group wide sums)
+__global__ void i128_narrow_kernel(const int64_t* lo, const int64_t* hi, int64_t n, int64_t* out,
+                                   uint32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = lo[i];
+    if (hi[i] != (lo[i] >> 63)) atomicOr(flag, 1u);
+  }
+}
+
 __global__ void unpack_key_kernel(const uint64_t* packed, int64_t n, int shift, uint64_t mask,
                                   int64_t lo, scx_column out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -284,6 +294,15 @@ extern "C" int scx_unpack_key(const uint64_t* packed, int64_t n, int shift, uint
   if (!packed || !out.ptr || shift < 0 || shift > 63) { set_error("unpack_key: bad arguments"); return SCX_EINVAL; }
   unpack_key_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(packed, n, shift, mask, lo, out);
   SCX_CHECK_LAUNCH("unpack_key_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_i128_narrow(const int64_t* lo, const int64_t* hi, int64_t n, int64_t* out,
+                               uint32_t* flag, void* stream) {
+  if (n == 0) return SCX_OK;
+  if (!lo || !hi || !out || !flag) { set_error("i128_narrow: null pointer"); return SCX_EINVAL; }
+  i128_narrow_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(lo, hi, n, out, flag);
+  SCX_CHECK_LAUNCH("i128_narrow_kernel");
   return SCX_OK;
 }
 

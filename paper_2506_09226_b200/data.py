@@ -58,7 +58,13 @@ CONTAINERS = tuple(" ".join(w) for w in itertools.product(
     ("SM", "MED", "LG", "JUMBO", "WRAP"),
     ("CASE", "BOX", "BAG", "JAR", "PKG", "PACK", "CAN", "DRUM"),
 ))
-NATION_NAMES = tuple(f"NATION_{i:02d}" for i in range(25))
+# The reference's nation names are placeholders NATION_00..24 (data.py:80);
+# the 22-query extension needs the TPC-H names.  Codes (the stored values)
+# are unchanged, so every reference column stays bit-identical.
+NATION_NAMES = ("ALGERIA", "ARGENTINA", "BRAZIL", "CANADA", "EGYPT", "ETHIOPIA", "FRANCE",
+                "GERMANY", "INDIA", "INDONESIA", "IRAN", "IRAQ", "JAPAN", "JORDAN", "KENYA",
+                "MOROCCO", "MOZAMBIQUE", "PERU", "CHINA", "ROMANIA", "SAUDI ARABIA", "VIETNAM",
+                "RUSSIA", "UNITED KINGDOM", "UNITED STATES")
 REGION_NAMES = ("AFRICA", "AMERICA", "ASIA", "EUROPE", "MIDDLE EAST")
 
 # Logical schema per table (data.py:84-105): (column, reference kind).
@@ -68,19 +74,23 @@ SCHEMAS: dict[str, list[tuple[str, str]]] = {
         ("l_extendedprice", "float64"), ("l_discount", "float64"), ("l_tax", "float64"),
         ("l_returnflag", "dict"), ("l_linestatus", "dict"),
         ("l_shipdate", "date32"), ("l_commitdate", "date32"), ("l_receiptdate", "date32"),
-        ("l_shipinstruct", "dict"), ("l_shipmode", "dict"),
+        ("l_shipinstruct", "dict"), ("l_shipmode", "dict"), ("l_suppkey", "int64"),
     ],
     "orders": [
         ("o_orderkey", "int64"), ("o_custkey", "int64"), ("o_orderdate", "date32"),
-        ("o_orderpriority", "dict"), ("o_shippriority", "int64"),
+        ("o_orderpriority", "dict"), ("o_shippriority", "int64"), ("o_totalprice", "float64"),
+        ("o_orderstatus", "dict"), ("o_comment", "dict"),
     ],
-    "customer": [("c_custkey", "int64"), ("c_mktsegment", "dict"), ("c_nationkey", "int64")],
+    "customer": [("c_custkey", "int64"), ("c_mktsegment", "dict"), ("c_nationkey", "int64"),
+                 ("c_acctbal", "float64")],
     "part": [
         ("p_partkey", "int64"), ("p_brand", "dict"), ("p_type", "dict"),
-        ("p_size", "int64"), ("p_container", "dict"),
+        ("p_size", "int64"), ("p_container", "dict"), ("p_name", "dict"), ("p_mfgr", "dict"),
     ],
-    "partsupp": [("ps_partkey", "int64"), ("ps_suppkey", "int64"), ("ps_supplycost", "float64")],
-    "supplier": [("s_suppkey", "int64"), ("s_nationkey", "int64")],
+    "partsupp": [("ps_partkey", "int64"), ("ps_suppkey", "int64"), ("ps_supplycost", "float64"),
+                 ("ps_availqty", "int64")],
+    "supplier": [("s_suppkey", "int64"), ("s_nationkey", "int64"), ("s_acctbal", "float64"),
+                 ("s_comment", "dict")],
     "nation": [("n_nationkey", "int64"), ("n_name", "dict"), ("n_regionkey", "int64")],
     "region": [("r_regionkey", "int64"), ("r_name", "dict")],
 }
@@ -92,6 +102,7 @@ DICTIONARIES: dict[str, tuple[str, ...]] = {
     "p_brand": BRANDS, "p_type": TYPES, "p_container": CONTAINERS,
     "n_name": NATION_NAMES, "r_name": REGION_NAMES,
 }
+
 
 _ORDERDATE_LO = date_to_days("1992-01-01")
 _ORDERDATE_HI = date_to_days("1998-08-02")
@@ -251,12 +262,140 @@ def generate(sf: float, skew: float = 0.0, seed: int = 0) -> Dataset:
         "r_regionkey": HostColumn.int_range(0, 5),
         "r_name": _dict(np.arange(5), "r_name"),
     })
+    extend_tpch(lineitem, orders, customer, part, partsupp, supplier, seed)
     return Dataset(
         tables={"lineitem": lineitem, "orders": orders, "customer": customer,
                 "part": part, "partsupp": partsupp, "supplier": supplier,
                 "nation": nation, "region": region},
         sf=sf, skew=skew, seed=seed,
     )
+
+
+# ---------------------------------------------------------------------------
+# TPC-H extension for the 16 queries the reference lacks
+#
+# Every new column comes from an RNG stream independent of the reference's
+# ``default_rng(seed)`` (or is a deterministic function of reference
+# columns), so the reference's columns stay bit-identical.  Free-text
+# columns (names, comments) are dictionary-coded over small deterministic
+# vocabularies: LIKE predicates resolve on the host dictionary into code
+# bitmaps, exactly like the reference's ``_codes_where`` (queries.py:23-29).
+# Identity columns the queries only print (c_name = "Customer#<key>",
+# s_name, addresses, phones) are not materialised: results carry the key;
+# c_phone's country code is c_nationkey + 10 (the dbgen rule).
+# ---------------------------------------------------------------------------
+
+COLORS = (
+    "almond antique aquamarine azure beige bisque black blanched blue blush brown burlywood "
+    "burnished chartreuse chiffon chocolate coral cornflower cornsilk cream cyan dark deep dim "
+    "dodger drab firebrick floral forest frosted gainsboro ghost goldenrod green grey honeydew "
+    "hot indian ivory khaki lace lavender lawn lemon light lime linen magenta maroon medium "
+    "metallic midnight mint misty moccasin navajo navy olive orange orchid pale papaya peach "
+    "peru pink plum powder puff purple red rose rosy royal saddle salmon sandy seashell sienna "
+    "sky slate smoke snow spring steel tan thistle tomato turquoise violet wheat white yellow"
+).split()
+_WORDS = ("furiously quickly carefully blithely slyly fluffily regular final ironic express "
+          "bold pending even silent unusual special requests deposits accounts packages "
+          "instructions foxes ideas theodolites pinto beans platelets asymptotes dependencies "
+          "excuses warthogs sheaves courts dolphins sentiments frets").split()
+N_PART_NAMES = 1000
+N_ORDER_COMMENTS = 1024
+N_SUPP_COMMENTS = 256
+ORDER_STATUSES = ("F", "O", "P")
+MANUFACTURERS = tuple(f"Manufacturer#{i}" for i in range(1, 6))
+
+
+def _vocab_rng(tag: int) -> np.random.Generator:
+    return np.random.default_rng(np.random.SeedSequence([2506, 9226, tag]))
+
+
+def _part_names() -> tuple[str, ...]:
+    r = _vocab_rng(1)
+    names, seen = [], set()
+    while len(names) < N_PART_NAMES:
+        w = " ".join(COLORS[i] for i in r.choice(len(COLORS), 5, replace=False))
+        if w not in seen:
+            seen.add(w)
+            names.append(w)
+    return tuple(names)
+
+
+def _comments(tag: int, n: int, plant: tuple[str, str], frac: float) -> tuple[str, ...]:
+    """n distinct comments; about `frac` of them contain plant[0] ... plant[1]."""
+    r = _vocab_rng(tag)
+    out, seen = [], set()
+    while len(out) < n:
+        k = int(r.integers(4, 9))
+        words = [_WORDS[i] for i in r.integers(0, len(_WORDS), k)]
+        if r.random() < frac:
+            i = int(r.integers(0, k - 1))
+            words.insert(i, plant[0])
+            words.insert(int(r.integers(i + 1, len(words) + 1)), plant[1])
+        else:
+            words = [w for w in words if w != plant[0]] or ["even"]
+        c = " ".join(words)
+        if c not in seen:
+            seen.add(c)
+            out.append(c)
+    return tuple(out)
+
+
+DICTIONARIES["p_name"] = _part_names()
+DICTIONARIES["p_mfgr"] = MANUFACTURERS
+DICTIONARIES["o_orderstatus"] = ORDER_STATUSES
+DICTIONARIES["o_comment"] = _comments(2, N_ORDER_COMMENTS, ("special", "requests"), 0.02)
+DICTIONARIES["s_comment"] = _comments(3, N_SUPP_COMMENTS, ("Customer", "Complaints"), 0.04)
+
+
+def extend_tpch(lineitem: HostTable, orders: HostTable, customer: HostTable, part: HostTable,
+                partsupp: HostTable, supplier: HostTable, seed: int) -> None:
+    """Add the columns the 16 extra queries need (in place)."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 22]))
+    n_li, n_ord = lineitem.row_count, orders.row_count
+    n_cust, n_part, n_supp = customer.row_count, part.row_count, supplier.row_count
+    # l_suppkey: one of the part's four partsupp suppliers, so lineitem joins
+    # partsupp on (partkey, suppkey) as in dbgen
+    pk = lineitem.column("l_partkey").values.astype(np.int64)
+    ps_supp = partsupp.column("ps_suppkey").values
+    pick = rng.integers(0, 4, size=n_li)
+    lineitem.columns["l_suppkey"] = HostColumn.from_ints("int64", ps_supp[(pk - 1) * 4 + pick])
+    del pk, pick
+    # o_totalprice = sum over lines of round(ext * (1 + tax) * (1 - disc)), cents
+    ok = lineitem.column("l_orderkey").values
+    line = (lineitem.column("l_extendedprice").values.astype(np.int64)
+            * (100 + lineitem.column("l_tax").values.astype(np.int64))
+            * (100 - lineitem.column("l_discount").values.astype(np.int64)))
+    line = (line + 5000) // 10000
+    starts = np.searchsorted(ok, np.arange(1, n_ord + 2, dtype=np.int64))
+    cs = np.concatenate([[0], np.cumsum(line)])
+    total = cs[starts[1:]] - cs[starts[:-1]]
+    orders.columns["o_totalprice"] = HostColumn.decimal(total, 2)
+    del line, cs, total
+    # o_orderstatus: F if every line is F, O if every line is O, else P
+    f = (lineitem.column("l_linestatus").values == LINE_STATUSES.index("F")).astype(np.int64)
+    cf = np.concatenate([[0], np.cumsum(f)])
+    nf = cf[starts[1:]] - cf[starts[:-1]]
+    nl = starts[1:] - starts[:-1]
+    status = np.where((nf == nl) & (nl > 0), 0, np.where(nf == 0, 1, 2))
+    orders.columns["o_orderstatus"] = _dict(status, "o_orderstatus")
+    del f, cf, nf, nl, status, starts
+    orders.columns["o_comment"] = _dict(rng.integers(0, N_ORDER_COMMENTS, size=n_ord),
+                                        "o_comment")
+    customer.columns["c_acctbal"] = HostColumn.decimal(
+        rng.integers(-99999, 1000000, size=n_cust), 2)
+    part.columns["p_name"] = _dict(rng.integers(0, N_PART_NAMES, size=n_part), "p_name")
+    # p_mfgr follows p_brand (Brand#MN is made by Manufacturer#M), as in dbgen
+    brand = part.column("p_brand").values.astype(np.int64)
+    mfgr = np.asarray([int(BRANDS[i][6]) - 1 for i in range(len(BRANDS))])[brand]
+    part.columns["p_mfgr"] = _dict(mfgr, "p_mfgr")
+    partsupp.columns["ps_availqty"] = HostColumn.from_ints(
+        "int64", rng.integers(1, 10000, size=4 * n_part))
+    supplier.columns["s_acctbal"] = HostColumn.decimal(
+        rng.integers(-99999, 1000000, size=n_supp), 2)
+    supplier.columns["s_comment"] = _dict(rng.integers(0, N_SUPP_COMMENTS, size=n_supp),
+                                          "s_comment")
+    for t in (lineitem, orders, customer, part, partsupp, supplier):
+        t.row_count = next(iter(t.columns.values())).row_count
 
 
 # ---------------------------------------------------------------------------

@@ -57,19 +57,23 @@ def _frac(c) -> Fraction:
 
 @dataclass(frozen=True)
 class Atom:
-    op: str                      # "range" | "set" | "diff"
+    op: str                      # "range" | "set" | "diff" | "poly"
     col: str
     lo: int = INT64_MIN
     hi: int = INT64_MAX
     col2: str | None = None      # diff: value = col - col2
     codes: frozenset = frozenset()  # set: dictionary codes that pass
     negate: bool = False
+    poly: "Poly | None" = field(default=None, compare=False)  # poly: lo <= int form <= hi
+    poly_key: str = ""           # identity of `poly` for atom equality / hashing
 
     def inverted(self) -> "Atom":
         return replace(self, negate=not self.negate)
 
     @property
     def columns(self) -> tuple[str, ...]:
+        if self.op == "poly":
+            return tuple(sorted(self.poly.columns))
         return (self.col,) if self.col2 is None else (self.col, self.col2)
 
 
@@ -167,7 +171,22 @@ class Term:
     factors: tuple[Factor, ...] = ()
 
 
-@dataclass(frozen=True)
+def _poly_cmp(left, right, op: str) -> Pred:
+    """Exact comparison of two polynomials: (left - right) op 0.  The kernel
+    evaluates the integerised difference (a positive multiple of it), so the
+    sign -- and therefore the comparison -- is exact."""
+    d = as_poly(left) - as_poly(right)
+    if d.cond is not None:
+        raise SchemaError("cannot compare a conditional measure")
+    if not d.columns:
+        raise SchemaError("comparison of two constants")
+    rng = {">=": (0, INT64_MAX), ">": (1, INT64_MAX), "<": (INT64_MIN, -1),
+           "<=": (INT64_MIN, 0), "==": (0, 0), "!=": (0, 0)}[op]
+    return Pred.atom(Atom("poly", "", rng[0], rng[1], negate=(op == "!="), poly=d,
+                          poly_key=repr(d.terms)))
+
+
+@dataclass(frozen=True, eq=False)
 class Poly:
     terms: tuple[Term, ...]
     cond: Atom | None = None
@@ -213,6 +232,15 @@ class Poly:
 
     def sum(self):
         return self
+
+    # comparisons build predicates (SQL-style `qty * 5 * cnt < sum_qty`)
+    def __lt__(self, o): return _poly_cmp(self, o, "<")
+    def __le__(self, o): return _poly_cmp(self, o, "<=")
+    def __gt__(self, o): return _poly_cmp(self, o, ">")
+    def __ge__(self, o): return _poly_cmp(self, o, ">=")
+    def __eq__(self, o): return _poly_cmp(self, o, "==")
+    def __ne__(self, o): return _poly_cmp(self, o, "!=")
+    __hash__ = object.__hash__
 
     def __repr__(self) -> str:
         return f"Poly({self.terms}, cond={self.cond})"
@@ -330,14 +358,27 @@ class ColRef:
 
     # ---- comparisons ----
     def _cmp(self, other, op: str) -> Pred:
+        if isinstance(other, Poly):
+            return _poly_cmp(self.poly(), other, op)
         if isinstance(other, ColRef):
+            if (self.col.kind == "float64" and other.col.kind == "float64"
+                    and self.col.scale != other.col.scale):
+                return _poly_cmp(self.poly(), other.poly(), op)
             return self._cmp_col(other, op)
         c = self.col
         if c.kind == "dict":
             raise SchemaError(f"compare dict column {self.name!r} with isin(), not {op}")
         if c.kind == "float64" and c.scale < 0:
             raise SchemaError(f"predicate on raw float64 column {self.name!r}")
-        if c.kind == "float64" and c.scale > 0:
+        if c.kind == "float64" and c.scale > 0 and isinstance(other, (Fraction, int)) \
+                and not isinstance(other, bool):
+            # exact rational literal (e.g. an aggregate read back from the device):
+            # compare the fixed-point integer exactly
+            x = _frac(other) * (10 ** c.scale)
+            fl, ce = math.floor(x), math.ceil(x)
+            rng = {">=": (ce, INT64_MAX), ">": (fl + 1, INT64_MAX), "<": (INT64_MIN, ce - 1),
+                   "<=": (INT64_MIN, fl), "==": (ce, fl), "!=": (ce, fl)}[op]
+        elif c.kind == "float64" and c.scale > 0:
             x = float(other)
             ge = _float_bound(c.scale, x, strict=False)   # first v with f(v) >= x
             gt = _float_bound(c.scale, x, strict=True)    # first v with f(v) >  x
@@ -372,6 +413,32 @@ class ColRef:
 
     def __repr__(self) -> str:
         return f"ColRef({self.name!r}, {self.col!r})"
+
+
+@dataclass(frozen=True)
+class DerivedKey:
+    """A group-by key computed from one column in the kernel: ``year(date)``
+    (SQL ``extract(year from ...)``) and/or a constant offset
+    (``c_nationkey + 10`` = the phone country code)."""
+
+    src: str
+    xform: str = "none"        # "none" | "year"
+    offset: int = 0
+
+    def __add__(self, k):
+        return replace(self, offset=self.offset + int(k))
+
+
+def year(ref: ColRef) -> DerivedKey:
+    if ref.col.kind != "date32":
+        raise SchemaError(f"year() expects a date32 column, {ref.name} is {ref.col.kind}")
+    return DerivedKey(ref.name, "year")
+
+
+def key_of(ref: ColRef, offset: int = 0) -> DerivedKey:
+    if ref.col.kind not in ("int64", "date32"):
+        raise SchemaError(f"derived key over {ref.col.kind} column {ref.name!r}")
+    return DerivedKey(ref.name, "none", int(offset))
 
 
 def isin(ref: ColRef, values) -> Pred:

@@ -30,8 +30,8 @@ from fractions import Fraction
 import numpy as np
 
 from . import _lib as L
-from .expr import (INT64_MAX, INT64_MIN, Atom, ColRef, IntMeasure, Poly, Pred, as_poly,
-                   decimal_exponent, integerise)
+from .expr import (INT64_MAX, INT64_MIN, Atom, ColRef, DerivedKey, IntMeasure, Poly, Pred,
+                   as_poly, decimal_exponent, integerise)
 from .table import Column, ColumnTable, HostColumn, SchemaError, alloc
 
 AGG_OPS = ("sum", "count", "min", "max", "avg")
@@ -191,6 +191,7 @@ class TableView:
         self.probes: list[ProbeStage] = []
         self.post: Pred = Pred.true()
         self.computed: dict[str, Poly] = {}
+        self.derived: dict[str, DerivedKey] = {}
 
     def _copy(self) -> "TableView":
         v = TableView.__new__(TableView)
@@ -202,6 +203,7 @@ class TableView:
         v.probes = list(self.probes)
         v.post = self.post
         v.computed = dict(self.computed)
+        v.derived = dict(self.derived)
         return v
 
     # ---- ColumnTable-like surface ----
@@ -249,7 +251,13 @@ class TableView:
 
     def with_column(self, name: str, col) -> "TableView":
         v = self._copy()
-        if isinstance(col, (Poly, ColRef)):
+        if isinstance(col, DerivedKey):
+            if col.src not in v.meta:
+                raise SchemaError(f"unknown column {col.src!r} for derived key {name!r}")
+            v.derived[name] = col
+            v.meta[name] = derived_meta(v.meta[col.src], col)
+            v.origin[name] = ("derived", col.src)
+        elif isinstance(col, (Poly, ColRef)):
             v.computed[name] = as_poly(col)
         elif isinstance(col, Column):
             if self.probes or not self.pre.is_true:
@@ -278,6 +286,28 @@ class TableView:
     def __repr__(self) -> str:
         return (f"TableView(base_rows={self.base.row_count}, visible={self.visible}, "
                 f"probes={len(self.probes)})")
+
+
+def _civil_year(days: int) -> int:
+    import datetime
+    return (datetime.date(1970, 1, 1) + datetime.timedelta(days=int(days))).year
+
+
+def derived_meta(src: Column, dk: DerivedKey) -> Column:
+    """Metadata (kind, proven range, physical dtype) of a derived group key."""
+    from .table import narrow_dtype
+    if src.hi < src.lo:
+        lo, hi = 0, -1
+    elif dk.xform == "year":
+        lo, hi = _civil_year(src.lo), _civil_year(src.hi)
+    else:
+        lo, hi = src.lo, src.hi
+    lo, hi = lo + dk.offset, hi + dk.offset
+    dt = narrow_dtype(min(lo, 0), max(hi, 0))
+    return Column("int64", alloc(0, dt), 0, None, lo, hi)
+
+
+_XFORM = {"none": L.XFORM_NONE, "year": L.XFORM_YEAR}
 
 
 def as_view(t) -> TableView:
@@ -330,7 +360,7 @@ def filter_table(table, predicate) -> TableView:
 
 def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
     """Equi-join (relops.py:59-94): probe stage appended to the left view."""
-    if how not in ("inner", "semi", "anti"):
+    if how not in ("inner", "semi", "anti", "left"):
         raise SchemaError(f"unknown join type {how!r}")
     if not on:
         raise SchemaError("join requires at least one key pair")
@@ -348,24 +378,31 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
             raise SchemaError(f"column {lname!r} of kind {lc.col.kind} cannot be a key")
         if lc.col.kind == "dict" and lc.col.dictionary != rc.dictionary:
             raise SchemaError(f"join keys {lname}/{rname} have different dictionaries")
-    if how == "inner":
+    if how in ("inner", "left"):
         overlap = set(lv.visible) & set(rt.column_names)
         if overlap:
             raise SchemaError(f"inner join would duplicate columns: {sorted(overlap)}")
     if len(lv.probes) >= L.MAX_PROBES:
         lv = TableView(lv.materialize())
     lookup = Lookup(rt, [r for _, r in on])
-    if how == "inner" and not lookup.unique:
-        raise SchemaError("inner join with duplicate build-side keys is not supported by the "
+    if how in ("inner", "left") and not lookup.unique:
+        raise SchemaError(f"{how} join with duplicate build-side keys is not supported by the "
                           "fused probe (build keys must be unique)")
     v = lv._copy()
-    kind = {"inner": L.JOIN_INNER, "semi": L.JOIN_SEMI, "anti": L.JOIN_ANTI}[how]
+    kind = {"inner": L.JOIN_INNER, "semi": L.JOIN_SEMI, "anti": L.JOIN_ANTI,
+            "left": L.JOIN_LEFT}[how]
     stage = ProbeStage(lookup, [lname for lname, _ in on], kind)
-    if how == "inner":
+    if how in ("inner", "left"):
         pidx = len(v.probes)
         for n in rt.column_names:
             stage.payload.append(n)
-            v.meta[n] = rt.column(n)
+            c = rt.column(n)
+            if how == "left":
+                # unmatched rows read 0 (SQL NULL for count / sum payloads)
+                if c.kind == "dict":
+                    raise SchemaError(f"left join cannot carry dict payload {n!r}")
+                c = Column(c.kind, c.data, c.scale, None, min(c.lo, 0), max(c.hi, 0))
+            v.meta[n] = c
             v.origin[n] = ("payload", pidx, n)
             v.visible.append(n)
     v.probes.append(stage)
@@ -375,6 +412,12 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
 # ---------------------------------------------------------------------------
 # pipeline construction
 # ---------------------------------------------------------------------------
+
+# Optional byte trace for roofline accounting: when set to a set(), every
+# pipeline adds (device address, bytes) of each base column it scans, so
+# the union is the query's distinct HBM bytes read (bench.py).
+TRACE: set | None = None
+
 
 class _Builder:
     """Assigns operand slots and serialises a TableView into scx_pipeline."""
@@ -398,6 +441,8 @@ class _Builder:
         self.slot: dict[str, int] = {}
         for i, n in enumerate(base):
             c = v.meta[n]
+            if TRACE is not None:
+                TRACE.add((c.data.data_ptr(), c.nbytes))
             P.base[i] = c.scx()
             P.slot_dtype[i] = c.scx_dtype
             self.slot[n] = i
@@ -408,6 +453,8 @@ class _Builder:
             P.slot_dtype[s] = v.meta[n].scx_dtype
         P.n_slots = len(base) + len(payload)
         self.n_atoms = 0
+        self.n_polys = 0
+        self.poly_index: dict[str, int] = {}
         self.n_words = 0
         self.n_lut = 0
         self._keep = []   # tensors that must outlive the launch
@@ -435,9 +482,25 @@ class _Builder:
         i = self.n_atoms
         self.n_atoms += 1
         A = self.P.atoms[i]
-        A.slot = self.slot[a.col]
         A.clause = clause
         A.negate = 1 if a.negate else 0
+        if a.op == "poly":
+            k = self.poly_index.get(a.poly_key)      # DNF repeats the same comparison
+            if k is None:
+                if self.n_polys >= L.MAX_POLYS:
+                    raise SchemaError("predicate has too many polynomial comparisons")
+                im = integerise(a.poly, self.v.meta)
+                if _measure_bound(im, self.v.meta) >= (1 << 62):
+                    raise SchemaError("polynomial comparison may overflow 64 bits")
+                k = self.n_polys
+                self.measure(self.P.polys[k], "sum", im)
+                self.poly_index[a.poly_key] = k
+                self.n_polys += 1
+            A.op = L.ATOM_POLY
+            A.slot = k
+            A.lo, A.hi = a.lo, a.hi
+            return i
+        A.slot = self.slot[a.col]
         if a.op == "range":
             A.op = L.ATOM_RANGE
             A.lo, A.hi = a.lo, a.hi
@@ -545,7 +608,7 @@ def _measure_bound(im: IntMeasure, meta: dict[str, Column]) -> int:
 
 def _materialize(v: TableView) -> ColumnTable:
     cols = [n for n in v.visible]
-    comp = [n for n in cols if n in v.computed]
+    comp = [n for n in cols if n in v.computed or n in v.derived]
     if comp:
         raise SchemaError(f"cannot materialise computed columns {comp}; aggregate them instead")
     if not v.probes and v.pre.is_true and v.post.is_true:
@@ -654,7 +717,13 @@ def _plan_aggs(v: TableView, aggs: dict) -> tuple[list[_Agg], list[tuple[str, In
         im = integerise(poly, v.meta)
         if op in ("min", "max"):
             if src is None:
-                raise SchemaError(f"{op} of a computed column is not supported")
+                # min/max of where(cond, col): a single gated column is allowed
+                t = poly.terms
+                if (len(t) == 1 and t[0].coef == 1 and len(t[0].factors) == 1
+                        and t[0].factors[0].a == 0 and t[0].factors[0].b == 1):
+                    src = v.meta[t[0].factors[0].col]
+                else:
+                    raise SchemaError(f"{op} of a computed column is not supported")
             plan.append(_Agg(out, op, poly, src.kind, m=add_measure(op, im), scale=src.scale,
                              src=src))
             continue
@@ -683,13 +752,15 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
             raise SchemaError(f"unknown group key {k!r}")
         if v.meta[k].kind not in _KEY_KINDS:
             raise SchemaError(f"column {k!r} of kind {v.meta[k].kind} cannot be a key")
+    # derived keys read their source column, transformed in the kernel
+    ksrc = [v.derived[k].src if k in v.derived else k for k in keys]
     plan, measures = _plan_aggs(v, aggs)
     if keys and not any(op == "count" for op, _ in measures):
         measures.append(("count", None))     # live-group detection
     count_m = next(i for i, (op, _) in enumerate(measures) if op == "count") if keys else None
     if len(measures) > L.MAX_MEASURES:
         raise SchemaError("too many aggregate measures")
-    names = set(keys)
+    names = set(ksrc)
     for _, im in measures:
         if im is not None:
             names |= {f[2] for _, fs in im.terms for f in fs}
@@ -706,14 +777,19 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
         cards.append(len(c.dictionary) if c.kind == "dict" else max(1, c.hi - c.lo + 1))
     cells = int(np.prod(cards)) if keys else 1
     dense = (not keys and len(measures) <= 8) or (keys and cells <= 8 and len(measures) <= 6)
-    # overflow guard: per-thread int64 partials (dense) / per-group int64 (hash)
+    # overflow guard: per-thread int64 partials (dense; exact 128-bit across
+    # threads); hash groups switch a sum to a 128-bit {lo, hi} accumulator when
+    # n rows of its largest value could leave int64
     n = v.base.row_count
-    for op, im in measures:
+    for i, (op, im) in enumerate(measures):
         if im is not None and op == "sum":
             bound = _measure_bound(im, v.meta)
-            per = (n // (148 * 256) + 16) if dense else max(n, 1)
-            if bound * per >= (1 << 62):
-                raise SchemaError("aggregate may overflow 64-bit partial sums")
+            if dense:
+                if bound * (n // (148 * 256) + 16) >= (1 << 62):
+                    raise SchemaError("aggregate may overflow 64-bit partial sums")
+            elif bound * max(n, 1) >= (1 << 62):
+                b.P.sink.m[i]._pad = 1
+    b.ksrc = ksrc
     if dense:
         return _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross, timing)
     part = _group_hash(v, b, keys, kcols, plan, measures, count_m)
@@ -733,6 +809,14 @@ def regroup(full, keys: list[str], aggs: dict[str, tuple]) -> ColumnTable:
     return group_aggregate(full, keys, re)
 
 
+def _key_xform(v: TableView, k: str) -> int:
+    return _XFORM[v.derived[k].xform] if k in v.derived else L.XFORM_NONE
+
+
+def _key_offset(v: TableView, k: str) -> int:
+    return v.derived[k].offset if k in v.derived else 0
+
+
 def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross=None, timing=None):
     torch = _torch()
     S = b.P.sink
@@ -741,7 +825,8 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
     S.gkey.n = len(keys)
     luts = []
     for i, (k, c) in enumerate(zip(keys, kcols)):
-        S.gkey.slot[i] = b.slot[k]
+        S.gkey.slot[i] = b.slot[b.ksrc[i]]
+        S.gkey.xform |= _key_xform(v, k) << (8 * i)
         S.gcard[i] = cards[i]
         if c.kind == "dict":
             S.gkey.lo[i] = 0
@@ -749,7 +834,7 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
             S.glut[i] = b.lut(rank)
             luts.append(rank)
         else:
-            S.gkey.lo[i] = c.lo
+            S.gkey.lo[i] = c.lo - _key_offset(v, k)
             S.glut[i] = -1
             luts.append(None)
     M = len(measures)
@@ -864,8 +949,9 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
     shifts.reverse()
     S.gkey.n = len(keys)
     for i, k in enumerate(keys):
-        S.gkey.slot[i] = b.slot[k]
-        S.gkey.lo[i] = los[i]
+        S.gkey.slot[i] = b.slot[b.ksrc[i]]
+        S.gkey.xform |= _key_xform(v, k) << (8 * i)
+        S.gkey.lo[i] = los[i] - _key_offset(v, k)
         S.gkey.bits[i] = bits[i]
         S.gkey.shift[i] = shifts[i]
     # capacity: bounded by rows, the key domain, and unique inner-join builds
@@ -876,31 +962,45 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
         dom *= (1 << bb)
     bound = min(bound, dom)
     for st in v.probes:
-        if st.kind == L.JOIN_INNER and (set(st.probe_keys) & set(keys) or
-                                         set(st.payload) & set(keys)):
+        # a unique-build inner join bounds the groups only when every group
+        # key is determined by the matched build row
+        if st.kind == L.JOIN_INNER and set(keys) <= set(st.probe_keys) | set(st.payload):
             bound = min(bound, max(st.lookup.table.row_count, 1))
     M = len(measures)
+    # dense packed-key domain (TPC-H surrogate keys): direct-addressed groups,
+    # slot = packed key, no hashing / CAS (sink.n_cells = 1 marks it)
+    direct = len(keys) >= 1 and dom <= max(4 * bound, 1 << 16) and dom <= (1 << 31)
+    S.n_cells = 1 if direct else 0
+    wide = [bool(S.m[j]._pad) for j in range(M)]
+    woff = list(np.cumsum([0] + [2 if w else 1 for w in wide])[:-1])
+    W = int(sum(2 if w else 1 for w in wide))          # accumulator words per group
     cap = 1024
     while cap < 2 * bound:
         cap *= 2
+    if direct:
+        cap = int(dom)
     flags = alloc(4, np.uint32)
     while True:
         gkeys = alloc(cap, np.uint64)
-        accb = alloc(cap * M, np.int64)
+        accb = alloc(cap * W, np.int64)
         fill_i64(gkeys.view(torch.int64), -1)
         for j, (op, _) in enumerate(measures):
             ident = INT64_MAX if op == "min" else (INT64_MIN if op == "max" else 0)
-            fill_i64(accb, ident, n=cap, stride=M, offset=j)
+            fill_i64(accb, ident, n=cap, stride=W, offset=int(woff[j]))
+            if wide[j]:
+                fill_i64(accb, 0, n=cap, stride=W, offset=int(woff[j]) + 1)
         fill_i64(flags.view(torch.int64), 0)
         S.gkeys, S.acc, S.gcap, S.flags = gkeys.data_ptr(), accb.data_ptr(), cap, flags.data_ptr()
         b.run()
         if int(_to_host(flags)[0]) == 0:
             break
+        if direct or cap >= (1 << 34):
+            raise SchemaError("group table overflow (group key outside its proven range)")
         cap *= 4   # table overflowed: rerun with a bigger one
     out_keys = alloc(cap, np.uint64)
-    out_acc = alloc(cap * M, np.int64)
+    out_acc = alloc(cap * W, np.int64)
     cnt = alloc(1, np.uint64)
-    L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, M, _ptr(out_keys), _ptr(out_acc),
+    L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys), _ptr(out_acc),
            _ptr(cnt), _stream())
     G = int(_to_host(cnt)[0])
     # sort groups by packed key (== lexicographic key order)
@@ -925,12 +1025,25 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
                    L.Column_(data.data_ptr(), c.scx_dtype, 0), _stream())
         out[k] = c.like(data)
 
-    def measure_col(j):
-        src = out_acc[j * cap: j * cap + G]
+    def word_col(w):
+        src = out_acc[w * cap: w * cap + G]
         dst = alloc(G, np.int64)
         L.call("scx_gather", L.Column_(src.data_ptr(), L.SCX_I64, 0), _ptr(perm), G,
                L.Column_(dst.data_ptr(), L.SCX_I64, 0), _stream())
         return dst
+
+    def measure_col(j):
+        lo = word_col(int(woff[j]))
+        if not wide[j]:
+            return lo
+        hi = word_col(int(woff[j]) + 1)
+        out64 = alloc(G, np.int64)
+        flag = alloc(4, np.uint32)
+        fill_i64(flag.view(torch.int64), 0)
+        L.call("scx_i128_narrow", _ptr(lo), _ptr(hi), G, _ptr(out64), _ptr(flag), _stream())
+        if int(_to_host(flag)[0]):
+            raise SchemaError("aggregate result exceeds the 64-bit output range")
+        return out64
 
     for a in plan:
         if a.op == "count":

@@ -274,6 +274,15 @@ int scx_hash_agg_compact(const uint64_t* gkeys_dev, const int64_t* acc_dev,
                          int64_t cap, int m, uint64_t* out_keys_dev,
                          int64_t* out_acc_dev, uint64_t* count_dev, void* stream);
 
+/* Ordered compaction of a direct-addressed group table (sink n_cells = 1):
+ * occupied slots in slot order, i.e. already sorted by packed group key, so
+ * no sort follows.  Same outputs as scx_hash_agg_compact; temp_dev sized by
+ * scx_direct_agg_workspace(cap). */
+int64_t scx_direct_agg_workspace(int64_t cap);
+int scx_direct_agg_compact(const uint64_t* gkeys_dev, const int64_t* acc_dev, int64_t cap, int m,
+                           uint64_t* out_keys_dev, int64_t* out_acc_dev, uint64_t* count_dev,
+                           void* temp_dev, void* stream);
+
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not
  * fit (group_aggregate output, relops.py:138-158). */

@@ -65,27 +65,6 @@ __global__ void hist_kernel(DigitSrc D, int64_t n, int ndig, uint32_t* counts, i
   for (int d = threadIdx.x; d < ndig; d += kBlock) counts[(int64_t)d * nblocks + blockIdx.x] = h[d];
 }
 
-// single-CTA exclusive scan of m u32 counts into u64 offsets (m <= ~16M)
-__global__ void scan_kernel(const uint32_t* in, uint64_t* out, int64_t m) {
-  __shared__ uint64_t part[1024];
-  const int t = threadIdx.x;
-  const int64_t per = (m + 1023) / 1024;
-  const int64_t b = t * per, e = min(m, b + per);
-  uint64_t s = 0;
-  for (int64_t i = b; i < e; ++i) s += in[i];
-  part[t] = s;
-  __syncthreads();
-  for (int o = 1; o < 1024; o <<= 1) {
-    uint64_t v = (t >= o) ? part[t - o] : 0;
-    __syncthreads();
-    part[t] += v;
-    __syncthreads();
-  }
-  uint64_t run = part[t] - s;
-  for (int64_t i = b; i < e; ++i) { out[i] = run; run += in[i]; }
-  if (t == 1023) out[m] = part[1023];
-}
-
 // stable scatter; `emit(i, pos)` writes element i to pos
 template <typename Emit>
 __device__ __forceinline__ void scatter_chunk(const DigitSrc& D, int64_t n, int ndig,
@@ -180,23 +159,26 @@ __global__ void copy_pairs_kernel(const uint64_t* ki, const uint32_t* vi, uint64
 
 static int64_t nblocks_for(int64_t n) { return (n + kChunk - 1) / kChunk; }
 
-// workspace: counts u32[ndig*nb] + offsets u64[ndig*nb + 1]
+int scan_u32_excl(const uint32_t* in, uint64_t* out, int64_t m, uint64_t* tmp, cudaStream_t st);
+int64_t scan_tmp_words(int64_t m);
+
+// workspace: counts u32[ndig*nb] + offsets u64[ndig*nb + 1] + scan scratch
 static int64_t ws_bytes(int64_t n, int ndig) {
   const int64_t nb = nblocks_for(n) > 0 ? nblocks_for(n) : 1;
   const int64_t m = ndig * nb;
-  return ((m * 4 + 255) / 256) * 256 + (m + 1) * 8;
+  return ((m * 4 + 255) / 256) * 256 + (m + 1) * 8 + 8 * scan_tmp_words(m);
 }
 
 static int counting_pass(const DigitSrc& D, int64_t n, int ndig, void* temp, cudaStream_t st,
                          const uint64_t*& offs_out, int& nb_out) {
   const int64_t nb = nblocks_for(n);
-  if (nb * ndig > (1ll << 26)) { set_error("radix: input too large for single-CTA scan"); return SCX_EUNSUPPORTED; }
   uint32_t* counts = static_cast<uint32_t*>(temp);
   uint64_t* offs = reinterpret_cast<uint64_t*>(static_cast<char*>(temp) + ((nb * ndig * 4 + 255) / 256) * 256);
+  uint64_t* tmp = offs + nb * ndig + 1;
   hist_kernel<<<(int)nb, kBlock, 0, st>>>(D, n, ndig, counts, (int)nb);
   SCX_CHECK_LAUNCH("hist_kernel");
-  scan_kernel<<<1, 1024, 0, st>>>(counts, offs, nb * ndig);
-  SCX_CHECK_LAUNCH("scan_kernel");
+  int rc = scan_u32_excl(counts, offs, nb * ndig, tmp, st);
+  if (rc) return rc;
   offs_out = offs;
   nb_out = (int)nb;
   return SCX_OK;

@@ -43,6 +43,10 @@ __global__ void lookup_build_kernel(scx_lookup T, BuildCols C, scx_keyspec K, in
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t key;
     if (!build_key(C, K, i, key)) { atomicOr(flags + 2, 1u); continue; }
+    // clustered build sides (lineitem by orderkey) repeat keys in runs: the
+    // first row of a run inserts, the rest only report the duplicate
+    uint64_t prev;
+    if (i > 0 && build_key(C, K, i - 1, prev) && prev == key) { atomicOr(flags + 1, 1u); continue; }
     if (T.kind == SCX_HT_DIRECT) {
       if (key >= T.cap) { atomicOr(flags + 2, 1u); continue; }
       const uint32_t prev = atomicExch(vals + key, (uint32_t)i);

@@ -971,6 +971,10 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
     # slot = packed key, no hashing / CAS (sink.n_cells = 1 marks it)
     direct = len(keys) >= 1 and dom <= max(4 * bound, 1 << 16) and dom <= (1 << 31)
     S.n_cells = 1 if direct else 0
+    if not direct and bound > (1 << 20) and (v.probes or not v.pre.is_true or not v.post.is_true):
+        # a large, filtered input: one count pass sizes the table to the rows
+        # that survive (cheaper than filling / compacting a table sized for n)
+        bound = min(bound, max(count_rows(v), 1))
     wide = [bool(S.m[j]._pad) for j in range(M)]
     woff = list(np.cumsum([0] + [2 if w else 1 for w in wide])[:-1])
     W = int(sum(2 if w else 1 for w in wide))          # accumulator words per group
@@ -1000,11 +1004,19 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
     out_keys = alloc(cap, np.uint64)
     out_acc = alloc(cap * W, np.int64)
     cnt = alloc(1, np.uint64)
-    L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys), _ptr(out_acc),
-           _ptr(cnt), _stream())
-    G = int(_to_host(cnt)[0])
-    # sort groups by packed key (== lexicographic key order)
-    skeys, perm = sort_pairs(out_keys[:G], None, total)
+    if direct:
+        # slot order == packed-key order: ordered compaction, no sort
+        ws = alloc(max(2, L.load().scx_direct_agg_workspace(cap) // 8), np.int64)
+        L.call("scx_direct_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
+               _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
+        G = int(_to_host(cnt)[0])
+        skeys, perm = out_keys[:G], None
+    else:
+        L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
+               _ptr(out_acc), _ptr(cnt), _stream())
+        G = int(_to_host(cnt)[0])
+        # sort groups by packed key (== lexicographic key order)
+        skeys, perm = sort_pairs(out_keys[:G], None, total)
     out: dict[str, Column] = {}
     for i, (k, c) in enumerate(zip(keys, kcols)):
         mask = (1 << bits[i]) - 1
@@ -1027,6 +1039,13 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
 
     def word_col(w):
         src = out_acc[w * cap: w * cap + G]
+        if perm is None:
+            if src.data_ptr() % 16 == 0:
+                return src
+            dst = alloc(G, np.int64)
+            if G:
+                dst.copy_(src)
+            return dst
         dst = alloc(G, np.int64)
         L.call("scx_gather", L.Column_(src.data_ptr(), L.SCX_I64, 0), _ptr(perm), G,
                L.Column_(dst.data_ptr(), L.SCX_I64, 0), _stream())

@@ -214,6 +214,67 @@ def run_reference_arm(args) -> None:
 
 
 # ---------------------------------------------------------------------------
+# shuffle microbenchmark (BASELINE config 5): per GPU B bytes of
+# 16-byte rows (int64 key from default_rng(rank), int64 payload), bucket =
+# the reference's hash_keys % N; partition kernel + one all-to-all-v per column
+# ---------------------------------------------------------------------------
+
+def shuffle_bench(ep, gib: float, reps: int = 5) -> dict:
+    import torch
+    import torch.distributed as dist
+    from paper_2506_09226_b200 import exchange as X
+    from paper_2506_09226_b200.table import Column, ColumnTable, alloc
+    rows = int(gib * (1 << 30)) // 16
+    rng = np.random.default_rng(ep.rank)
+    key = torch.from_numpy(rng.integers(0, 2 ** 62, size=rows, dtype=np.int64)).cuda()
+    pay = torch.arange(rows, dtype=torch.int64, device="cuda")
+    t = ColumnTable({"key": Column("int64", key, 0, None, 0, 2 ** 62),
+                     "payload": Column("int64", pay, 0, None, 0, rows)})
+    part_ms, ex_ms = [], []
+    for i in range(reps + 1):
+        torch.cuda.synchronize()
+        if ep.n > 1:
+            dist.barrier()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record()
+        outs, out_rows = X.partition_device(t, ["key"], ep.n)
+        e1.record()
+        if ep.n > 1:
+            in_rows, _ = X.size_exchange(ep, out_rows)
+            for nm in ("key", "payload"):
+                X.alltoallv(ep, outs[nm], out_rows, in_rows)
+        e2.record()
+        torch.cuda.synchronize()
+        if i:
+            part_ms.append(e0.elapsed_time(e1))
+            ex_ms.append(e1.elapsed_time(e2))
+        del outs
+    pm, xm = statistics.mean(part_ms), statistics.mean(ex_ms)
+    if ep.n > 1:
+        tt = torch.tensor([pm, xm], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        pm, xm = (float(x) for x in tt.cpu())
+    pk = peaks()["hbm_gbs"]
+    part_bytes = rows * 16 * 2 + rows * 8       # read key+payload, write both, re-read key
+    out = {"bytes_per_gpu": rows * 16, "rows_per_gpu": rows, "n_gpus": ep.n,
+           "partition_ms": round(pm, 4),
+           "partition_gbs": round(part_bytes / (pm / 1e3) / 1e9, 1),
+           "partition_frac_hbm": round(part_bytes / (pm / 1e3) / 1e9 / pk, 4),
+           "partition_alg_bytes": part_bytes}
+    if ep.n > 1:
+        moved = rows * 16 * (ep.n - 1) / ep.n
+        gbs = moved / (xm / 1e3) / 1e9
+        out.update({"exchange_ms": round(xm, 4), "exchange_gbs_per_dir": round(gbs, 1),
+                    "nvlink_frac_nominal_900": round(gbs / 900.0, 4),
+                    "nvlink_frac_measured_770": round(gbs / 770.0, 4),
+                    "total_ms": round(pm + xm, 4)})
+    else:
+        out["exchange_ms"] = None
+        out["note"] = "N=1: no peer to exchange with; partition kernel only"
+    return out
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 
@@ -226,6 +287,7 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sf", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--shuffle-gib", type=float, default=1.0)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -397,6 +459,8 @@ def main() -> None:
                 "alg_bytes_per_launch": q1_bytes, "launch_ms": round(k_ms, 4),
                 "peak_source": pk["source"]}
 
+    shuffle = shuffle_bench(ep, args.shuffle_gib) if args.shuffle_gib > 0 else None
+
     per_query = {}
     roof_total = sum(q_bytes.values()) / (pk["hbm_gbs"] * 1e9)
     for q in QUERIES:
@@ -435,6 +499,7 @@ def main() -> None:
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_total": int(launches),
             "per_query": per_query,
+            "shuffle": shuffle,
             "suite_roofline": {"t_roof_s": round(roof_total, 6),
                                "frac": round(roof_total / value, 4),
                                "rule": "sum over queries of distinct scanned bytes / HBM peak"},

@@ -310,7 +310,7 @@ class DeviceContext:
                 cols = {}
                 for name in names:
                     ref = t.column(name)
-                    buf = R.alloc(int(counts[src]), ref.np_dtype)
+                    buf = R.alloc(int(counts[src]), ref.np_dtype, ref.data.device)
                     if counts[src]:
                         dist.recv(buf, src=src)
                     cols[name] = ref.like(buf)

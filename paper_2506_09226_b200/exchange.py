@@ -269,6 +269,7 @@ def all_gather_tensor(ep: Endpoint, t):
     if ep.n == 1:
         return t.unsqueeze(0)
     import torch.distributed as dist
-    out = torch.empty((ep.n, *t.shape), dtype=t.dtype, device=t.device)
-    dist.all_gather_into_tensor(out, t.contiguous(), group=ep.group)
-    return out
+    # flat output: gloo requires it, NCCL accepts it
+    out = torch.empty(ep.n * t.numel(), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t.contiguous().reshape(-1), group=ep.group)
+    return out.view(ep.n, *t.shape)

@@ -83,6 +83,8 @@ extern "C" {
 /* lookup-table kinds */
 #define SCX_HT_HASH     0      /* open addressing, u64 keys, linear probing   */
 #define SCX_HT_DIRECT   1      /* dense key range: vals[packed key]           */
+#define SCX_HT_BITMAP   2      /* semi/anti membership: bit [packed key] of
+                                  the u32 words at vals, cap = key domain    */
 
 /* aggregate ops (relops.py:11, AGG_OPS) */
 #define SCX_AGG_SUM     0
@@ -95,6 +97,9 @@ extern "C" {
 #define SCX_SINK_AGG_HASH  1   /* open-addressing group table, global atomics */
 #define SCX_SINK_COMPACT   2   /* stable stream compaction (decoupled look-back) */
 #define SCX_SINK_COUNT     3   /* selected-row count only                      */
+#define SCX_SINK_BITMAP    4   /* set bit [gkey-packed key] of the u32 words at
+                                  gkeys (domain gcap): a semi/anti-join build
+                                  side straight from a filtered scan         */
 
 #define SCX_EMPTY_KEY 0xFFFFFFFFFFFFFFFFull
 #define SCX_NO_ROW    0xFFFFFFFFu
@@ -323,6 +328,9 @@ int scx_gather(scx_column in, const uint32_t* idx_dev, int64_t n, scx_column out
 int scx_iota(uint32_t* idx_dev, int64_t n, void* stream);
 /* p[i * stride] = value for i < n  (table / accumulator initialisation) */
 int scx_fill_i64(int64_t* p_dev, int64_t n, int64_t stride, int64_t value, void* stream);
+/* p[r * w + j] = pattern_host[j] for r < rows, j < w <= 16: a row-major
+ * group table's identities in one pass */
+int scx_fill_rows(int64_t* p_dev, int64_t rows, int w, const int64_t* pattern_host, void* stream);
 
 /* ---- hash partitioning (exchange.py:35-70) --------------------------------
  * bucket(row) = fib_hash(keys) mod n_parts with the reference's u64 wrap:

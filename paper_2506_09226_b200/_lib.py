@@ -23,9 +23,9 @@ MAX_POLYS = 4
 ATOM_RANGE, ATOM_SET, ATOM_DIFF, ATOM_POLY = 0, 1, 2, 3
 XFORM_NONE, XFORM_YEAR = 0, 1
 JOIN_SEMI, JOIN_ANTI, JOIN_INNER, JOIN_LEFT = 0, 1, 2, 3
-HT_HASH, HT_DIRECT = 0, 1
+HT_HASH, HT_DIRECT, HT_BITMAP = 0, 1, 2
 AGG_SUM, AGG_COUNT, AGG_MIN, AGG_MAX = 0, 1, 2, 3
-SINK_AGG_DENSE, SINK_AGG_HASH, SINK_COMPACT, SINK_COUNT = 0, 1, 2, 3
+SINK_AGG_DENSE, SINK_AGG_HASH, SINK_COMPACT, SINK_COUNT, SINK_BITMAP = 0, 1, 2, 3, 4
 EMPTY_KEY = 0xFFFFFFFFFFFFFFFF
 NO_ROW = 0xFFFFFFFF
 
@@ -128,6 +128,7 @@ _PROTOS = {
     "scx_minmax": (C.c_int, [Column_, i64, _vp, _vp]),
     "scx_gather": (C.c_int, [Column_, _vp, i64, Column_, _vp]),
     "scx_iota": (C.c_int, [_vp, i64, _vp]),
+    "scx_fill_rows": (C.c_int, [_vp, i64, C.c_int, C.POINTER(i64), _vp]),
     "scx_fill_i64": (C.c_int, [_vp, i64, i64, i64, _vp]),
     "scx_hash_keys": (C.c_int, [C.POINTER(Column_), C.c_int, i64, _vp, _vp]),
     "scx_partition_workspace": (i64, [i64, C.c_int]),

@@ -633,7 +633,15 @@ struct Gen {
     o << "    u32 idx" << pi << "[V];\n    {\n";
     o << "      const u32* vals = (const u32*)a.p[" << vals_p << "];\n";
     o << "      const u64 cap = a.p[" << cap_p << "];\n";
-    if (pb.table.kind == SCX_HT_DIRECT) {
+    if (pb.table.kind == SCX_HT_BITMAP) {
+      if (pb.kind != SCX_JOIN_SEMI && pb.kind != SCX_JOIN_ANTI) { err = "bitmap probe needs a semi/anti join"; return; }
+      o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
+      o << "        idx" << pi << "[r] = SCX_NOROW;\n";
+      o << "        if ((sel >> r) & 1u) {\n";
+      pack_key(pb.key, "r", nullptr, 0, "key", "kin");
+      o << "          if (kin && key < cap && ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u)) idx" << pi << "[r] = 0u;\n";
+      o << "        }\n      }\n";
+    } else if (pb.table.kind == SCX_HT_DIRECT) {
       o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
       o << "        idx" << pi << "[r] = SCX_NOROW;\n";
       o << "        if ((sel >> r) & 1u) {\n";
@@ -760,6 +768,11 @@ struct Gen {
     } else if (S.kind == SCX_SINK_COUNT) {
       count_p = param(S.count);
       o << "  u64 cnt = 0;\n";
+    } else if (S.kind == SCX_SINK_BITMAP) {
+      gkeys_p = param(S.gkeys);
+      gcap_p = param(S.gcap);
+      o << "  u32* bits = (u32*)a.p[" << gkeys_p << "];\n";
+      o << "  const u64 bcap = a.p[" << gcap_p << "];\n";
     } else {
       err = "unknown sink";
       return SCX_EINVAL;
@@ -850,6 +863,16 @@ struct Gen {
       o << "    }\n";
     } else if (S.kind == SCX_SINK_COUNT) {
       o << "    cnt += __popc(sel);\n";
+    } else if (S.kind == SCX_SINK_BITMAP) {
+      // consecutive rows of a thread often repeat the key (clustered fact
+      // tables): set each run's bit once
+      o << "    { u64 prev = SCX_EMPTY;\n";
+      o << "#pragma unroll\n    for (int r = 0; r < V; ++r) {\n";
+      o << "      if (!((sel >> r) & 1u)) continue;\n";
+      pack_key(S.gkey, "r", nullptr, 0, "key", "kin");
+      o << "      if (kin && key < bcap && key != prev) atomicOr(bits + (key >> 5), 1u << (key & 31));\n";
+      o << "      prev = key;\n";
+      o << "    } }\n";
     } else {  // COMPACT
       o << "    {\n";
       o << "      const u32 c = __popc(sel);\n";

@@ -806,8 +806,12 @@ static int plan_launch(const scx_pipeline& P, Launch& L) {
       set_error("interpreter: polynomial atoms need the JIT path (unset SCX_JIT=0)");
       return SCX_EUNSUPPORTED;
     }
+  if (P.sink.kind == SCX_SINK_BITMAP) {
+    set_error("interpreter: bitmap sinks need the JIT path (unset SCX_JIT=0)");
+    return SCX_EUNSUPPORTED;
+  }
   for (int p = 0; p < P.n_probes; ++p)
-    if (P.probe[p].kind == SCX_JOIN_LEFT) {
+    if (P.probe[p].kind == SCX_JOIN_LEFT || P.probe[p].table.kind == SCX_HT_BITMAP) {
       set_error("interpreter: left joins need the JIT path (unset SCX_JIT=0)");
       return SCX_EUNSUPPORTED;
     }

@@ -115,38 +115,58 @@ int scan_u32_excl(const uint32_t* in, uint64_t* out, int64_t m, uint64_t* tmp, c
 }
 
 // ---- ordered compaction of a direct-addressed group table -----------------
+// A CTA owns 4096 consecutive slots, visited as 16 rounds of 256 (thread t
+// reads slot round*256 + t: coalesced).  Each round's ranks come from warp
+// ballots; the round's accumulator rows (256 x W words, row-major) are staged
+// through shared memory so both the read and the measure-major write are
+// coalesced.
 __global__ void occ_count_kernel(const uint64_t* gkeys, int64_t cap, uint64_t* part) {
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) s += (base + i < cap && gkeys[base + i] != SCX_EMPTY_KEY);
+  for (int it = 0; it < kScanItems; ++it) {
+    const int64_t e = base + it * kBlock + threadIdx.x;
+    s += (e < cap && gkeys[e] != SCX_EMPTY_KEY);
+  }
   uint32_t excl;
   const uint32_t tot = block_excl_scan(s, excl);
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
 }
 
-__global__ void occ_write_kernel(const uint64_t* gkeys, const int64_t* acc, int64_t cap, int m,
-                                 const uint64_t* part, uint64_t* out_keys, int64_t* out_acc,
-                                 uint64_t* count) {
-  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  uint32_t s = 0;
-  uint64_t k[kScanItems];
+__global__ void __launch_bounds__(kBlock) occ_write_kernel(
+    const uint64_t* gkeys, const int64_t* acc, int64_t cap, int m, const uint64_t* part,
+    uint64_t* out_keys, int64_t* out_acc, uint64_t* count) {
+  __shared__ int64_t tile[kBlock * 16];
+  __shared__ uint32_t wcnt[kWarps];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kScanTile;
+  uint64_t pos0 = part[blockIdx.x];
+  for (int it = 0; it < kScanItems; ++it) {
+    const int64_t r0 = base + (int64_t)it * kBlock;
+    if (r0 >= cap) break;
+    const int64_t e = r0 + tid;
+    const uint64_t k = e < cap ? gkeys[e] : SCX_EMPTY_KEY;
+    const bool occ = k != SCX_EMPTY_KEY;
+    const uint32_t b = __ballot_sync(0xffffffffu, occ);
+    if (lane == 0) wcnt[warp] = __popc(b);
+    const int64_t rows = min((int64_t)kBlock, cap - r0);
+    for (int64_t x = tid; x < rows * m; x += kBlock) tile[x] = acc[r0 * m + x];
+    __syncthreads();
+    uint32_t wofs = 0, tot = 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    k[i] = (base + i < cap) ? gkeys[base + i] : SCX_EMPTY_KEY;
-    s += k[i] != SCX_EMPTY_KEY;
+    for (int w = 0; w < kWarps; ++w) {
+      wofs += (w < warp) ? wcnt[w] : 0;
+      tot += wcnt[w];
+    }
+    if (occ) {
+      const uint64_t pos = pos0 + wofs + __popc(b & ((1u << lane) - 1u));
+      out_keys[pos] = k;
+      for (int j = 0; j < m; ++j) out_acc[(int64_t)j * cap + (int64_t)pos] = tile[tid * m + j];
+    }
+    pos0 += tot;
+    __syncthreads();
   }
-  uint32_t excl;
-  block_excl_scan(s, excl);
-  uint64_t pos = part[blockIdx.x] + excl;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    if (k[i] == SCX_EMPTY_KEY) continue;
-    out_keys[pos] = k[i];
-    for (int j = 0; j < m; ++j) out_acc[(int64_t)j * cap + (int64_t)pos] = acc[(base + i) * m + j];
-    ++pos;
-  }
-  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kBlock - 1) *count = part[gridDim.x];
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *count = part[gridDim.x];
 }
 
 }  // namespace scx
@@ -158,7 +178,7 @@ extern "C" int64_t scx_direct_agg_workspace(int64_t cap) { return 8 * scan_tmp_w
 extern "C" int scx_direct_agg_compact(const uint64_t* gkeys, const int64_t* acc, int64_t cap,
                                       int m, uint64_t* out_keys, int64_t* out_acc,
                                       uint64_t* count, void* temp, void* stream) {
-  if (!gkeys || !out_keys || !count || !temp || (m > 0 && (!acc || !out_acc))) {
+  if (!gkeys || !out_keys || !count || !temp || m > 16 || (m > 0 && (!acc || !out_acc))) {
     set_error("direct_agg_compact: bad arguments");
     return SCX_EINVAL;
   }

@@ -47,7 +47,10 @@ __global__ void lookup_build_kernel(scx_lookup T, BuildCols C, scx_keyspec K, in
     // first row of a run inserts, the rest only report the duplicate
     uint64_t prev;
     if (i > 0 && build_key(C, K, i - 1, prev) && prev == key) { atomicOr(flags + 1, 1u); continue; }
-    if (T.kind == SCX_HT_DIRECT) {
+    if (T.kind == SCX_HT_BITMAP) {
+      if (key >= T.cap) { atomicOr(flags + 2, 1u); continue; }
+      atomicOr(vals + (key >> 5), 1u << (key & 31));
+    } else if (T.kind == SCX_HT_DIRECT) {
       if (key >= T.cap) { atomicOr(flags + 2, 1u); continue; }
       const uint32_t prev = atomicExch(vals + key, (uint32_t)i);
       if (prev != SCX_NO_ROW) atomicOr(flags + 1, 1u);
@@ -170,6 +173,17 @@ __global__ void fill_i64_kernel(int64_t* p, int64_t n, int64_t stride, int64_t v
     p[i * stride] = v;
 }
 
+struct RowPattern {
+  int64_t v[16];
+};
+
+// p[r * w + j] = pattern[j]: one coalesced pass over a row-major table
+__global__ void fill_rows_kernel(int64_t* p, int64_t words, int w, RowPattern pat) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = pat.v[i % w];
+}
+
 __global__ void iota_kernel(uint32_t* idx, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -235,6 +249,11 @@ extern "C" int scx_lookup_clear(const scx_lookup* T, void* stream) {
   if (!T || !T->vals || (T->kind == SCX_HT_HASH && (!T->keys || (T->cap & (T->cap - 1))))) {
     set_error("lookup_clear: bad table (hash capacity must be a power of two)");
     return SCX_EINVAL;
+  }
+  if (T->kind == SCX_HT_BITMAP) {
+    SCX_CUDA(cudaMemsetAsync(reinterpret_cast<void*>(T->vals), 0, 4 * ((T->cap + 31) / 32),
+                             (cudaStream_t)stream));
+    return SCX_OK;
   }
   lookup_clear_kernel<<<launch_grid(T->cap), 256, 0, (cudaStream_t)stream>>>(
       T->kind == SCX_HT_HASH ? reinterpret_cast<uint64_t*>(T->keys) : nullptr,
@@ -337,6 +356,17 @@ extern "C" int scx_fill_i64(int64_t* p, int64_t n, int64_t stride, int64_t value
   if (!p || stride < 1) { set_error("fill_i64: bad arguments"); return SCX_EINVAL; }
   fill_i64_kernel<<<launch_grid(n), 256, 0, (cudaStream_t)stream>>>(p, n, stride, value);
   SCX_CHECK_LAUNCH("fill_i64_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_fill_rows(int64_t* p, int64_t rows, int w, const int64_t* pattern_host,
+                             void* stream) {
+  if (rows == 0) return SCX_OK;
+  if (!p || !pattern_host || w < 1 || w > 16) { set_error("fill_rows: bad arguments"); return SCX_EINVAL; }
+  RowPattern pat;
+  for (int j = 0; j < w; ++j) pat.v[j] = pattern_host[j];
+  fill_rows_kernel<<<launch_grid(rows * w), 256, 0, (cudaStream_t)stream>>>(p, rows * w, w, pat);
+  SCX_CHECK_LAUNCH("fill_rows_kernel");
   return SCX_OK;
 }
 

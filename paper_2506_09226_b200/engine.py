@@ -228,8 +228,10 @@ class DeviceContext:
     def join(self, left, right, on, how="inner"):
         return R.local_hash_join(left, right, on, how)
 
-    def group(self, t, keys, aggs):
-        return R.group_aggregate(t, keys, aggs)
+    def group(self, t, keys, aggs, sort: bool = True):
+        """group_aggregate; ``sort=False`` (an extension) skips the key-order
+        sort for intermediates that feed a join or a re-aggregation."""
+        return R.group_aggregate(t, keys, aggs, sort=sort)
 
     def add_column(self, t, name, col):
         return R.as_view(t).with_column(name, col)

@@ -167,6 +167,58 @@ class Lookup:
         return self._unique
 
 
+_BITMAP_MAX_BITS = 1 << 30       # 128 MB of bitmap words
+
+
+def _key_span(packing: KeyPacking, cols: list[Column]) -> int:
+    if len(cols) > 1:
+        return 1 << packing.total_bits
+    c = cols[0]
+    return (c.hi - c.lo + 1) if c.hi >= c.lo else 1
+
+
+class BitmapLookup:
+    """Membership table for semi / anti joins: one bit per packed key.
+
+    At TPC-H key densities the bitmap is 32x smaller than a direct row-index
+    table (150M orderkeys: 19 MB, L2-resident) and is built either from a
+    materialised table or -- without materialising anything -- by a fused
+    scan of the build-side view (SCX_SINK_BITMAP).
+    """
+
+    unique = False
+    table = None
+
+    def __init__(self, source, keys: list[str], cols: list[Column], packing: KeyPacking,
+                 span: int):
+        self.keys = list(keys)
+        self.packing = packing
+        self.lk = L.Lookup()
+        self.lk.kind = L.HT_BITMAP
+        self.lk.cap = span
+        self._bits = alloc((span + 31) // 32, np.uint32)
+        self.lk.vals = self._bits.data_ptr()
+        self.lk.keys = 0
+        L.call("scx_lookup_clear", C.byref(self.lk), _stream())
+        if isinstance(source, TableView) and (source.probes or not source.pre.is_true
+                                              or not source.post.is_true):
+            b = _Builder(source, set(keys))
+            S = b.P.sink
+            S.kind = L.SINK_BITMAP
+            S.gkey = packing.spec([b.slot[k] for k in keys])
+            S.gkeys = self._bits.data_ptr()
+            S.gcap = span
+            b.run()
+        else:
+            t = source.materialize() if isinstance(source, TableView) else source
+            flags = alloc(4, np.uint32)
+            fill_i64(flags.view(_torch().int64), 0)
+            colarr = (L.Column_ * len(keys))(*[t.column(k).scx() for k in keys])
+            spec = packing.spec(list(range(len(keys))))
+            L.call("scx_lookup_build", C.byref(self.lk), colarr, len(keys), C.byref(spec),
+                   t.row_count, _ptr(flags), _stream())
+
+
 # ---------------------------------------------------------------------------
 # lazy views
 # ---------------------------------------------------------------------------
@@ -365,12 +417,19 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
     if not on:
         raise SchemaError("join requires at least one key pair")
     lv = as_view(left)
-    rt = right.materialize() if isinstance(right, TableView) else right
+    if how in ("semi", "anti"):
+        rmeta = right.meta if isinstance(right, TableView) else right.columns
+        rt = right
+    else:
+        rt = right.materialize() if isinstance(right, TableView) else right
+        rmeta = rt.columns
     for lname, rname in on:
         lc = lv[lname]
         if not isinstance(lc, ColRef):
             raise SchemaError(f"join key {lname!r} must be a column")
-        rc = rt.column(rname)
+        if rname not in rmeta:
+            raise SchemaError(f"unknown column {rname!r}")
+        rc = rmeta[rname]
         if lc.col.kind != rc.kind:
             raise SchemaError(f"join key type mismatch: {lname} is {lc.col.kind}, "
                               f"{rname} is {rc.kind}")
@@ -384,7 +443,18 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
             raise SchemaError(f"inner join would duplicate columns: {sorted(overlap)}")
     if len(lv.probes) >= L.MAX_PROBES:
         lv = TableView(lv.materialize())
-    lookup = Lookup(rt, [r for _, r in on])
+    rkeys = [r for _, r in on]
+    lookup = None
+    if how in ("semi", "anti"):
+        kc = [rmeta[r] for r in rkeys]
+        packing = key_packing(kc)
+        span = _key_span(packing, kc)
+        if span <= _BITMAP_MAX_BITS:
+            lookup = BitmapLookup(rt, rkeys, kc, packing, span)
+        else:
+            rt = rt.materialize() if isinstance(rt, TableView) else rt
+    if lookup is None:
+        lookup = Lookup(rt, rkeys)
     if how in ("inner", "left") and not lookup.unique:
         raise SchemaError(f"{how} join with duplicate build-side keys is not supported by the "
                           "fused probe (build keys must be unique)")
@@ -738,7 +808,7 @@ def _plan_aggs(v: TableView, aggs: dict) -> tuple[list[_Agg], list[tuple[str, In
 
 
 def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
-                    cross=None, timing: list | None = None) -> ColumnTable:
+                    cross=None, timing: list | None = None, sort: bool = True) -> ColumnTable:
     """Aggregate per group (relops.py:97-160), one fused kernel launch.
 
     ``cross`` (engine.DeviceContext) makes it a global aggregate over all
@@ -792,7 +862,7 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
     b.ksrc = ksrc
     if dense:
         return _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross, timing)
-    part = _group_hash(v, b, keys, kcols, plan, measures, count_m)
+    part = _group_hash(v, b, keys, kcols, plan, measures, count_m, sort)
     if cross is None or cross.ep.n == 1:
         return part
     full = cross.gather(part)
@@ -920,7 +990,7 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
     return ColumnTable(out)
 
 
-def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
+def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> ColumnTable:
     torch = _torch()
     S = b.P.sink
     S.kind = L.SINK_AGG_HASH
@@ -988,11 +1058,13 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
         gkeys = alloc(cap, np.uint64)
         accb = alloc(cap * W, np.int64)
         fill_i64(gkeys.view(torch.int64), -1)
+        pattern = []
         for j, (op, _) in enumerate(measures):
-            ident = INT64_MAX if op == "min" else (INT64_MIN if op == "max" else 0)
-            fill_i64(accb, ident, n=cap, stride=W, offset=int(woff[j]))
+            pattern.append(INT64_MAX if op == "min" else (INT64_MIN if op == "max" else 0))
             if wide[j]:
-                fill_i64(accb, 0, n=cap, stride=W, offset=int(woff[j]) + 1)
+                pattern.append(0)
+        pat = (C.c_int64 * W)(*pattern)
+        L.call("scx_fill_rows", _ptr(accb), cap, W, pat, _stream())
         fill_i64(flags.view(torch.int64), 0)
         S.gkeys, S.acc, S.gcap, S.flags = gkeys.data_ptr(), accb.data_ptr(), cap, flags.data_ptr()
         b.run()
@@ -1015,8 +1087,11 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m) -> ColumnTable:
         L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
                _ptr(out_acc), _ptr(cnt), _stream())
         G = int(_to_host(cnt)[0])
-        # sort groups by packed key (== lexicographic key order)
-        skeys, perm = sort_pairs(out_keys[:G], None, total)
+        if sort:
+            # sort groups by packed key (== lexicographic key order)
+            skeys, perm = sort_pairs(out_keys[:G], None, total)
+        else:     # intermediate (e.g. a join build side): order is irrelevant
+            skeys, perm = out_keys[:G], None
     out: dict[str, Column] = {}
     for i, (k, c) in enumerate(zip(keys, kcols)):
         mask = (1 << bits[i]) - 1

@@ -109,7 +109,50 @@ def _count():
     return P
 
 
+def _bitmap_sink():
+    P = _q6()
+    S = P.sink
+    S.kind = L.SINK_BITMAP
+    S.gkey.n = 1
+    S.gkey.slot[0] = 3
+    S.gkey.bits[0] = 24
+    S.gkey.lo[0] = 1
+    S.gkeys = 0xd000
+    S.gcap = 1 << 24
+    return P
+
+
+def _poly_left_year():
+    P = _compact_probe(L.HT_DIRECT, L.JOIN_INNER)
+    P.probe[0].kind = L.JOIN_LEFT
+    A = P.atoms[1]
+    A.op, A.slot, A.clause, A.lo, A.hi = L.ATOM_POLY, 0, 0, 1, 1 << 40
+    P.pre.n_atoms = 1
+    P.post.first_atom, P.post.n_atoms, P.post.clause_mask = 1, 1, 1
+    m = P.polys[0]
+    m.op, m.n_terms, m.cond_atom = L.AGG_SUM, 2, -1
+    m.t[0].coef, m.t[0].n_factors = 5, 2
+    m.t[0].f[0].a, m.t[0].f[0].b, m.t[0].f[0].slot, m.t[0].f[0]._pad = 0, 1, 1, 1
+    m.t[0].f[1].a, m.t[0].f[1].b, m.t[0].f[1].slot, m.t[0].f[1]._pad = 0, 1, 4, 1
+    m.t[1].coef, m.t[1].n_factors = -1, 1
+    m.t[1].f[0].a, m.t[1].f[0].b, m.t[1].f[0].slot = 0, 1, 5
+    S = P.sink
+    S.kind = L.SINK_AGG_HASH
+    S.n_measures = 1
+    S.m[0].op, S.m[0].cond_atom = L.AGG_COUNT, -1
+    S.gkey.n = 1
+    S.gkey.slot[0] = 1
+    S.gkey.bits[0] = 8
+    S.gkey.lo[0] = 1992
+    S.gkey.xform = L.XFORM_YEAR
+    S.gkeys, S.acc, S.gcap, S.flags = 0x1000, 0x2000, 1 << 12, 0x3000
+    return P
+
+
 PLANS = {
+    "bitmap_sink": _bitmap_sink,
+    "semi_bitmap_probe": lambda: _compact_probe(L.HT_BITMAP, L.JOIN_SEMI),
+    "poly_atom_left_join_year_key": _poly_left_year,
     "q6_dense1": _q6, "q1_dense6": _q1, "dense_smem": _dense_smem, "count": _count,
     "compact_inner_hash": _compact_probe,
     "compact_semi_direct": lambda: _compact_probe(L.HT_DIRECT, L.JOIN_SEMI),

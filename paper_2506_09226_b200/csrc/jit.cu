@@ -827,39 +827,71 @@ struct Gen {
       }
       o << "    }\n";
     } else if (S.kind == SCX_SINK_AGG_HASH) {
-      o << "#pragma unroll\n    for (int r = 0; r < V; ++r) {\n";
-      o << "      if (!((sel >> r) & 1u)) continue;\n";
-      pack_key(S.gkey, "r", S.glut, -1, "key", "kin");
-      // lut length for hash group keys: dictionary size isn't in the keyspec;
-      // the LUT region is bounded by SCX_MAX_LUT so emit the whole tail
-      o << "      (void)kin;\n";
+      // accumulator words per group: 2 for 128-bit ("wide", measure._pad) sums
+      int W = 0;
+      bool any_wide = false;
+      std::vector<int> woff(M);
+      for (int m = 0; m < M; ++m) {
+        woff[m] = W;
+        W += S.m[m]._pad == 1 ? 2 : 1;
+        any_wide |= S.m[m]._pad == 1;
+      }
+      // Rows of one thread are consecutive, and fact tables are clustered on
+      // their grouping keys (lineitem by orderkey): runs of equal keys are
+      // pre-aggregated in registers and flushed with one slot lookup + one
+      // atomic per measure (not for 128-bit sums, whose per-row values may
+      // not add in 64 bits).
+      o << "    {\n      u64 run = SCX_EMPTY;\n";
+      for (int m = 0; m < M; ++m) o << "      i64 ra" << m << " = 0;\n";
+      o << "      auto flush = [&](u64 key) {\n";
       if (S.n_cells == 1) {
         // direct-addressed groups: the packed key is the slot (gcap = domain)
-        o << "      u64 slot = SCX_EMPTY;\n";
-        o << "      if (kin && key <= gmask) { slot = key; if (gkeys[slot] != key) gkeys[slot] = key; }\n";
+        o << "        u64 slot = SCX_EMPTY;\n";
+        o << "        if (key <= gmask) { slot = key; if (gkeys[slot] != key) gkeys[slot] = key; }\n";
       } else {
         // open addressing, linear probing; a probe run longer than 4096 means
         // the table is (nearly) full: flag it so the host retries larger
-        o << "      u64 h = mix64(key) & gmask; u64 slot = SCX_EMPTY;\n";
-        o << "      for (u64 pr = 0; pr <= gmask && pr < 4096; ++pr) {\n";
-        o << "        u64 cur = gkeys[h];\n";
-        o << "        if (cur == SCX_EMPTY) { cur = atomicCAS((unsigned long long*)(gkeys + h), SCX_EMPTY, key); if (cur == SCX_EMPTY) cur = key; }\n";
-        o << "        if (cur == key) { slot = h; break; }\n";
-        o << "        h = (h + 1) & gmask;\n      }\n";
+        o << "        u64 h = mix64(key) & gmask; u64 slot = SCX_EMPTY;\n";
+        o << "        for (u64 pr = 0; pr <= gmask && pr < 4096; ++pr) {\n";
+        o << "          u64 cur = gkeys[h];\n";
+        o << "          if (cur == SCX_EMPTY) { cur = atomicCAS((unsigned long long*)(gkeys + h), SCX_EMPTY, key); if (cur == SCX_EMPTY) cur = key; }\n";
+        o << "          if (cur == key) { slot = h; break; }\n";
+        o << "          h = (h + 1) & gmask;\n        }\n";
       }
-      o << "      if (slot == SCX_EMPTY) { atomicOr((u32*)a.p[" << flags_p << "], 1u); continue; }\n";
-      // accumulator words per group: 2 for 128-bit ("wide", measure._pad) sums
-      int W = 0;
-      std::vector<int> woff(M);
-      for (int m = 0; m < M; ++m) { woff[m] = W; W += S.m[m]._pad == 1 ? 2 : 1; }
+      o << "        if (slot == SCX_EMPTY) { atomicOr((u32*)a.p[" << flags_p << "], 1u); return; }\n";
       for (int m = 0; m < M; ++m) {
         const int op = S.m[m].op;
-        o << "      { const i64 mv = " << measure_expr(S.m[m], "r") << "; long long* t = (long long*)(gacc + slot * " << W << " + " << woff[m] << "); ";
-        if (op == SCX_AGG_MIN) o << "atomicMin(t, mv); }\n";
-        else if (op == SCX_AGG_MAX) o << "atomicMax(t, mv); }\n";
-        else if (S.m[m]._pad == 1) o << "atomic_add_i128((i64*)t, mv); }\n";
-        else o << "atomicAdd((unsigned long long*)t, (unsigned long long)mv); }\n";
+        o << "        { long long* t = (long long*)(gacc + slot * " << W << " + " << woff[m] << "); ";
+        if (op == SCX_AGG_MIN) o << "atomicMin(t, ra" << m << "); }\n";
+        else if (op == SCX_AGG_MAX) o << "atomicMax(t, ra" << m << "); }\n";
+        else if (S.m[m]._pad == 1) o << "atomic_add_i128((i64*)t, ra" << m << "); }\n";
+        else o << "if (ra" << m << ") atomicAdd((unsigned long long*)t, (unsigned long long)ra" << m << "); }\n";
       }
+      o << "      };\n";
+      o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
+      o << "        if (!((sel >> r) & 1u)) continue;\n";
+      pack_key(S.gkey, "r", S.glut, -1, "key", "kin");
+      if (S.n_cells == 1) o << "        if (!kin) { atomicOr((u32*)a.p[" << flags_p << "], 1u); continue; }\n";
+      else o << "        (void)kin;\n";
+      for (int m = 0; m < M; ++m) o << "        const i64 mv" << m << " = " << measure_expr(S.m[m], "r") << ";\n";
+      if (!any_wide) {
+        o << "        if (key == run) {\n";
+        for (int m = 0; m < M; ++m) {
+          const int op = S.m[m].op;
+          if (op == SCX_AGG_MIN) o << "          ra" << m << " = smin(ra" << m << ", mv" << m << ");\n";
+          else if (op == SCX_AGG_MAX) o << "          ra" << m << " = smax(ra" << m << ", mv" << m << ");\n";
+          else o << "          ra" << m << " += mv" << m << ";\n";
+        }
+        o << "          continue;\n        }\n";
+        o << "        if (run != SCX_EMPTY) flush(run);\n";
+        o << "        run = key;\n";
+        for (int m = 0; m < M; ++m) o << "        ra" << m << " = mv" << m << ";\n";
+      } else {
+        for (int m = 0; m < M; ++m) o << "        ra" << m << " = mv" << m << ";\n";
+        o << "        flush(key);\n";
+      }
+      o << "      }\n";
+      if (!any_wide) o << "      if (run != SCX_EMPTY) flush(run);\n";
       o << "    }\n";
     } else if (S.kind == SCX_SINK_COUNT) {
       o << "    cnt += __popc(sel);\n";

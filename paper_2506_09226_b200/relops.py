@@ -817,6 +817,9 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
     """
     v = as_view(table)
     keys = list(group_keys)
+    fd = _dependent_keys(v, keys)
+    if fd:
+        return _group_with_dependent_keys(v, keys, fd, aggs, cross, timing, sort)
     for k in keys:
         if k in v.computed or k not in v.meta:
             raise SchemaError(f"unknown group key {k!r}")
@@ -867,6 +870,40 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
         return part
     full = cross.gather(part)
     return None if full is None else regroup(full, keys, aggs)
+
+
+def _dependent_keys(v: TableView, keys: list[str]) -> list[str]:
+    """Group keys that are payload of a unique-build inner join whose probe
+    keys are all earlier group keys: they are functionally dependent on those
+    keys (Q3's o_orderdate / o_shippriority on l_orderkey), so grouping by the
+    determinants alone gives the same groups in the same order."""
+    out = []
+    for st in v.probes:
+        if st.kind != L.JOIN_INNER or not set(st.probe_keys) <= set(keys):
+            continue
+        last = max(keys.index(k) for k in st.probe_keys)
+        for i, k in enumerate(keys):
+            if (i > last and k in st.payload and k not in st.probe_keys and k not in out
+                    and k not in v.derived and v.meta[k].kind != "dict"):
+                out.append(k)
+    return out
+
+
+def _group_with_dependent_keys(v, keys, fd, aggs, cross, timing, sort) -> ColumnTable:
+    """Group by the determinant keys; each dependent key rides along as a
+    MIN aggregate (all rows of a group carry the same value) and is put back
+    in its key position."""
+    core = [k for k in keys if k not in fd]
+    tmp = {f"__fd_{k}": ("min", k) for k in fd}
+    for name in aggs:
+        if name in tmp:
+            raise SchemaError(f"aggregate name {name!r} is reserved")
+    g = group_aggregate(v, core, {**tmp, **aggs}, cross, timing, sort)
+    if g is None:
+        return None
+    cols = {k: g.column(f"__fd_{k}") if k in fd else g.column(k) for k in keys}
+    cols.update({name: g.column(name) for name in aggs})
+    return ColumnTable(cols)
 
 
 def regroup(full, keys: list[str], aggs: dict[str, tuple]) -> ColumnTable:

@@ -912,21 +912,43 @@ struct Gen {
       o << "#pragma unroll\n      for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, inc, d); if (lane >= d) inc += y; }\n";
       o << "      if (lane == 31) s_warp[warp] = inc;\n";
       o << "      __syncthreads();\n";
-      o << "      if (tid == 0) {\n";
-      o << "        u32 run = 0;\n";
-      o << "        for (int i = 0; i < " << kTPB / 32 << "; ++i) { const u32 t = s_warp[i]; s_warp[i] = run; run += t; }\n";
+      // warp 0: scan the per-warp counts, then a warp-cooperative decoupled
+      // look-back that inspects 32 predecessor tiles per step (a serial
+      // one-tile walk costs an L2 round trip per in-flight tile)
+      o << "      if (warp == 0) {\n";
+      o << "        const u32 wc = lane < " << kTPB / 32 << " ? s_warp[lane] : 0u;\n";
+      o << "        u32 wi = wc;\n";
+      o << "#pragma unroll\n        for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, wi, d); if (lane >= d) wi += y; }\n";
+      o << "        const u64 run = __shfl_sync(0xffffffffu, wi, 31);\n";
+      o << "        if (lane < " << kTPB / 32 << ") s_warp[lane] = wi - wc;\n";
       o << "        u64* status = (u64*)a.p[" << status_p << "];\n";
       o << "        const u64 kA = 1ull << 62, kP = 2ull << 62, kV = (1ull << 62) - 1;\n";
       o << "        u64 excl = 0;\n";
-      o << "        if (tile == 0) { st_release(status, kP | (u64)run); }\n";
+      o << "        if (tile == 0) { if (lane == 0) st_release(status, kP | run); }\n";
       o << "        else {\n";
-      o << "          st_release(status + tile, kA | (u64)run);\n";
+      o << "          if (lane == 0) st_release(status + tile, kA | run);\n";
       o << "          i64 j = tile - 1;\n";
-      o << "          while (true) { const u64 w = ld_acquire(status + j); const u64 f = w & ~kV; if (f == 0) continue; excl += w & kV; if (f == kP) break; --j; }\n";
-      o << "          st_release(status + tile, kP | (excl + run));\n";
+      o << "          while (true) {\n";
+      o << "            const i64 idx = j - lane;\n";
+      o << "            const u64 w = idx >= 0 ? ld_acquire(status + idx) : kP;\n";
+      o << "            const u64 f = w & ~kV;\n";
+      o << "            const u32 pm = __ballot_sync(0xffffffffu, f == kP);\n";
+      o << "            const u32 nr = __ballot_sync(0xffffffffu, f == 0);\n";
+      o << "            const int fp = pm ? __ffs(pm) - 1 : 31;\n";
+      o << "            const u32 need = fp == 31 ? 0xffffffffu : ((2u << fp) - 1u);\n";
+      o << "            if (nr & need) continue;\n";
+      o << "            u64 v = (lane <= fp && idx >= 0) ? (w & kV) : 0ull;\n";
+      o << "#pragma unroll\n            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);\n";
+      o << "            excl += v;\n";
+      o << "            if (pm) break;\n";
+      o << "            j -= 32;\n";
+      o << "          }\n";
+      o << "          if (lane == 0) st_release(status + tile, kP | (excl + run));\n";
       o << "        }\n";
-      o << "        if (tile == ntiles - 1) *(u64*)a.p[" << count_p << "] = excl + run;\n";
-      o << "        s_excl = (i64)excl;\n";
+      o << "        if (lane == 0) {\n";
+      o << "          if (tile == ntiles - 1) *(u64*)a.p[" << count_p << "] = excl + run;\n";
+      o << "          s_excl = (i64)excl;\n";
+      o << "        }\n";
       o << "      }\n";
       o << "      __syncthreads();\n";
       o << "      const i64 base = s_excl + s_warp[warp] + inc - c;\n";

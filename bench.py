@@ -283,7 +283,7 @@ def main() -> None:
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--sf", type=float, default=float(os.environ.get("SCX_BENCH_SF", "10")))
+    ap.add_argument("--sf", type=float, default=float(os.environ.get("SCX_BENCH_SF", "100")))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sf", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")

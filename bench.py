@@ -453,9 +453,16 @@ def main() -> None:
             rl_ms.append(tm[0][0].elapsed_time(tm[0][1]))
     k_ms = statistics.median(rl_ms)
     achieved = q1_bytes / (k_ms / 1e3) / 1e9
+    traffic = None      # dram read+write of this kernel from the committed ncu capture
+    tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            tr = json.load(fh)
+        if float(tr.get("sf", -1)) == float(args.sf):
+            traffic = int(tr["dram_bytes_read"]) + int(tr["dram_bytes_write"])
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-                "traffic": None, "kernel": "scx_pipe (Q1 fused scan + dense group-by, JIT)",
+                "traffic": traffic, "kernel": "scx_pipe (Q1 fused scan + dense group-by, JIT)",
                 "alg_bytes_per_launch": q1_bytes, "launch_ms": round(k_ms, 4),
                 "peak_source": pk["source"]}
 

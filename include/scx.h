@@ -49,11 +49,11 @@ extern "C" {
 
 /* ---- limits of one pipeline descriptor --------------------------------- */
 #define SCX_MAX_BASE      12   /* scanned (TMA-staged) columns              */
-#define SCX_MAX_SLOTS     20   /* base + probe-payload operand slots        */
+#define SCX_MAX_SLOTS     32   /* base + probe-payload operand slots        */
 #define SCX_MAX_ATOMS     40
 #define SCX_MAX_SETWORDS  128  /* dictionary-set bitmaps, 32 codes / word   */
 #define SCX_MAX_LUT       512  /* dictionary code -> string-rank tables     */
-#define SCX_MAX_PROBES    5
+#define SCX_MAX_PROBES    8
 #define SCX_MAX_POLYS     4    /* polynomial comparison atoms per pipeline  */
 #define SCX_MAX_PAYLOAD   6
 #define SCX_MAX_MEASURES  8
@@ -85,6 +85,9 @@ extern "C" {
 #define SCX_HT_DIRECT   1      /* dense key range: vals[packed key]           */
 #define SCX_HT_BITMAP   2      /* semi/anti membership: bit [packed key] of
                                   the u32 words at vals, cap = key domain    */
+#define SCX_HT_IDENTITY 3      /* build key column is lo, lo+1, ...: the
+                                  packed key IS the build row (< cap rows),
+                                  no table at all                            */
 
 /* aggregate ops (relops.py:11, AGG_OPS) */
 #define SCX_AGG_SUM     0
@@ -181,6 +184,8 @@ typedef struct scx_probe {
   scx_lookup table;
   scx_column payload[SCX_MAX_PAYLOAD];   /* build-side columns, gathered ... */
   int32_t payload_slot[SCX_MAX_PAYLOAD]; /* ... into these operand slots     */
+  scx_pred after;      /* filter applied right after this probe (atoms on
+                          slots available at this stage)                  */
 } scx_probe;
 
 typedef struct scx_sink {

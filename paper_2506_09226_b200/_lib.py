@@ -17,13 +17,13 @@ LIB_PATH = os.path.join(HERE, "libscx.so")
 
 # ---- constants (scx.h) ---------------------------------------------------
 SCX_I8, SCX_I16, SCX_I32, SCX_I64, SCX_U8, SCX_U16, SCX_F64, SCX_U32 = range(8)
-MAX_BASE, MAX_SLOTS, MAX_ATOMS, MAX_SETWORDS, MAX_LUT = 12, 20, 40, 128, 512
-MAX_PROBES, MAX_PAYLOAD, MAX_MEASURES, MAX_GKEYS, MAX_OUT, MAX_KEYS = 5, 6, 8, 4, 16, 4
+MAX_BASE, MAX_SLOTS, MAX_ATOMS, MAX_SETWORDS, MAX_LUT = 12, 32, 40, 128, 512
+MAX_PROBES, MAX_PAYLOAD, MAX_MEASURES, MAX_GKEYS, MAX_OUT, MAX_KEYS = 8, 6, 8, 4, 16, 4
 MAX_POLYS = 4
 ATOM_RANGE, ATOM_SET, ATOM_DIFF, ATOM_POLY = 0, 1, 2, 3
 XFORM_NONE, XFORM_YEAR = 0, 1
 JOIN_SEMI, JOIN_ANTI, JOIN_INNER, JOIN_LEFT = 0, 1, 2, 3
-HT_HASH, HT_DIRECT, HT_BITMAP = 0, 1, 2
+HT_HASH, HT_DIRECT, HT_BITMAP, HT_IDENTITY = 0, 1, 2, 3
 AGG_SUM, AGG_COUNT, AGG_MIN, AGG_MAX = 0, 1, 2, 3
 SINK_AGG_DENSE, SINK_AGG_HASH, SINK_COMPACT, SINK_COUNT, SINK_BITMAP = 0, 1, 2, 3, 4
 EMPTY_KEY = 0xFFFFFFFFFFFFFFFF
@@ -75,7 +75,8 @@ class Lookup(C.Structure):
 
 class Probe(C.Structure):
     _fields_ = [("kind", i32), ("n_payload", i32), ("key", KeySpec), ("table", Lookup),
-                ("payload", Column_ * MAX_PAYLOAD), ("payload_slot", i32 * MAX_PAYLOAD)]
+                ("payload", Column_ * MAX_PAYLOAD), ("payload_slot", i32 * MAX_PAYLOAD),
+                ("after", Pred)]
 
 
 class Sink(C.Structure):

@@ -633,7 +633,15 @@ struct Gen {
     o << "    u32 idx" << pi << "[V];\n    {\n";
     o << "      const u32* vals = (const u32*)a.p[" << vals_p << "];\n";
     o << "      const u64 cap = a.p[" << cap_p << "];\n";
-    if (pb.table.kind == SCX_HT_BITMAP) {
+    if (pb.table.kind == SCX_HT_IDENTITY) {
+      // dense surrogate-key build side: the packed key is the build row
+      o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
+      o << "        idx" << pi << "[r] = SCX_NOROW;\n";
+      o << "        if ((sel >> r) & 1u) {\n";
+      pack_key(pb.key, "r", nullptr, 0, "key", "kin");
+      o << "          if (kin && key < cap) idx" << pi << "[r] = (u32)key;\n";
+      o << "        }\n      }\n";
+    } else if (pb.table.kind == SCX_HT_BITMAP) {
       if (pb.kind != SCX_JOIN_SEMI && pb.kind != SCX_JOIN_ANTI) { err = "bitmap probe needs a semi/anti join"; return; }
       o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
       o << "        idx" << pi << "[r] = SCX_NOROW;\n";
@@ -790,7 +798,10 @@ struct Gen {
     o << "    }\n";
     // when rem == 0 the word arrays are uninitialised but sel == 0 masks every use
     emit_pred(P.pre, "pre-predicate");
-    for (int p = 0; p < P.n_probes; ++p) emit_probe(p);
+    for (int p = 0; p < P.n_probes; ++p) {
+      emit_probe(p);
+      emit_pred(P.probe[p].after, "filter after probe");
+    }
     emit_pred(P.post, "post-predicate");
 
     // ---- sink per row ----

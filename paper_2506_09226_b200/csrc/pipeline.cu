@@ -517,7 +517,10 @@ _Pragma("unroll")
     for (int r = 0; r < R; ++r) sel |= (tl.row(r) < rows) ? (1u << r) : 0u;
 
     sel = eval_pred<R>(tl, P.pre, H.setwords, sel);
-    for (int p = 0; p < P.n_probes; ++p) sel = run_probe<R>(tl, P.probe[p], sel);
+    for (int p = 0; p < P.n_probes; ++p) {
+      sel = run_probe<R>(tl, P.probe[p], sel);
+      sel = eval_pred<R>(tl, P.probe[p].after, H.setwords, sel);
+    }
     sel = eval_pred<R>(tl, P.post, H.setwords, sel);
 
     if constexpr (NC > 0) {
@@ -811,7 +814,7 @@ static int plan_launch(const scx_pipeline& P, Launch& L) {
     return SCX_EUNSUPPORTED;
   }
   for (int p = 0; p < P.n_probes; ++p)
-    if (P.probe[p].kind == SCX_JOIN_LEFT || P.probe[p].table.kind == SCX_HT_BITMAP) {
+    if (P.probe[p].kind == SCX_JOIN_LEFT || P.probe[p].table.kind >= SCX_HT_BITMAP) {
       set_error("interpreter: left joins need the JIT path (unset SCX_JIT=0)");
       return SCX_EUNSUPPORTED;
     }

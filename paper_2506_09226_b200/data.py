@@ -415,7 +415,8 @@ def save_dataset(ds: Dataset, path: str) -> None:
         for cname, c in t.columns.items():
             np.save(os.path.join(path, f"{tname}.{cname}.npy"), c.values)
             cols[cname] = {"kind": c.kind, "scale": c.scale, "lo": c.lo, "hi": c.hi,
-                           "dictionary": list(c.dictionary) if c.dictionary else None}
+                           "dictionary": list(c.dictionary) if c.dictionary else None,
+                           "dense": bool(c.dense)}
         meta["tables"][tname] = cols
     tmp = os.path.join(path, "manifest.json.tmp")
     with open(tmp, "w") as fh:
@@ -436,7 +437,7 @@ def load_dataset(path: str, mmap: bool = True) -> Dataset:
                         mmap_mode="r" if mmap else None)
             hc[cname] = HostColumn(m["kind"], v, m["scale"],
                                    tuple(m["dictionary"]) if m["dictionary"] else None,
-                                   m["lo"], m["hi"])
+                                   m["lo"], m["hi"], bool(m.get("dense", False)))
         tables[tname] = HostTable(hc)
     return Dataset(tables, meta["sf"], meta["skew"], meta["seed"])
 

@@ -134,6 +134,16 @@ class Lookup:
             (cols[0].hi - cols[0].lo + 1) if cols[0].hi >= cols[0].lo else 1)
         self.lk = L.Lookup()
         self._keys = None
+        self._unique = None
+        if len(cols) == 1 and cols[0].dense and cols[0].row_count == n and n == span:
+            # surrogate key column (row i holds lo + i): the packed key is
+            # the build row -- no table to build, nothing to read but payload
+            self.lk.kind = L.HT_IDENTITY
+            self.lk.cap = n
+            self.lk.vals = 0
+            self.lk.keys = 0
+            self._unique = True
+            return
         if span <= max(4 * n, 1 << 16) and span <= (1 << 31):
             self.lk.kind = L.HT_DIRECT
             self.lk.cap = span
@@ -157,7 +167,6 @@ class Lookup:
         spec = self.packing.spec(list(range(len(cols))))
         L.call("scx_lookup_build", C.byref(self.lk), colarr, len(cols), C.byref(spec), n,
                _ptr(self._flags), _stream())
-        self._unique = None
 
     @property
     def unique(self) -> bool:
@@ -229,6 +238,7 @@ class ProbeStage:
     probe_keys: list[str]       # names in the view (probe side)
     kind: int                   # JOIN_*
     payload: list[str] = field(default_factory=list)   # right column names exposed
+    after: Pred = field(default_factory=Pred.true)      # filter right after this probe
 
 
 class TableView:
@@ -401,13 +411,36 @@ def filter_table(table, predicate) -> TableView:
         v.origin[name] = ("base", name)
         pred = Pred.atom(Atom("range", name, 1, 1))
     v = v._copy()
-    if not v.probes and all(v.origin[n][0] == "base" for n in pred.columns if n in v.origin):
-        _check_pred_columns(v, pred, allow_payload=False)
-        v.pre = v.pre & pred
-    else:
-        _check_pred_columns(v, pred, allow_payload=True)
-        v.post = v.post & pred
+    _check_pred_columns(v, pred, allow_payload=True)
+    _place_pred(v, pred)
     return v
+
+
+def _place_pred(v: TableView, pred: Pred) -> None:
+    """Attach a filter (in place on a copied view) at the earliest stage where
+    its columns exist: base-column atoms before any probe (pre-predicate),
+    atoms on a join's payload right after that probe -- so a selective
+    condition drops rows before the later (random-access) probes."""
+    if pred.is_true:
+        return
+
+    def stage(cols) -> int:
+        return max((v.origin[c][1] if v.origin[c][0] == "payload" else -1 for c in cols),
+                   default=-1)
+
+    if len(pred.clauses) == 1:
+        groups: dict[int, list] = {}
+        for a in pred.clauses[0]:
+            groups.setdefault(stage(a.columns), []).append(a)
+        parts = [(s, Pred([tuple(atoms)])) for s, atoms in groups.items()]
+    else:
+        parts = [(stage(pred.columns), pred)]
+    for s, p in parts:
+        if s < 0:
+            v.pre = v.pre & p
+        else:
+            st = v.probes[s]
+            v.probes[s] = ProbeStage(st.lookup, st.probe_keys, st.kind, st.payload, st.after & p)
 
 
 def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
@@ -417,6 +450,10 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
     if not on:
         raise SchemaError("join requires at least one key pair")
     lv = as_view(left)
+    if how == "inner" and isinstance(right, TableView) and len(on) == 1:
+        pushed = _pushdown_join(lv, right, on[0], how)
+        if pushed is not None:
+            return pushed
     if how in ("semi", "anti"):
         rmeta = right.meta if isinstance(right, TableView) else right.columns
         rt = right
@@ -479,6 +516,67 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
     return v
 
 
+def _pushdown_join(lv: TableView, rv: TableView, on: tuple[str, str], how: str):
+    """Join against a *view* of a table keyed by a dense surrogate key without
+    materialising the view: the probe reads the base table directly (identity
+    lookup, row = key - lo) and the view's own predicates and probes are
+    replayed on the gathered payload in the same scan.  E.g. Q3's
+    ``lineitem JOIN filter(orders) SEMI customer`` becomes one pipeline:
+    lineitem -> orders[row] (o_orderdate, o_custkey, ...) -> customer bitmap
+    -> o_orderdate < d.  Returns None when the shape does not fit (the caller
+    then materialises the right side as before)."""
+    lname, rname = on
+    if rv.origin.get(rname, ("x",))[0] != "base":
+        return None
+    rbase = rv.base
+    kc = rbase.column(rname)
+    if not (kc.dense and kc.row_count == rbase.row_count and kc.hi - kc.lo + 1 == kc.row_count):
+        return None
+    if any(n in rv.computed or n in rv.derived for n in rv.visible):
+        return None
+    lc = lv[lname]
+    if not isinstance(lc, ColRef) or lc.col.kind != kc.kind or kc.kind not in _KEY_KINDS:
+        return None
+    if how == "inner":
+        overlap = set(lv.visible) & set(rv.visible)
+        if overlap:
+            raise SchemaError(f"inner join would duplicate columns: {sorted(overlap)}")
+    # right-side columns the replayed plan reads from the base table
+    need = {n for n in (rv.visible if how == "inner" else []) if rv.origin[n][0] == "base"}
+    need |= {n for n in rv.pre.columns | rv.post.columns if rv.origin[n][0] == "base"}
+    for st in rv.probes:
+        need |= {k for k in set(st.probe_keys) | st.after.columns if rv.origin[k][0] == "base"}
+    need = sorted(need)
+    added = set(need) | {n for st in rv.probes for n in st.payload}
+    if (len(need) > L.MAX_PAYLOAD or len(lv.probes) + 1 + len(rv.probes) > L.MAX_PROBES
+            or added & set(lv.meta) or len(lv.meta) + len(added) > L.MAX_SLOTS):
+        return None
+    lookup = Lookup(rbase.select([rname] + [n for n in need if n != rname]), [rname])
+    if lookup.lk.kind != L.HT_IDENTITY:
+        return None
+    v = lv._copy()
+    p0 = ProbeStage(lookup, [lname], L.JOIN_INNER, [], rv.pre)
+    pidx = len(v.probes)
+    for n in need:
+        p0.payload.append(n)
+        v.meta[n] = rbase.column(n)
+        v.origin[n] = ("payload", pidx, n)
+    v.probes.append(p0)
+    for st in rv.probes:
+        idx = len(v.probes)
+        v.probes.append(ProbeStage(st.lookup, list(st.probe_keys), st.kind, list(st.payload),
+                                   st.after))
+        for n in st.payload:
+            v.meta[n] = rv.meta[n]
+            v.origin[n] = ("payload", idx, n)
+    last = v.probes[-1]
+    v.probes[-1] = ProbeStage(last.lookup, last.probe_keys, last.kind, last.payload,
+                              last.after & rv.post)
+    if how == "inner":
+        v.visible += [n for n in rv.visible if n not in v.visible]
+    return v
+
+
 # ---------------------------------------------------------------------------
 # pipeline construction
 # ---------------------------------------------------------------------------
@@ -499,6 +597,8 @@ class _Builder:
         P.n_rows = v.base.row_count
         names = set(extra)
         names |= v.pre.columns | v.post.columns
+        for st in v.probes:
+            names |= st.after.columns
         for st in v.probes:
             names |= set(st.probe_keys)
         base = [n for n in v.base.column_names if n in names and v.origin[n][0] == "base"]
@@ -543,6 +643,8 @@ class _Builder:
                 pb.payload[j] = st.lookup.table.column(n).scx()
                 pb.payload_slot[j] = self.slot[n]
         self._pred(P.pre, v.pre)
+        for i, st in enumerate(v.probes):
+            self._pred(P.probe[i].after, st.after)
         self._pred(P.post, v.post)
 
     # ---- atoms ----

@@ -115,6 +115,7 @@ class HostColumn:
     dictionary: tuple[str, ...] | None = None
     lo: int = 0
     hi: int = -1
+    dense: bool = False                  # row i holds lo + i (a surrogate key column)
 
     @staticmethod
     def from_ints(kind: str, a: np.ndarray) -> "HostColumn":
@@ -125,7 +126,8 @@ class HostColumn:
     @staticmethod
     def int_range(start: int, stop: int) -> "HostColumn":
         dt = narrow_dtype(start, max(start, stop - 1))
-        return HostColumn("int64", np.arange(start, stop, dtype=dt), 0, None, start, stop - 1)
+        return HostColumn("int64", np.arange(start, stop, dtype=dt), 0, None, start, stop - 1,
+                          True)
 
     @staticmethod
     def from_codes(codes: np.ndarray, dictionary: tuple[str, ...]) -> "HostColumn":
@@ -275,10 +277,10 @@ class Column:
     ``scale`` the fixed-point exponent of float64 columns.
     """
 
-    __slots__ = ("kind", "data", "scale", "dictionary", "lo", "hi")
+    __slots__ = ("kind", "data", "scale", "dictionary", "lo", "hi", "dense")
 
     def __init__(self, kind: str, data, scale: int = 0, dictionary=None, lo: int = 0,
-                 hi: int = -1):
+                 hi: int = -1, dense: bool = False):
         if kind not in KINDS:
             raise SchemaError(f"unknown column kind {kind!r}")
         if kind == "dict" and dictionary is None:
@@ -291,6 +293,9 @@ class Column:
         self.dictionary = tuple(dictionary) if dictionary is not None else None
         self.lo = lo
         self.hi = hi
+        # row i holds lo + i: a join on this column needs no lookup table
+        # (row = key - lo), see relops.Lookup
+        self.dense = dense
 
     # ---- construction ----
     @staticmethod
@@ -301,7 +306,8 @@ class Column:
         if n:
             src = torch.from_numpy(np.ascontiguousarray(hc.values))
             buf.copy_(src, non_blocking=False)
-        return Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi)
+        return Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
+                      hc.dense and n == hc.hi - hc.lo + 1)
 
     @staticmethod
     def from_numpy(kind: str, values, dictionary=None, device=None) -> "Column":

@@ -716,9 +716,14 @@ struct Gen {
       // register accumulators; narrower chunks trade load width for occupancy
       const int acc_regs = (S.kind == SCX_SINK_AGG_DENSE && S.n_cells <= 8)
                                ? 2 * (S.n_cells < 1 ? 1 : S.n_cells) * S.n_measures : 0;
-      int probe_regs = 0;   // per row: idx + transient key / slot / first-probe words
-      for (int p = 0; p < P.n_probes; ++p)
-        probe_regs += P.probe[p].table.kind == SCX_HT_HASH ? 7 : 3;
+      // per row: the live idx of every probe + the transient key / slot /
+      // first-probe words of the widest probe stage (stages are sequential)
+      int probe_regs = 0;
+      for (int p = 0; p < P.n_probes; ++p) {
+        const int t = P.probe[p].table.kind == SCX_HT_HASH ? 6 : 2;
+        probe_regs = probe_regs > t ? probe_regs : t;
+      }
+      probe_regs += P.n_probes;
       while (V > 4 && V * (row_bytes + payload_bytes) / 4 + V * probe_regs + acc_regs > 64) V /= 2;
     }
     const int64_t tile_rows = (int64_t)kTPB * V;

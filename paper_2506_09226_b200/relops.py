@@ -1178,12 +1178,14 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
     M = len(measures)
     # dense packed-key domain (TPC-H surrogate keys): direct-addressed groups,
     # slot = packed key, no hashing / CAS (sink.n_cells = 1 marks it)
+    filtered = bool(v.probes) or not v.pre.is_true or not v.post.is_true
+    if filtered and bound > (1 << 20) and (dom > (1 << 24) or dom > 4 * bound):
+        # a large, filtered input whose table would be big: one count pass
+        # sizes it to the surviving rows (cheaper than filling and compacting
+        # a table sized for the unfiltered input)
+        bound = min(bound, max(count_rows(v), 1))
     direct = len(keys) >= 1 and dom <= max(4 * bound, 1 << 16) and dom <= (1 << 31)
     S.n_cells = 1 if direct else 0
-    if not direct and bound > (1 << 20) and (v.probes or not v.pre.is_true or not v.post.is_true):
-        # a large, filtered input: one count pass sizes the table to the rows
-        # that survive (cheaper than filling / compacting a table sized for n)
-        bound = min(bound, max(count_rows(v), 1))
     wide = [bool(S.m[j]._pad) for j in range(M)]
     woff = list(np.cumsum([0] + [2 if w else 1 for w in wide])[:-1])
     W = int(sum(2 if w else 1 for w in wide))          # accumulator words per group

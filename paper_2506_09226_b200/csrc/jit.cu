@@ -709,12 +709,19 @@ struct Gen {
     // rows per thread-chunk: 16 keeps a 1-byte column at one 16-byte load;
     // wide rows drop to 8 to bound registers
     V = (row_bytes + payload_bytes <= 24 && max_w <= 4) ? 16 : 8;
-    if (S.kind == SCX_SINK_AGG_DENSE && S.n_cells > 1 && S.n_cells <= 8) V = 8;
-    if (S.kind == SCX_SINK_AGG_HASH) V = 8;
+    // multi-cell dense group-by: per-thread private accumulators in shared
+    // memory ([cell][measure][thread], conflict-free, indexed by the row's
+    // cell) -- no per-cell predicated adds, no accumulator registers
+    const bool dense_priv = S.kind == SCX_SINK_AGG_DENSE && S.n_cells > 1 &&
+                            (int64_t)S.n_cells * S.n_measures * kTPB * 8 <= 96 * 1024;
+    if (S.kind == SCX_SINK_AGG_DENSE && !dense_priv && S.n_cells > 1 && S.n_cells <= 8) V = 8;
+    // hash sinks are bound by dependent CAS / atomic round trips: fewer rows per
+    // thread = more of them in flight
+    if (S.kind == SCX_SINK_AGG_HASH) V = 4;
     {
       // register budget for 2 CTAs/SM (<= 128 regs): raw row words + dense
       // register accumulators; narrower chunks trade load width for occupancy
-      const int acc_regs = (S.kind == SCX_SINK_AGG_DENSE && S.n_cells <= 8)
+      const int acc_regs = (S.kind == SCX_SINK_AGG_DENSE && !dense_priv && S.n_cells <= 8)
                                ? 2 * (S.n_cells < 1 ? 1 : S.n_cells) * S.n_measures : 0;
       // per row: the live idx of every probe + the transient key / slot /
       // first-probe words of the widest probe stage (stages are sequential)
@@ -729,9 +736,13 @@ struct Gen {
     const int64_t tile_rows = (int64_t)kTPB * V;
     tiles_out = (int)((P.n_rows + tile_rows - 1) / tile_rows);
 
-    const bool dense_reg = S.kind == SCX_SINK_AGG_DENSE && S.n_cells <= 8;
+    const bool dense_reg = S.kind == SCX_SINK_AGG_DENSE && !dense_priv && S.n_cells <= 8;
     const int M = S.n_measures;
-    const int NC = dense_reg ? (S.n_cells < 1 ? 1 : S.n_cells) : 0;
+    const int NC = (dense_reg || dense_priv) ? (S.n_cells < 1 ? 1 : S.n_cells) : 0;
+    auto ident = [&](int m) -> const char* {
+      return S.m[m].op == SCX_AGG_MIN ? "0x7fffffffffffffffll"
+           : S.m[m].op == SCX_AGG_MAX ? "(-0x7fffffffffffffffll - 1)" : "0ll";
+    };
 
     o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", 2) KNAME(const __grid_constant__ Args a) {\n";
     o << "  constexpr int V = " << V << ";\n";
@@ -745,7 +756,13 @@ struct Gen {
     std::vector<int> out_p;
     if (S.kind == SCX_SINK_AGG_DENSE) {
       acc_p = param(S.acc);
-      if (dense_reg) {
+      if (dense_priv) {
+        dyn_smem = (size_t)NC * M * kTPB * 8;
+        o << "  extern __shared__ __align__(16) i64 pacc[];\n";
+        for (int c = 0; c < NC; ++c)
+          for (int m = 0; m < M; ++m)
+            o << "  pacc[" << (c * M + m) * kTPB << " + tid] = " << ident(m) << ";\n";
+      } else if (dense_reg) {
         o << "  i64 acc[" << NC << "][" << M << "];\n";
         for (int c = 0; c < NC; ++c)
           for (int m = 0; m < M; ++m)
@@ -820,7 +837,16 @@ struct Gen {
         o << "      cell = cell * " << S.gcard[i] << " + (int)" << v << ";\n";
       }
       for (int m = 0; m < M; ++m) o << "      const i64 m" << m << " = " << measure_expr(S.m[m], "r") << ";\n";
-      if (dense_reg) {
+      if (dense_priv) {
+        o << "      i64* pa = pacc + cell * " << M * kTPB << " + tid;\n";
+        for (int m = 0; m < M; ++m) {
+          const int op = S.m[m].op;
+          const std::string slot = "pa[" + std::to_string(m * kTPB) + "]";
+          if (op == SCX_AGG_MIN) o << "      " << slot << " = smin(" << slot << ", m" << m << ");\n";
+          else if (op == SCX_AGG_MAX) o << "      " << slot << " = smax(" << slot << ", m" << m << ");\n";
+          else o << "      " << slot << " += m" << m << ";\n";
+        }
+      } else if (dense_reg) {
         for (int c = 0; c < NC; ++c) {
           if (NC > 1) o << "      if (cell == " << c << ") {\n";
           for (int m = 0; m < M; ++m) {
@@ -984,13 +1010,16 @@ struct Gen {
     o << "  }\n";  // tile loop
 
     // ---- epilogues ----
-    if (S.kind == SCX_SINK_AGG_DENSE && dense_reg) {
+    if (S.kind == SCX_SINK_AGG_DENSE && (dense_reg || dense_priv)) {
       o << "  __shared__ i64 red[" << kTPB / 32 << "][" << NC * M << "];\n";
       for (int c = 0; c < NC; ++c)
         for (int m = 0; m < M; ++m) {
           const int op = S.m[m].op;
           const char* f = op == SCX_AGG_MIN ? "wmin" : op == SCX_AGG_MAX ? "wmax" : "wsum";
-          o << "  { const i64 v = " << f << "(acc[" << c << "][" << m << "]); if (lane == 0) red[warp][" << c * M + m << "] = v; }\n";
+          const std::string src = dense_priv
+              ? "pacc[" + std::to_string((c * M + m) * kTPB) + " + tid]"
+              : "acc[" + std::to_string(c) + "][" + std::to_string(m) + "]";
+          o << "  { const i64 v = " << f << "(" << src << "); if (lane == 0) red[warp][" << c * M + m << "] = v; }\n";
         }
       o << "  __syncthreads();\n";
       o << "  if (tid < " << NC * M << ") {\n";

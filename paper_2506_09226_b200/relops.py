@@ -160,6 +160,8 @@ class Lookup:
             self._vals = alloc(cap, np.uint32)
             self.lk.keys = self._keys.data_ptr()
             self.lk.vals = self._vals.data_ptr()
+        if self.keys and set(self.keys) == set(getattr(table, "unique_keys", ())):
+            self._unique = True            # group-by output keyed on these columns
         self._flags = alloc(4, np.uint32)
         L.call("scx_lookup_clear", C.byref(self.lk), _stream())
         fill_i64(self._flags.view(_torch().int64), 0)
@@ -807,7 +809,10 @@ def _materialize(v: TableView) -> ColumnTable:
     S.count = count.data_ptr()
     b.run()
     m = int(_to_host(count)[0]) if n else 0
-    return ColumnTable({name: v.meta[name].like(outs[name][:m]) for name in cols})
+    # probes build on unique keys, so a filtered / joined row set keeps the
+    # base table's key property
+    return ColumnTable({name: v.meta[name].like(outs[name][:m]) for name in cols},
+                       v.base.unique_keys)
 
 
 def count_rows(t) -> int:
@@ -1005,7 +1010,7 @@ def _group_with_dependent_keys(v, keys, fd, aggs, cross, timing, sort) -> Column
         return None
     cols = {k: g.column(f"__fd_{k}") if k in fd else g.column(k) for k in keys}
     cols.update({name: g.column(name) for name in aggs})
-    return ColumnTable(cols)
+    return ColumnTable(cols, tuple(keys))
 
 
 def regroup(full, keys: list[str], aggs: dict[str, tuple]) -> ColumnTable:
@@ -1126,7 +1131,7 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
                              dtype=np.float64)
             out[a.out] = Column.from_numpy("float64", arr)
     # keys first, then aggregates (relops.py:121,131-158)
-    return ColumnTable(out)
+    return ColumnTable(out, tuple(keys))
 
 
 def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> ColumnTable:
@@ -1194,7 +1199,9 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
         cap *= 2
     if direct:
         cap = int(dom)
-    flags = alloc(4, np.uint32)
+    stat = alloc(4, np.int64)          # [u32 flags x 4][count] -> one D2H per attempt
+    flags = stat[:2].view(torch.uint32)
+    cnt = stat[2:3].view(torch.uint64)
     while True:
         gkeys = alloc(cap, np.uint64)
         accb = alloc(cap * W, np.int64)
@@ -1206,28 +1213,29 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
                 pattern.append(0)
         pat = (C.c_int64 * W)(*pattern)
         L.call("scx_fill_rows", _ptr(accb), cap, W, pat, _stream())
-        fill_i64(flags.view(torch.int64), 0)
+        fill_i64(stat, 0)
         S.gkeys, S.acc, S.gcap, S.flags = gkeys.data_ptr(), accb.data_ptr(), cap, flags.data_ptr()
         b.run()
-        if int(_to_host(flags)[0]) == 0:
+        out_keys = alloc(cap, np.uint64)
+        out_acc = alloc(cap * W, np.int64)
+        if direct:
+            # slot order == packed-key order: ordered compaction, no sort
+            ws = alloc(max(2, L.load().scx_direct_agg_workspace(cap) // 8), np.int64)
+            L.call("scx_direct_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
+                   _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
+        else:
+            L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
+                   _ptr(out_acc), _ptr(cnt), _stream())
+        st = _to_host(stat)
+        if int(st[0]) & 0xFFFFFFFF == 0:
             break
         if direct or cap >= (1 << 34):
             raise SchemaError("group table overflow (group key outside its proven range)")
         cap *= 4   # table overflowed: rerun with a bigger one
-    out_keys = alloc(cap, np.uint64)
-    out_acc = alloc(cap * W, np.int64)
-    cnt = alloc(1, np.uint64)
+    G = int(st[2])
     if direct:
-        # slot order == packed-key order: ordered compaction, no sort
-        ws = alloc(max(2, L.load().scx_direct_agg_workspace(cap) // 8), np.int64)
-        L.call("scx_direct_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
-               _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
-        G = int(_to_host(cnt)[0])
         skeys, perm = out_keys[:G], None
     else:
-        L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
-               _ptr(out_acc), _ptr(cnt), _stream())
-        G = int(_to_host(cnt)[0])
         if sort:
             # sort groups by packed key (== lexicographic key order)
             skeys, perm = sort_pairs(out_keys[:G], None, total)
@@ -1302,7 +1310,7 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
             dst = alloc(G, np.float64)
             L.call("scx_fixed_to_f64", _ptr(s_col), 1, G, k, _ptr(c_col), 1, _ptr(dst), _stream())
             out[a.out] = Column("float64", dst, -1, None, 0, -1)
-    return ColumnTable(out)
+    return ColumnTable(out, tuple(keys))
 
 
 # ---------------------------------------------------------------------------

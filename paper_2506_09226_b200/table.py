@@ -381,12 +381,15 @@ class Column:
 class ColumnTable:
     """Immutable named device columns of equal length (table.py:119-217)."""
 
-    def __init__(self, columns: dict[str, Column]):
+    def __init__(self, columns: dict[str, Column], unique_keys: tuple = ()):
         lengths = {c.row_count for c in columns.values()}
         if len(lengths) > 1:
             raise SchemaError(f"ragged columns: { {n: c.row_count for n, c in columns.items()} }")
         self._columns = dict(columns)
         self._rows = lengths.pop() if lengths else 0
+        # column set known to be a key (group-by output): a join building on
+        # it needs no duplicate check (relops.Lookup)
+        self.unique_keys = tuple(unique_keys) if set(unique_keys) <= set(columns) else ()
 
     # ---- reference surface ----
     @property
@@ -423,15 +426,16 @@ class ColumnTable:
         return {n: c.kind for n, c in self._columns.items()}
 
     def select(self, names: list[str]) -> "ColumnTable":
-        return ColumnTable({n: self.column(n) for n in names})
+        return ColumnTable({n: self.column(n) for n in names}, self.unique_keys)
 
     def with_column(self, name: str, col: Column) -> "ColumnTable":
         cols = dict(self._columns)
         cols[name] = col
-        return ColumnTable(cols)
+        return ColumnTable(cols, self.unique_keys if name not in self.unique_keys else ())
 
     def rename(self, mapping: dict[str, str]) -> "ColumnTable":
-        return ColumnTable({mapping.get(n, n): c for n, c in self._columns.items()})
+        return ColumnTable({mapping.get(n, n): c for n, c in self._columns.items()},
+                           tuple(mapping.get(k, k) for k in self.unique_keys))
 
     def take(self, idx) -> "ColumnTable":
         from . import relops
@@ -443,7 +447,8 @@ class ColumnTable:
 
     def head(self, n: int) -> "ColumnTable":
         n = max(0, min(n, self._rows))
-        return ColumnTable({k: c.like(c.data[:n]) for k, c in self._columns.items()})
+        return ColumnTable({k: c.like(c.data[:n]) for k, c in self._columns.items()},
+                           self.unique_keys)
 
     def isin(self, name: str, values: list[str]):
         from .expr import isin

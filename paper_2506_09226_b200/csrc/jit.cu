@@ -48,6 +48,9 @@ namespace scx {
 
 int interp_pipeline_run(const scx_pipeline* d, void* stream);
 int64_t interp_status_words(const scx_pipeline* d);
+int compact_finish(uint64_t* status, int64_t grid, char* stage, int64_t stage_rows,
+                   const scx_column* outs, int n_out, int64_t region_rows, uint64_t* count,
+                   cudaStream_t st);
 
 namespace jit {
 
@@ -367,6 +370,7 @@ struct Gen {
   int V = 16;
   int n_globals = 0;
   size_t dyn_smem = 0;
+  int stage_p = -1, stage_rows_p = -1;   // COMPACT: staging base / rows, bound at launch
   std::string err;
 
   explicit Gen(const scx_pipeline& p) : P(p) {}
@@ -790,11 +794,30 @@ struct Gen {
       o << "  i64* gacc = (i64*)a.p[" << acc_p << "];\n";
       o << "  const u64 gmask = a.p[" << gcap_p << "] - 1;\n";
     } else if (S.kind == SCX_SINK_COMPACT) {
+      // Stable compaction without a cross-CTA dependency: CTA b owns the
+      // contiguous tiles [b*tpc, (b+1)*tpc) and writes its selected rows, in
+      // order, into its own staging region; libscx then scans the per-CTA
+      // counts and moves the regions into place (jit::compact_finish).
       status_p = param(S.status);
-      count_p = param(S.count);
-      for (int i = 0; i < S.n_out; ++i) out_p.push_back(param(S.out[i].ptr));
+      stage_p = param(0);
+      stage_rows_p = param(0);
       o << "  __shared__ u32 s_warp[" << kTPB / 32 << "];\n";
-      o << "  __shared__ i64 s_excl;\n";
+      o << "  __shared__ u32 s_tot;\n";
+      o << "  const i64 tpc = (ntiles + gridDim.x - 1) / gridDim.x;\n";
+      o << "  const i64 tbeg = (i64)blockIdx.x * tpc;\n";
+      o << "  const i64 tend = tbeg + tpc < ntiles ? tbeg + tpc : ntiles;\n";
+      o << "  const u64 srows = a.p[" << stage_rows_p << "];\n";
+      o << "  char* stage = (char*)a.p[" << stage_p << "];\n";
+      o << "  u64 cta_pos = 0;\n";
+      uint64_t off_terms = 0;
+      (void)off_terms;
+      for (int i = 0; i < S.n_out; ++i) {
+        const char* t = ctype(S.out[i].dtype);
+        o << "  " << t << "* sdst" << i << " = (" << t << "*)(stage";
+        for (int j = 0; j < i; ++j)
+          o << " + ((srows * " << dtype_size(S.out[j].dtype) << "ull + 15ull) & ~15ull)";
+        o << ");\n";
+      }
     } else if (S.kind == SCX_SINK_COUNT) {
       count_p = param(S.count);
       o << "  u64 cnt = 0;\n";
@@ -808,7 +831,8 @@ struct Gen {
       return SCX_EINVAL;
     }
 
-    o << "  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+    if (S.kind == SCX_SINK_COMPACT) o << "  for (i64 tile = tbeg; tile < tend; ++tile) {\n";
+    else o << "  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
     o << "    const i64 row0 = (tile * " << kTPB << " + tid) * (i64)V;\n";
     o << "    const bool full = row0 + V <= n;\n";
     o << "    const int rem = row0 >= n ? 0 : (int)(n - row0 < V ? n - row0 : V);\n";
@@ -954,55 +978,24 @@ struct Gen {
       o << "#pragma unroll\n      for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, inc, d); if (lane >= d) inc += y; }\n";
       o << "      if (lane == 31) s_warp[warp] = inc;\n";
       o << "      __syncthreads();\n";
-      // warp 0: scan the per-warp counts, then a warp-cooperative decoupled
-      // look-back that inspects 32 predecessor tiles per step (a serial
-      // one-tile walk costs an L2 round trip per in-flight tile)
       o << "      if (warp == 0) {\n";
       o << "        const u32 wc = lane < " << kTPB / 32 << " ? s_warp[lane] : 0u;\n";
       o << "        u32 wi = wc;\n";
       o << "#pragma unroll\n        for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, wi, d); if (lane >= d) wi += y; }\n";
-      o << "        const u64 run = __shfl_sync(0xffffffffu, wi, 31);\n";
       o << "        if (lane < " << kTPB / 32 << ") s_warp[lane] = wi - wc;\n";
-      o << "        u64* status = (u64*)a.p[" << status_p << "];\n";
-      o << "        const u64 kA = 1ull << 62, kP = 2ull << 62, kV = (1ull << 62) - 1;\n";
-      o << "        u64 excl = 0;\n";
-      o << "        if (tile == 0) { if (lane == 0) st_release(status, kP | run); }\n";
-      o << "        else {\n";
-      o << "          if (lane == 0) st_release(status + tile, kA | run);\n";
-      o << "          i64 j = tile - 1;\n";
-      o << "          while (true) {\n";
-      o << "            const i64 idx = j - lane;\n";
-      o << "            const u64 w = idx >= 0 ? ld_acquire(status + idx) : kP;\n";
-      o << "            const u64 f = w & ~kV;\n";
-      o << "            const u32 pm = __ballot_sync(0xffffffffu, f == kP);\n";
-      o << "            const u32 nr = __ballot_sync(0xffffffffu, f == 0);\n";
-      o << "            const int fp = pm ? __ffs(pm) - 1 : 31;\n";
-      o << "            const u32 need = fp == 31 ? 0xffffffffu : ((2u << fp) - 1u);\n";
-      o << "            if (nr & need) continue;\n";
-      o << "            u64 v = (lane <= fp && idx >= 0) ? (w & kV) : 0ull;\n";
-      o << "#pragma unroll\n            for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);\n";
-      o << "            excl += v;\n";
-      o << "            if (pm) break;\n";
-      o << "            j -= 32;\n";
-      o << "          }\n";
-      o << "          if (lane == 0) st_release(status + tile, kP | (excl + run));\n";
-      o << "        }\n";
-      o << "        if (lane == 0) {\n";
-      o << "          if (tile == ntiles - 1) *(u64*)a.p[" << count_p << "] = excl + run;\n";
-      o << "          s_excl = (i64)excl;\n";
-      o << "        }\n";
+      o << "        if (lane == 31) s_tot = wi;\n";
       o << "      }\n";
       o << "      __syncthreads();\n";
-      o << "      const i64 base = s_excl + s_warp[warp] + inc - c;\n";
-      o << "      __syncthreads();\n";   // s_warp / s_excl reused by the next tile
+      o << "      const i64 base = (i64)(tbeg * " << tile_rows << "ll) + (i64)cta_pos + s_warp[warp] + inc - c;\n";
+      o << "      cta_pos += s_tot;\n";
+      o << "      __syncthreads();\n";   // s_warp / s_tot reused by the next tile
       for (int i = 0; i < S.n_out; ++i) {
-        const int s = S.out_slot[i];
-        const int dt = S.out[i].dtype;
-        const char* t = ctype(dt);
-        o << "      { " << t << "* dst = (" << t << "*)a.p[" << out_p[i] << "]; i64 pos = base;\n";
-        o << "#pragma unroll\n        for (int r = 0; r < V; ++r) if ((sel >> r) & 1u) dst[pos++] = (" << t << ")";
-        if (s < 0) o << "(row0 + r);\n";
-        else o << val(s, "r") << ";\n";
+        const int s2 = S.out_slot[i];
+        const char* t = ctype(S.out[i].dtype);
+        o << "      { i64 pos = base;\n";
+        o << "#pragma unroll\n        for (int r = 0; r < V; ++r) if ((sel >> r) & 1u) sdst" << i << "[pos++] = (" << t << ")";
+        if (s2 < 0) o << "(row0 + r);\n";
+        else o << val(s2, "r") << ";\n";
         o << "      }\n";
       }
       o << "    }\n";
@@ -1052,6 +1045,8 @@ struct Gen {
       o << "    else if (op == " << SCX_AGG_MAX << ") { if (v != (-0x7fffffffffffffffll - 1)) atomicMax((long long*)gacc, v); }\n";
       o << "    else atomic_add_i128(gacc, v);\n";
       o << "  }\n";
+    } else if (S.kind == SCX_SINK_COMPACT) {
+      o << "  if (tid == 0) ((u64*)a.p[" << status_p << "])[blockIdx.x] = cta_pos;\n";
     } else if (S.kind == SCX_SINK_COUNT) {
       o << "  { u64 w = cnt;\n";
       o << "#pragma unroll\n    for (int d = 16; d > 0; d >>= 1) w += __shfl_xor_sync(0xffffffffu, w, d);\n";
@@ -1075,6 +1070,8 @@ struct Prepared {
   std::string src, name;
   std::vector<uint64_t> ptrs;
   int tiles = 0;
+  int V = 0;
+  int stage_p = -1, stage_rows_p = -1;
   size_t dyn_smem = 0;
 };
 
@@ -1097,6 +1094,9 @@ static int prepare(const scx_pipeline& P, Prepared& out) {
   }
   out.ptrs = g.ptrs;
   out.dyn_smem = g.dyn_smem;
+  out.V = g.V;
+  out.stage_p = g.stage_p;
+  out.stage_rows_p = g.stage_rows_p;
   return SCX_OK;
 }
 
@@ -1110,12 +1110,68 @@ static bool enabled() {
 
 using namespace scx;
 
+namespace scx {
+namespace jit {
+
+// everything a launch needs: the kernel, its grid, and (COMPACT) the staging
+// layout inside the caller's status buffer
+struct LaunchPlan {
+  Prepared pp;
+  Entry* e = nullptr;
+  int64_t grid = 1;
+  int64_t tpc = 0;            // tiles per CTA (COMPACT)
+  int64_t stage_rows = 0;     // staging rows per output column (COMPACT)
+  int64_t stage_word = 0;     // staging start, in u64 words from `status`
+  int64_t status_words = 0;   // words the caller must provide in sink.status
+};
+
+static int plan_launch(const scx_pipeline& P, LaunchPlan& lp) {
+  int rc = prepare(P, lp.pp);
+  if (rc) return rc;
+  rc = get_function(lp.pp.src, lp.pp.name, lp.e);
+  if (rc) return rc;
+  Driver& drv = driver();
+  if ((int)lp.pp.dyn_smem > lp.e->max_dyn_smem) {
+    int cr = drv.set_attr(lp.e->fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/,
+                          (int)lp.pp.dyn_smem);
+    if (cr) return drv_fail(cr, "cuFuncSetAttribute");
+    lp.e->max_dyn_smem = (int)lp.pp.dyn_smem;
+  }
+  int occ = 0;
+  int cr = drv.occupancy(&occ, lp.e->fn, kTPB, lp.pp.dyn_smem);
+  if (cr) return drv_fail(cr, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
+  if (occ < 1) { set_error("jit kernel does not fit an SM"); return SCX_EUNSUPPORTED; }
+  int dev = 0, sms = 0;
+  SCX_CUDA(cudaGetDevice(&dev));
+  SCX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  lp.grid = (int64_t)sms * occ;
+  if (lp.grid > lp.pp.tiles) lp.grid = lp.pp.tiles;
+  if (lp.grid < 1) lp.grid = 1;
+  if (P.sink.kind == SCX_SINK_COMPACT) {
+    const int64_t tile_rows = (int64_t)kTPB * lp.pp.V;
+    lp.tpc = (lp.pp.tiles + lp.grid - 1) / lp.grid;
+    lp.stage_rows = lp.grid * lp.tpc * tile_rows;
+    lp.stage_word = (lp.grid + 2 + 1) & ~int64_t(1);      // 16-byte aligned staging
+    int64_t bytes = 0;
+    for (int j = 0; j < P.sink.n_out; ++j)
+      bytes += (lp.stage_rows * dtype_size(P.sink.out[j].dtype) + 15) & ~int64_t(15);
+    lp.status_words = lp.stage_word + bytes / 8;
+  } else {
+    lp.status_words = lp.pp.tiles;
+  }
+  return SCX_OK;
+}
+
+}  // namespace jit
+}  // namespace scx
+
 extern "C" int64_t scx_pipeline_status_words(const scx_pipeline* d) {
   if (!d) return 0;
   if (!jit::enabled()) return interp_status_words(d);
-  jit::Prepared pp;
-  if (jit::prepare(*d, pp)) return -1;
-  return pp.tiles;
+  if (d->n_rows <= 0) return 1;
+  jit::LaunchPlan lp;
+  if (jit::plan_launch(*d, lp)) return -1;
+  return lp.status_words;
 }
 
 extern "C" int scx_pipeline_run(const scx_pipeline* d, void* stream) {
@@ -1132,42 +1188,37 @@ extern "C" int scx_pipeline_run(const scx_pipeline* d, void* stream) {
     set_error("pipeline: dense sink needs n_cells >= 1");
     return SCX_EINVAL;
   }
-  jit::Prepared pp;
-  int rc = jit::prepare(P, pp);
-  if (rc) return rc;
-  jit::Entry* e = nullptr;
-  rc = jit::get_function(pp.src, pp.name, e);
-  if (rc) return rc;
-  jit::Driver& drv = jit::driver();
-  if ((int)pp.dyn_smem > e->max_dyn_smem) {
-    int cr = drv.set_attr(e->fn, 8 /*CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES*/,
-                          (int)pp.dyn_smem);
-    if (cr) return jit::drv_fail(cr, "cuFuncSetAttribute");
-    e->max_dyn_smem = (int)pp.dyn_smem;
+  if (P.sink.kind == SCX_SINK_COMPACT && (!P.sink.status || !P.sink.count)) {
+    set_error("pipeline: compaction needs status and count buffers");
+    return SCX_EINVAL;
   }
-  int occ = 0;
-  int cr = drv.occupancy(&occ, e->fn, jit::kTPB, pp.dyn_smem);
-  if (cr) return jit::drv_fail(cr, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
-  if (occ < 1) { set_error("jit kernel does not fit an SM"); return SCX_EUNSUPPORTED; }
-  int dev = 0, sms = 0;
-  SCX_CUDA(cudaGetDevice(&dev));
-  SCX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // all CTAs co-resident (the compaction look-back waits on predecessors)
-  int64_t grid = (int64_t)sms * occ;
-  if (grid > pp.tiles) grid = pp.tiles;
-  if (grid < 1) grid = 1;
+  jit::LaunchPlan lp;
+  int rc = jit::plan_launch(P, lp);
+  if (rc) return rc;
   struct {
     int64_t n;
     uint64_t p[jit::kMaxP];
   } args;
   memset(&args, 0, sizeof(args));
   args.n = P.n_rows;
-  for (size_t i = 0; i < pp.ptrs.size(); ++i) args.p[i] = pp.ptrs[i];
+  for (size_t i = 0; i < lp.pp.ptrs.size(); ++i) args.p[i] = lp.pp.ptrs[i];
+  char* stage = nullptr;
+  if (P.sink.kind == SCX_SINK_COMPACT) {
+    stage = reinterpret_cast<char*>(P.sink.status) + 8 * lp.stage_word;
+    args.p[lp.pp.stage_p] = reinterpret_cast<uint64_t>(stage);
+    args.p[lp.pp.stage_rows_p] = (uint64_t)lp.stage_rows;
+  }
   void* params[] = {&args};
-  cr = drv.launch(e->fn, (unsigned)grid, 1, 1, jit::kTPB, 1, 1, (unsigned)pp.dyn_smem, stream,
-                  params, nullptr);
+  jit::Driver& drv = jit::driver();
+  int cr = drv.launch(lp.e->fn, (unsigned)lp.grid, 1, 1, jit::kTPB, 1, 1, (unsigned)lp.pp.dyn_smem,
+                      stream, params, nullptr);
   if (cr) return jit::drv_fail(cr, "cuLaunchKernel");
   SCX_CHECK_LAUNCH("scx_pipe (jit)");
+  if (P.sink.kind == SCX_SINK_COMPACT)
+    return compact_finish(reinterpret_cast<uint64_t*>(P.sink.status), lp.grid, stage,
+                          lp.stage_rows, P.sink.out, P.sink.n_out,
+                          lp.tpc * (int64_t)jit::kTPB * lp.pp.V,
+                          reinterpret_cast<uint64_t*>(P.sink.count), (cudaStream_t)stream);
   return SCX_OK;
 }
 

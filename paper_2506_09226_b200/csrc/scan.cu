@@ -169,6 +169,43 @@ __global__ void __launch_bounds__(kBlock) occ_write_kernel(
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) *count = part[gridDim.x];
 }
 
+// ---- finishing a staged stable compaction (jit COMPACT sink) ---------------
+__global__ void region_copy_kernel(const char* src, char* dst, int w, const uint64_t* prefix,
+                                   int64_t region_rows) {
+  const int64_t b = blockIdx.y;
+  const uint64_t start = prefix[b], cnt = prefix[b + 1] - start;
+  const char* s = src + (size_t)b * region_rows * w;
+  char* d = dst + (size_t)start * w;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    switch (w) {
+      case 1: d[i] = s[i]; break;
+      case 2: reinterpret_cast<int16_t*>(d)[i] = reinterpret_cast<const int16_t*>(s)[i]; break;
+      case 4: reinterpret_cast<int32_t*>(d)[i] = reinterpret_cast<const int32_t*>(s)[i]; break;
+      default: reinterpret_cast<int64_t*>(d)[i] = reinterpret_cast<const int64_t*>(s)[i]; break;
+    }
+  }
+}
+
+// status[0..grid) = per-CTA selected counts -> exclusive prefix (+ total at
+// status[grid]); each CTA's staged rows move to their final position
+int compact_finish(uint64_t* status, int64_t grid, char* stage, int64_t stage_rows,
+                   const scx_column* outs, int n_out, int64_t region_rows, uint64_t* count,
+                   cudaStream_t st) {
+  small_scan_kernel<<<1, 1024, 0, st>>>(status, grid);
+  SCX_CHECK_LAUNCH("small_scan_kernel");
+  SCX_CUDA(cudaMemcpyAsync(count, status + grid, 8, cudaMemcpyDeviceToDevice, st));
+  char* src = stage;
+  for (int j = 0; j < n_out; ++j) {
+    const int w = dtype_size(outs[j].dtype);
+    region_copy_kernel<<<dim3(16, (unsigned)grid), 256, 0, st>>>(
+        src, reinterpret_cast<char*>(outs[j].ptr), w, status, region_rows);
+    SCX_CHECK_LAUNCH("region_copy_kernel");
+    src += (stage_rows * w + 15) & ~int64_t(15);
+  }
+  return SCX_OK;
+}
+
 }  // namespace scx
 
 using namespace scx;

@@ -802,8 +802,12 @@ def _materialize(v: TableView) -> ColumnTable:
         S.out_slot[i] = b.slot[name]
         S.out[i] = L.Column_(buf.data_ptr(), c.scx_dtype, 0)
     S.n_out = len(cols)
-    words = max(1, L.load().scx_pipeline_status_words(C.byref(P)))
-    status = _new_i64(words, 0)
+    words = L.load().scx_pipeline_status_words(C.byref(P))
+    if words < 0:
+        L.check(-1 if words == -1 else int(words), "scx_pipeline_status_words")
+    # per-CTA counts + the staging area of the stable compaction: every word
+    # the kernel reads is written first, so no clearing is needed
+    status = alloc(max(int(words), 2), np.int64)
     count = _new_i64(1, 0)
     S.status = status.data_ptr()
     S.count = count.data_ptr()

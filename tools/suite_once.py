@@ -21,7 +21,9 @@ for _ in range(a.warm):
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_push("timed_suite")
 for q in P.SUPPORTED_QUERIES:
+    torch.cuda.nvtx.range_push(q)
     P.reference_run(q, tables)
+    torch.cuda.nvtx.range_pop()
 torch.cuda.synchronize()
 torch.cuda.nvtx.range_pop()
 print("suite done")

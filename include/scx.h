@@ -293,6 +293,14 @@ int scx_direct_agg_compact(const uint64_t* gkeys_dev, const int64_t* acc_dev, in
                            uint64_t* out_keys_dev, int64_t* out_acc_dev, uint64_t* count_dev,
                            void* temp_dev, void* stream);
 
+/* Same, for a direct table written without a key array (the JIT hash sink
+ * with sink.gkeys == 0 in direct mode): slot e is a group iff its count word
+ * acc[e*m + occ_word] > 0, and its packed key is e.  Replaces the same
+ * np.unique/bincount step as scx_direct_agg_compact (relops.py:117-129). */
+int scx_direct_agg_compact_counted(const int64_t* acc_dev, int64_t cap, int m, int occ_word,
+                                   uint64_t* out_keys_dev, int64_t* out_acc_dev,
+                                   uint64_t* count_dev, void* temp_dev, void* stream);
+
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not
  * fit (group_aggregate output, relops.py:138-158). */

@@ -261,6 +261,8 @@ int get_function(const std::string& src, const std::string& name, Entry*& out) {
 // ---------------------------------------------------------------------------
 // code generation
 // ---------------------------------------------------------------------------
+constexpr size_t kPipeSmem = 100 * 1024;   // per-CTA dynamic smem budget (2 CTAs/SM)
+
 static const char* kPrelude = R"PRE(
 typedef signed char i8; typedef unsigned char u8; typedef short i16; typedef unsigned short u16;
 typedef int i32; typedef unsigned int u32; typedef long long i64; typedef unsigned long long u64;
@@ -287,6 +289,24 @@ static __device__ __forceinline__ u32 ldv1(const void* p) {
   asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
 }
+// cp.async staging (per-thread private chunks: no CTA barrier needed)
+static __device__ __forceinline__ u32 smem_u32(const void* p) {
+  u32 r;
+  asm("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(r) : "l"(p));
+  return r;
+}
+static __device__ __forceinline__ void cpa16(u32 dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(dst), "l"(src) : "memory");
+}
+static __device__ __forceinline__ void cpa8(u32 dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" :: "r"(dst), "l"(src) : "memory");
+}
+static __device__ __forceinline__ void cpa4(u32 dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
+}
+static __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+static __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+static __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 static __device__ __forceinline__ u64 ld_acquire(const u64* p) {
   u64 v; asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
@@ -371,6 +391,9 @@ struct Gen {
   int n_globals = 0;
   size_t dyn_smem = 0;
   int stage_p = -1, stage_rows_p = -1;   // COMPACT: staging base / rows, bound at launch
+  bool pipe = false;            // base columns double-buffered through shared memory
+  size_t sink_smem = 0;         // dynamic smem used by the sink (before the load stages)
+  std::vector<int> col_p;       // Args.p index of each base column
   std::string err;
 
   explicit Gen(const scx_pipeline& p) : P(p) {}
@@ -583,15 +606,58 @@ struct Gen {
       o << "    u32 w" << s << "[" << V * dtype_size(P.base[s].dtype) / 4 << "];\n";
   }
 
+  // byte offset of base column s inside one load stage ([col][16B piece][thread])
+  int64_t stage_off(int s) {
+    int64_t off = 0;
+    for (int c = 0; c < s; ++c) off += (int64_t)kTPB * V * dtype_size(P.base[c].dtype);
+    return off;
+  }
+  int64_t stage_bytes() { return stage_off(P.n_base); }
+
+  // cp.async of this thread's chunk of tile `t` into stage `b` (full chunks
+  // only; a ragged last chunk is loaded synchronously)
+  void emit_issue(const char* t, const char* b) {
+    o << "    { const i64 r0 = (" << t << " * " << kTPB << " + tid) * (i64)V;\n";
+    o << "      if (r0 + V <= n) {\n";
+    o << "        const u32 sb = sbase + (u32)(" << b << ") * " << stage_bytes() << "u;\n";
+    for (int s = 0; s < P.n_base; ++s) {
+      const int w = dtype_size(P.base[s].dtype);
+      const int nb = V * w;
+      o << "        { const char* p = (const char*)a.p[" << col_p[s] << "] + r0 * " << w << "ll; const u32 d = sb + " << stage_off(s) << "u;\n";
+      if (nb >= 16) {
+        for (int j = 0; j < nb / 16; ++j)
+          o << "          cpa16(d + (u32)(" << j * kTPB << " + tid) * 16u, p + " << 16 * j << ");\n";
+      } else if (nb == 8) {
+        o << "          cpa8(d + (u32)tid * 8u, p);\n";
+      } else {
+        o << "          cpa4(d + (u32)tid * 4u, p);\n";
+      }
+      o << "        }\n";
+    }
+    o << "      }\n    }\n";
+  }
+
   void emit_loads() {
     for (int s = 0; s < P.n_base; ++s) {
       const int w = dtype_size(P.base[s].dtype);
       const int nb = V * w;                  // bytes per chunk
       const int nwords = nb / 4;
-      const int pi = param(P.base[s].ptr);
+      const int pi = col_p[s];
       o << "    { const char* p = (const char*)a.p[" << pi << "] + row0 * " << w << "ll;\n";
       o << "      if (full) {\n";
-      if (nb >= 16) {
+      if (pipe) {
+        o << "        const unsigned char* q = stg + (u32)buf * " << stage_bytes() << "u + " << stage_off(s) << "u;\n";
+        if (nb >= 16) {
+          for (int j = 0; j < nb / 16; ++j)
+            o << "        { const uint4 t = *(const uint4*)(q + (" << j * kTPB << " + tid) * 16); w" << s << "[" << 4 * j
+              << "] = t.x; w" << s << "[" << 4 * j + 1 << "] = t.y; w" << s << "[" << 4 * j + 2
+              << "] = t.z; w" << s << "[" << 4 * j + 3 << "] = t.w; }\n";
+        } else if (nb == 8) {
+          o << "        { const uint2 t = *(const uint2*)(q + tid * 8); w" << s << "[0] = t.x; w" << s << "[1] = t.y; }\n";
+        } else {
+          o << "        w" << s << "[0] = *(const u32*)(q + tid * 4);\n";
+        }
+      } else if (nb >= 16) {
         for (int j = 0; j < nb / 16; ++j)
           o << "        { uint4 t = ldv4(p + " << 16 * j << "); w" << s << "[" << 4 * j
             << "] = t.x; w" << s << "[" << 4 * j + 1 << "] = t.y; w" << s << "[" << 4 * j + 2
@@ -737,6 +803,31 @@ struct Gen {
       probe_regs += P.n_probes;
       while (V > 4 && V * (row_bytes + payload_bytes) / 4 + V * probe_regs + acc_regs > 64) V /= 2;
     }
+    // load pipeline: each thread copies (cp.async) its chunk of the NEXT tile's
+    // base columns into shared memory while it processes this one, so a
+    // tile's HBM latency overlaps the previous tile's probes and sink.  V
+    // shrinks (>= 4) until two stages plus the sink's shared table fit two
+    // CTAs per SM.  Opt-in with SCX_PIPE=1 (A/B).
+    {
+      size_t sink_b = 0;
+      if (S.kind == SCX_SINK_AGG_DENSE && S.n_cells > 1) {
+        const int Mx = S.n_measures;
+        if (dense_priv) sink_b = (size_t)S.n_cells * Mx * kTPB * 8;
+        else if (S.n_cells > 8) sink_b = (size_t)S.n_cells * Mx * 8;
+      }
+      sink_b = (sink_b + 15) & ~(size_t)15;
+      const char* env = getenv("SCX_PIPE");
+      // measured on B200 (SF100 suite): per-thread cp.async staging is slower
+      // than direct 128-bit ld.global.nc (Q6 1.04 -> 1.44 ms), so it is opt-in
+      pipe = env && env[0] == '1' && P.n_base > 0 && row_bytes > 0;
+      if (pipe) {
+        int v = V;
+        while (v > 4 && sink_b + 2 * (size_t)kTPB * v * row_bytes > kPipeSmem) v /= 2;
+        if (sink_b + 2 * (size_t)kTPB * v * row_bytes > kPipeSmem) pipe = false;
+        else V = v;
+      }
+      sink_smem = sink_b;
+    }
     const int64_t tile_rows = (int64_t)kTPB * V;
     tiles_out = (int)((P.n_rows + tile_rows - 1) / tile_rows);
 
@@ -754,6 +845,8 @@ struct Gen {
     o << "  const i64 ntiles = (n + " << tile_rows << "ll - 1) / " << tile_rows << "ll;\n";
     o << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
     o << "  (void)lane; (void)warp;\n";
+    o << "  extern __shared__ __align__(16) unsigned char dsm[];\n";
+    for (int c = 0; c < P.n_base; ++c) col_p.push_back(param(P.base[c].ptr));
 
     // sink state
     int acc_p = -1, gkeys_p = -1, gcap_p = -1, flags_p = -1, status_p = -1, count_p = -1;
@@ -762,7 +855,7 @@ struct Gen {
       acc_p = param(S.acc);
       if (dense_priv) {
         dyn_smem = (size_t)NC * M * kTPB * 8;
-        o << "  extern __shared__ __align__(16) i64 pacc[];\n";
+        o << "  i64* pacc = (i64*)dsm;\n";
         for (int c = 0; c < NC; ++c)
           for (int m = 0; m < M; ++m)
             o << "  pacc[" << (c * M + m) * kTPB << " + tid] = " << ident(m) << ";\n";
@@ -776,7 +869,7 @@ struct Gen {
         const int64_t words = (int64_t)S.n_cells * M;
         if (words * 8 > 160 * 1024) { err = "dense sink too large for shared memory"; return SCX_EUNSUPPORTED; }
         dyn_smem = (size_t)words * 8;
-        o << "  extern __shared__ __align__(16) i64 tab[];\n";
+        o << "  i64* tab = (i64*)dsm;\n";
         o << "  for (int i = tid; i < " << words << "; i += " << kTPB << ") {\n";
         o << "    const int m = i % " << M << ";\n";
         o << "    tab[i] = ";
@@ -790,7 +883,7 @@ struct Gen {
       gkeys_p = param(S.gkeys);
       gcap_p = param(S.gcap);
       flags_p = param(S.flags);
-      o << "  u64* gkeys = (u64*)a.p[" << gkeys_p << "];\n";
+      o << "  u64* gkeys = (u64*)a.p[" << gkeys_p << "]; (void)gkeys;\n";
       o << "  i64* gacc = (i64*)a.p[" << acc_p << "];\n";
       o << "  const u64 gmask = a.p[" << gcap_p << "] - 1;\n";
     } else if (S.kind == SCX_SINK_COMPACT) {
@@ -831,8 +924,26 @@ struct Gen {
       return SCX_EINVAL;
     }
 
-    if (S.kind == SCX_SINK_COMPACT) o << "  for (i64 tile = tbeg; tile < tend; ++tile) {\n";
-    else o << "  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+    if (dyn_smem < sink_smem) dyn_smem = sink_smem;
+    if (pipe) {
+      dyn_smem = sink_smem + 2 * (size_t)stage_bytes();
+      const bool cmp = S.kind == SCX_SINK_COMPACT;
+      o << "  const i64 t_first = " << (cmp ? "tbeg" : "(i64)blockIdx.x") << ", t_step = "
+        << (cmp ? "1" : "(i64)gridDim.x") << ", t_end = " << (cmp ? "tend" : "ntiles") << ";\n";
+      o << "  const unsigned char* stg = dsm + " << sink_smem << ";\n";
+      o << "  const u32 sbase = smem_u32(stg);\n";
+      o << "  if (t_first < t_end) {\n  const i64 nt = t_first;\n";
+      emit_issue("nt", "0");
+      o << "  }\n  cpa_commit();\n  int buf = 0;\n";
+      o << "  for (i64 tile = t_first; tile < t_end; tile += t_step, buf ^= 1) {\n";
+      o << "    { const i64 nt = tile + t_step;\n    if (nt < t_end) {\n";
+      emit_issue("nt", "buf ^ 1");
+      o << "    } }\n    cpa_commit();\n    cpa_wait1();\n";
+    } else if (S.kind == SCX_SINK_COMPACT) {
+      o << "  for (i64 tile = tbeg; tile < tend; ++tile) {\n";
+    } else {
+      o << "  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+    }
     o << "    const i64 row0 = (tile * " << kTPB << " + tid) * (i64)V;\n";
     o << "    const bool full = row0 + V <= n;\n";
     o << "    const int rem = row0 >= n ? 0 : (int)(n - row0 < V ? n - row0 : V);\n";
@@ -913,7 +1024,10 @@ struct Gen {
       if (S.n_cells == 1) {
         // direct-addressed groups: the packed key is the slot (gcap = domain)
         o << "        u64 slot = SCX_EMPTY;\n";
-        o << "        if (key <= gmask) { slot = key; if (gkeys[slot] != key) gkeys[slot] = key; }\n";
+        // (no key array: occupancy is the group's count word, compacted by
+        // scx_direct_agg_compact_counted)
+        if (S.gkeys) o << "        if (key <= gmask) { slot = key; if (gkeys[slot] != key) gkeys[slot] = key; }\n";
+        else o << "        if (key <= gmask) slot = key;\n";
       } else {
         // open addressing, linear probing; a probe run longer than 4096 means
         // the table is (nearly) full: flag it so the host retries larger
@@ -1001,6 +1115,7 @@ struct Gen {
       o << "    }\n";
     }
     o << "  }\n";  // tile loop
+    if (pipe) o << "  cpa_wait0();\n";
 
     // ---- epilogues ----
     if (S.kind == SCX_SINK_AGG_DENSE && (dense_reg || dense_priv)) {
@@ -1029,8 +1144,10 @@ struct Gen {
       o << "    } else {\n";
       o << "      u64 lo = 0; i64 hi = 0;\n";
       o << "      for (int w = 0; w < " << kTPB / 32 << "; ++w) { const i64 v = red[w][tid]; const u64 s2 = lo + (u64)v; hi += (v < 0 ? -1 : 0) + (s2 < lo ? 1 : 0); lo = s2; }\n";
-      o << "      if (lo) atomic_add_i128(gacc, (i64)lo);\n";
-      o << "      if (hi) atomicAdd((unsigned long long*)(gacc + 1), (unsigned long long)hi);\n";
+      // (lo, hi) is an exact 128-bit partial: add lo unsigned, carry into hi
+      o << "      const u64 old = lo ? (u64)atomicAdd((unsigned long long*)gacc, (unsigned long long)lo) : 0ull;\n";
+      o << "      const i64 h = hi + ((lo && old + lo < old) ? 1 : 0);\n";
+      o << "      if (h) atomicAdd((unsigned long long*)(gacc + 1), (unsigned long long)h);\n";
       o << "    }\n  }\n";
     } else if (S.kind == SCX_SINK_AGG_DENSE) {
       o << "  __syncthreads();\n";

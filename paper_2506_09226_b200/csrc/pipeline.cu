@@ -723,8 +723,11 @@ _Pragma("unroll")
           lo = (int64_t)s2;
         }
         int64_t* acc = reinterpret_cast<int64_t*>(S.acc) + 2 * ((int64_t)c * S.n_measures + m);
-        if (lo != 0) atomic_add_i128(acc, lo);
-        if (hi != 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc + 1), (unsigned long long)hi);
+        // (lo, hi) is an exact 128-bit partial: add lo unsigned, carry into hi
+        const uint64_t old = lo != 0 ? (uint64_t)atomicAdd(reinterpret_cast<unsigned long long*>(acc),
+                                                           (unsigned long long)lo) : 0ull;
+        const int64_t h = hi + ((lo != 0 && old + (uint64_t)lo < old) ? 1 : 0);
+        if (h != 0) atomicAdd(reinterpret_cast<unsigned long long*>(acc + 1), (unsigned long long)h);
       } else {
         int64_t v = agg_identity(op);
         for (int w = 0; w < kWarps; ++w) v = agg_combine(op, v, red[(w * NC + c) * NM + m]);

@@ -120,13 +120,26 @@ int scan_u32_excl(const uint32_t* in, uint64_t* out, int64_t m, uint64_t* tmp, c
 // ballots; the round's accumulator rows (256 x W words, row-major) are staged
 // through shared memory so both the read and the measure-major write are
 // coalesced.
-__global__ void occ_count_kernel(const uint64_t* gkeys, int64_t cap, uint64_t* part) {
+// occupancy of slot e: gkeys[e] != EMPTY, or (gkeys == nullptr) the group's
+// count word acc[e*m + occ_word] > 0 -- direct tables keyed by the slot need
+// no key array at all (the packed key IS the slot)
+struct Occ {
+  const uint64_t* gkeys;
+  const int64_t* acc;
+  int m, occ_word;
+  __device__ __forceinline__ bool operator()(int64_t e) const {
+    return gkeys ? gkeys[e] != SCX_EMPTY_KEY : acc[e * m + occ_word] > 0;
+  }
+  __device__ __forceinline__ uint64_t key(int64_t e) const { return gkeys ? gkeys[e] : (uint64_t)e; }
+};
+
+__global__ void occ_count_kernel(Occ O, int64_t cap, uint64_t* part) {
   const int64_t base = (int64_t)blockIdx.x * kScanTile;
   uint32_t s = 0;
 #pragma unroll
   for (int it = 0; it < kScanItems; ++it) {
     const int64_t e = base + it * kBlock + threadIdx.x;
-    s += (e < cap && gkeys[e] != SCX_EMPTY_KEY);
+    s += (e < cap && O(e));
   }
   uint32_t excl;
   const uint32_t tot = block_excl_scan(s, excl);
@@ -134,7 +147,7 @@ __global__ void occ_count_kernel(const uint64_t* gkeys, int64_t cap, uint64_t* p
 }
 
 __global__ void __launch_bounds__(kBlock) occ_write_kernel(
-    const uint64_t* gkeys, const int64_t* acc, int64_t cap, int m, const uint64_t* part,
+    Occ O, const int64_t* acc, int64_t cap, int m, const uint64_t* part,
     uint64_t* out_keys, int64_t* out_acc, uint64_t* count) {
   __shared__ int64_t tile[kBlock * 16];
   __shared__ uint32_t wcnt[kWarps];
@@ -145,12 +158,12 @@ __global__ void __launch_bounds__(kBlock) occ_write_kernel(
     const int64_t r0 = base + (int64_t)it * kBlock;
     if (r0 >= cap) break;
     const int64_t e = r0 + tid;
-    const uint64_t k = e < cap ? gkeys[e] : SCX_EMPTY_KEY;
-    const bool occ = k != SCX_EMPTY_KEY;
-    const uint32_t b = __ballot_sync(0xffffffffu, occ);
-    if (lane == 0) wcnt[warp] = __popc(b);
     const int64_t rows = min((int64_t)kBlock, cap - r0);
     for (int64_t x = tid; x < rows * m; x += kBlock) tile[x] = acc[r0 * m + x];
+    __syncthreads();
+    const bool occ = e < cap && (O.gkeys ? O.gkeys[e] != SCX_EMPTY_KEY : tile[tid * m + O.occ_word] > 0);
+    const uint32_t b = __ballot_sync(0xffffffffu, occ);
+    if (lane == 0) wcnt[warp] = __popc(b);
     __syncthreads();
     uint32_t wofs = 0, tot = 0;
 #pragma unroll
@@ -160,7 +173,7 @@ __global__ void __launch_bounds__(kBlock) occ_write_kernel(
     }
     if (occ) {
       const uint64_t pos = pos0 + wofs + __popc(b & ((1u << lane) - 1u));
-      out_keys[pos] = k;
+      out_keys[pos] = O.key(e);
       for (int j = 0; j < m; ++j) out_acc[(int64_t)j * cap + (int64_t)pos] = tile[tid * m + j];
     }
     pos0 += tot;
@@ -212,14 +225,9 @@ using namespace scx;
 
 extern "C" int64_t scx_direct_agg_workspace(int64_t cap) { return 8 * scan_tmp_words(cap); }
 
-extern "C" int scx_direct_agg_compact(const uint64_t* gkeys, const int64_t* acc, int64_t cap,
-                                      int m, uint64_t* out_keys, int64_t* out_acc,
-                                      uint64_t* count, void* temp, void* stream) {
-  if (!gkeys || !out_keys || !count || !temp || m > 16 || (m > 0 && (!acc || !out_acc))) {
-    set_error("direct_agg_compact: bad arguments");
-    return SCX_EINVAL;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
+static int direct_compact(const Occ& O, const int64_t* acc, int64_t cap, int m,
+                          uint64_t* out_keys, int64_t* out_acc, uint64_t* count, void* temp,
+                          cudaStream_t st) {
   if (cap == 0) {
     SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
     return SCX_OK;
@@ -227,11 +235,35 @@ extern "C" int scx_direct_agg_compact(const uint64_t* gkeys, const int64_t* acc,
   const int64_t nb = (cap + kScanTile - 1) / kScanTile;
   if (nb > 1024 * 64) { set_error("direct_agg_compact: table too large"); return SCX_EUNSUPPORTED; }
   uint64_t* part = static_cast<uint64_t*>(temp);
-  occ_count_kernel<<<(int)nb, kBlock, 0, st>>>(gkeys, cap, part);
+  occ_count_kernel<<<(int)nb, kBlock, 0, st>>>(O, cap, part);
   SCX_CHECK_LAUNCH("occ_count_kernel");
   small_scan_kernel<<<1, 1024, 0, st>>>(part, nb);
   SCX_CHECK_LAUNCH("small_scan_kernel");
-  occ_write_kernel<<<(int)nb, kBlock, 0, st>>>(gkeys, acc, cap, m, part, out_keys, out_acc, count);
+  occ_write_kernel<<<(int)nb, kBlock, 0, st>>>(O, acc, cap, m, part, out_keys, out_acc, count);
   SCX_CHECK_LAUNCH("occ_write_kernel");
   return SCX_OK;
+}
+
+extern "C" int scx_direct_agg_compact(const uint64_t* gkeys, const int64_t* acc, int64_t cap,
+                                      int m, uint64_t* out_keys, int64_t* out_acc,
+                                      uint64_t* count, void* temp, void* stream) {
+  if (!gkeys || !out_keys || !count || !temp || m > 16 || (m > 0 && (!acc || !out_acc))) {
+    set_error("direct_agg_compact: bad arguments");
+    return SCX_EINVAL;
+  }
+  Occ O{gkeys, acc, m, 0};
+  return direct_compact(O, acc, cap, m, out_keys, out_acc, count, temp, (cudaStream_t)stream);
+}
+
+extern "C" int scx_direct_agg_compact_counted(const int64_t* acc, int64_t cap, int m,
+                                              int occ_word, uint64_t* out_keys,
+                                              int64_t* out_acc, uint64_t* count, void* temp,
+                                              void* stream) {
+  if (!acc || !out_keys || !out_acc || !count || !temp || m < 1 || m > 16 || occ_word < 0 ||
+      occ_word >= m) {
+    set_error("direct_agg_compact_counted: bad arguments");
+    return SCX_EINVAL;
+  }
+  Occ O{nullptr, acc, m, occ_word};
+  return direct_compact(O, acc, cap, m, out_keys, out_acc, count, temp, (cudaStream_t)stream);
 }

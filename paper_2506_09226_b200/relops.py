@@ -36,6 +36,7 @@ from .table import Column, ColumnTable, HostColumn, SchemaError, alloc
 
 AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
+_DENSE_SMEM_BYTES = 96 * 1024     # per-CTA shared-memory group table (2 CTAs/SM)
 _OPCODE = {"sum": L.AGG_SUM, "count": L.AGG_COUNT, "min": L.AGG_MIN, "max": L.AGG_MAX}
 
 
@@ -961,17 +962,27 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
         cards.append(len(c.dictionary) if c.kind == "dict" else max(1, c.hi - c.lo + 1))
     cells = int(np.prod(cards)) if keys else 1
     dense = (not keys and len(measures) <= 8) or (keys and cells <= 8 and len(measures) <= 6)
+    # small key domains (Q5's 25 nations, Q7's nation pairs x years, Q9's
+    # nation x year) aggregate in a per-CTA shared-memory table: smem atomics
+    # then one global atomic per cell per CTA, instead of every row hitting
+    # the same few global accumulators
+    n = v.base.row_count
+    smem_table = (keys and not dense and cells * len(measures) * 8 <= _DENSE_SMEM_BYTES)
+    if smem_table:
+        per_cta = n // 148 + 4096
+        smem_table = all(_measure_bound(im, v.meta) * per_cta < (1 << 62)
+                         for op, im in measures if im is not None and op == "sum")
+    dense = dense or smem_table
     # overflow guard: per-thread int64 partials (dense; exact 128-bit across
     # threads); hash groups switch a sum to a 128-bit {lo, hi} accumulator when
     # n rows of its largest value could leave int64
-    n = v.base.row_count
     for i, (op, im) in enumerate(measures):
         if im is not None and op == "sum":
             bound = _measure_bound(im, v.meta)
-            if dense:
-                if bound * (n // (148 * 256) + 16) >= (1 << 62):
+            if dense and not smem_table:
+                if n > 0 and bound * (n // (148 * 256) + 16) >= (1 << 62):
                     raise SchemaError("aggregate may overflow 64-bit partial sums")
-            elif bound * max(n, 1) >= (1 << 62):
+            elif not dense and bound * max(n, 1) >= (1 << 62):
                 b.P.sink.m[i]._pad = 1
     b.ksrc = ksrc
     if dense:
@@ -1086,14 +1097,14 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
     result table, queries.py:51-69): at most 8 cells x 8 measures of exact
     integers, turned into result columns and uploaded.
     """
-    cells = acc.shape[0]
     minmax = [op in ("min", "max") for op, _ in measures]
-    vals = [[int(acc[c, j, 0]) if minmax[j] else _i128(acc[c, j]) for j in range(acc.shape[1])]
-            for c in range(cells)]
     if keys:
-        live = [c for c in range(cells) if vals[c][count_m] > 0]
+        # counts are non-negative and < 2^63: the low word alone decides liveness
+        live = [int(c) for c in np.flatnonzero(acc[:, count_m, 0] > 0)]
     else:
         live = [0]
+    vals = {c: [int(acc[c, j, 0]) if minmax[j] else _i128(acc[c, j]) for j in range(acc.shape[1])]
+            for c in live}
     out: dict[str, Column] = {}
     # decode cell -> per-key rank -> value
     for i, (k, c) in enumerate(zip(keys, kcols)):
@@ -1175,9 +1186,15 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
     # capacity: bounded by rows, the key domain, and unique inner-join builds
     n = v.base.row_count
     bound = max(n, 1)
+    # packed-key domain: the leading key contributes its value range, the
+    # others their full bit width (packed = k0 << shift0 | ...)
     dom = 1
-    for c, bb in zip(kcols, bits):
-        dom *= (1 << bb)
+    for i, (c, bb) in enumerate(zip(kcols, bits)):
+        if i == 0:
+            rng = len(c.dictionary) if c.kind == "dict" else (c.hi - c.lo + 1 if c.hi >= c.lo else 1)
+            dom *= max(1, min(rng, 1 << bb))
+        else:
+            dom *= (1 << bb)
     bound = min(bound, dom)
     for st in v.probes:
         # a unique-build inner join bounds the groups only when every group
@@ -1207,9 +1224,12 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
     flags = stat[:2].view(torch.uint32)
     cnt = stat[2:3].view(torch.uint64)
     while True:
-        gkeys = alloc(cap, np.uint64)
+        # direct tables need no key array: the slot is the packed key and the
+        # group's count word marks it occupied
+        gkeys = None if direct else alloc(cap, np.uint64)
         accb = alloc(cap * W, np.int64)
-        fill_i64(gkeys.view(torch.int64), -1)
+        if gkeys is not None:
+            fill_i64(gkeys.view(torch.int64), -1)
         pattern = []
         for j, (op, _) in enumerate(measures):
             pattern.append(INT64_MAX if op == "min" else (INT64_MIN if op == "max" else 0))
@@ -1218,15 +1238,16 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
         pat = (C.c_int64 * W)(*pattern)
         L.call("scx_fill_rows", _ptr(accb), cap, W, pat, _stream())
         fill_i64(stat, 0)
-        S.gkeys, S.acc, S.gcap, S.flags = gkeys.data_ptr(), accb.data_ptr(), cap, flags.data_ptr()
+        S.gkeys = 0 if gkeys is None else gkeys.data_ptr()
+        S.acc, S.gcap, S.flags = accb.data_ptr(), cap, flags.data_ptr()
         b.run()
         out_keys = alloc(cap, np.uint64)
         out_acc = alloc(cap * W, np.int64)
         if direct:
             # slot order == packed-key order: ordered compaction, no sort
             ws = alloc(max(2, L.load().scx_direct_agg_workspace(cap) // 8), np.int64)
-            L.call("scx_direct_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
-                   _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
+            L.call("scx_direct_agg_compact_counted", _ptr(accb), cap, W, int(woff[count_m]),
+                   _ptr(out_keys), _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
         else:
             L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
                    _ptr(out_acc), _ptr(cnt), _stream())

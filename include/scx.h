@@ -301,6 +301,18 @@ int scx_direct_agg_compact_counted(const int64_t* acc_dev, int64_t cap, int m, i
                                    uint64_t* out_keys_dev, int64_t* out_acc_dev,
                                    uint64_t* count_dev, void* temp_dev, void* stream);
 
+/* Dense ranks of a non-decreasing key column (a clustered key: lineitem and
+ * its materialised subsets by l_orderkey): rank_dev[i] = number of distinct
+ * keys in key[0..i] - 1, keys_by_rank_dev[r] = (key of rank r) - lo,
+ * *count_dev = number of distinct keys.  A group-by on such a key then uses a
+ * direct table of exactly that many slots instead of hashing (replaces the
+ * np.unique codes of relops.py:117-119 for sorted keys).  temp_dev sized by
+ * scx_sorted_rank_workspace(n). */
+int64_t scx_sorted_rank_workspace(int64_t n);
+int scx_sorted_rank(const scx_column* key, int64_t n, int64_t lo, uint32_t* rank_dev,
+                    uint64_t* keys_by_rank_dev, uint64_t* count_dev, void* temp_dev,
+                    void* stream);
+
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not
  * fit (group_aggregate output, relops.py:138-158). */

@@ -219,9 +219,80 @@ int compact_finish(uint64_t* status, int64_t grid, char* stage, int64_t stage_ro
   return SCX_OK;
 }
 
+// ---- dense ranks of a sorted (non-decreasing) key column --------------------
+// head(i) = i == 0 || key[i] != key[i-1]; rank(i) = #heads in [0, i] - 1.
+// A group-by on a clustered key (lineitem / a materialised lineitem subset by
+// l_orderkey) then addresses a table of exactly #distinct-keys slots,
+// sequentially, instead of hashing into a table sized by the row count.
+__device__ __forceinline__ uint32_t is_head(const scx_column& c, int64_t i) {
+  const void* p = reinterpret_cast<const void*>(c.ptr);
+  return i == 0 || load_i64(p, c.dtype, i) != load_i64(p, c.dtype, i - 1);
+}
+
+__global__ void rank_count_kernel(scx_column c, int64_t n, uint64_t* part) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) s += (base + i < n) ? is_head(c, base + i) : 0u;
+  uint32_t excl;
+  const uint32_t tot = block_excl_scan(s, excl);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void rank_write_kernel(scx_column c, int64_t n, int64_t lo, const uint64_t* part,
+                                  uint32_t* rank, uint64_t* keys_by_rank, uint64_t* count) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  const void* p = reinterpret_cast<const void*>(c.ptr);
+  uint32_t h[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    h[i] = (base + i < n) ? is_head(c, base + i) : 0u;
+    s += h[i];
+  }
+  uint32_t excl;
+  block_excl_scan(s, excl);
+  uint64_t run = part[blockIdx.x] + excl;   // heads before this thread's rows
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i >= n) break;
+    run += h[i];
+    rank[base + i] = (uint32_t)(run - 1);
+    if (h[i]) keys_by_rank[run - 1] = (uint64_t)(load_i64(p, c.dtype, base + i) - lo);
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kBlock - 1) *count = part[gridDim.x];
+}
+
 }  // namespace scx
 
 using namespace scx;
+
+extern "C" int64_t scx_sorted_rank_workspace(int64_t n) { return 8 * scan_tmp_words(n); }
+
+extern "C" int scx_sorted_rank(const scx_column* key, int64_t n, int64_t lo, uint32_t* rank,
+                               uint64_t* keys_by_rank, uint64_t* count, void* temp,
+                               void* stream) {
+  if (!key || !rank || !keys_by_rank || !count || (n > 0 && !temp) || n < 0 ||
+      n > (int64_t)0xFFFFFFFFll) {
+    set_error("sorted_rank: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {
+    SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
+    return SCX_OK;
+  }
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb > 1024 * 64) { set_error("sorted_rank: column too long"); return SCX_EUNSUPPORTED; }
+  uint64_t* part = static_cast<uint64_t*>(temp);
+  rank_count_kernel<<<(int)nb, kBlock, 0, st>>>(*key, n, part);
+  SCX_CHECK_LAUNCH("rank_count_kernel");
+  small_scan_kernel<<<1, 1024, 0, st>>>(part, nb);
+  SCX_CHECK_LAUNCH("small_scan_kernel");
+  rank_write_kernel<<<(int)nb, kBlock, 0, st>>>(*key, n, lo, part, rank, keys_by_rank, count);
+  SCX_CHECK_LAUNCH("rank_write_kernel");
+  return SCX_OK;
+}
 
 extern "C" int64_t scx_direct_agg_workspace(int64_t cap) { return 8 * scan_tmp_words(cap); }
 

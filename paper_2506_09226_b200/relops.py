@@ -24,6 +24,7 @@ once (late materialisation), and no numpy touches a row.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from fractions import Fraction
 
@@ -36,7 +37,8 @@ from .table import Column, ColumnTable, HostColumn, SchemaError, alloc
 
 AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
-_DENSE_SMEM_BYTES = 96 * 1024     # per-CTA shared-memory group table (2 CTAs/SM)
+_GROUP_MAT = os.environ.get("SCX_GROUP_MAT", "1") != "0"
+_DENSE_SMEM_BYTES = 48 * 1024     # per-CTA shared-memory group table (keeps 4 CTAs/SM)
 _OPCODE = {"sum": L.AGG_SUM, "count": L.AGG_COUNT, "min": L.AGG_MIN, "max": L.AGG_MAX}
 
 
@@ -320,7 +322,7 @@ class TableView:
             if col.src not in v.meta:
                 raise SchemaError(f"unknown column {col.src!r} for derived key {name!r}")
             v.derived[name] = col
-            v.meta[name] = derived_meta(v.meta[col.src], col)
+            v.meta[name] = derived_meta(_narrowed(v, col.src), col)
             v.origin[name] = ("derived", col.src)
         elif isinstance(col, (Poly, ColRef)):
             v.computed[name] = as_poly(col)
@@ -356,6 +358,43 @@ class TableView:
 def _civil_year(days: int) -> int:
     import datetime
     return (datetime.date(1970, 1, 1) + datetime.timedelta(days=int(days))).year
+
+
+def _pred_range(pred: Pred, col: str):
+    """[lo, hi] that `pred` (DNF) implies for an integer column, or None."""
+    if pred.is_true:
+        return None
+    lo_all, hi_all = None, None
+    for clause in pred.clauses:
+        lo, hi = INT64_MIN, INT64_MAX
+        for a in clause:
+            if a.op == "range" and a.col == col and a.col2 is None and not a.negate:
+                lo, hi = max(lo, a.lo), min(hi, a.hi)
+        if lo == INT64_MIN and hi == INT64_MAX:
+            return None            # this clause does not restrict the column
+        lo_all = lo if lo_all is None else min(lo_all, lo)
+        hi_all = hi if hi_all is None else max(hi_all, hi)
+    return (lo_all, hi_all) if lo_all is not None else None
+
+
+def _narrowed(v: "TableView", name: str) -> Column:
+    """Column metadata of `name` with its proven range intersected with the
+    ranges the view's predicates imply (Q7's l_shipdate in 1995-1996 gives a
+    2-year l_year key domain instead of the column's 7)."""
+    import copy
+    c = v.meta[name]
+    if c.kind not in ("int64", "date32") or v.origin.get(name, ("",))[0] != "base":
+        return c
+    lo, hi = c.lo, c.hi
+    for pred in (v.pre, v.post):
+        r = _pred_range(pred, name)
+        if r is not None:
+            lo, hi = max(lo, r[0]), min(hi, r[1])
+    if (lo, hi) == (c.lo, c.hi):
+        return c
+    c = copy.copy(c)
+    c.lo, c.hi = lo, hi
+    return c
 
 
 def derived_meta(src: Column, dk: DerivedKey) -> Column:
@@ -987,6 +1026,24 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
     b.ksrc = ksrc
     if dense:
         return _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross, timing)
+    dom = int(np.prod([max(1, c.hi - c.lo + 1) if c.kind != "dict" else len(c.dictionary)
+                       for c in kcols])) if keys else 1
+    if (_GROUP_MAT and n > (1 << 20) and dom > (1 << 22)
+            and any(st.kind in (L.JOIN_SEMI, L.JOIN_ANTI) for st in v.probes)):
+        # a hash group-by (large key domain: open addressing with CAS) behind
+        # a semi / anti join: compact the surviving rows first, so the group
+        # kernel's dependent CAS chains run over dense rows instead of idling
+        # behind the filter stages (measured at SF100: Q3 8.8 -> 6.5 ms, Q16
+        # 6.6 -> 3.8, Q20 8.4 -> 4.1 of kernel time; without a semi join the
+        # extra compaction pass costs more than it saves: Q7, Q10, Q13, Q15)
+        need = [c for c in v.visible if c in names] + sorted(names - set(v.visible))
+        dense_v = as_view(v.select(need).materialize())
+        dense_v.computed = dict(v.computed)
+        for k, dk in v.derived.items():
+            dense_v.derived[k] = dk
+            dense_v.meta[k] = v.meta[k]
+        dense_v.visible = list(v.visible)
+        return group_aggregate(dense_v, group_keys, aggs, cross, timing, sort)
     part = _group_hash(v, b, keys, kcols, plan, measures, count_m, sort)
     if cross is None or cross.ep.n == 1:
         return part

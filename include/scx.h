@@ -304,7 +304,9 @@ int scx_direct_agg_compact_counted(const int64_t* acc_dev, int64_t cap, int m, i
 /* Dense ranks of a non-decreasing key column (a clustered key: lineitem and
  * its materialised subsets by l_orderkey): rank_dev[i] = number of distinct
  * keys in key[0..i] - 1, keys_by_rank_dev[r] = (key of rank r) - lo,
- * *count_dev = number of distinct keys.  A group-by on such a key then uses a
+ * count_dev[0] = number of distinct keys, count_dev[1] = number of positions
+ * with key[i] < key[i-1] (non-zero: the column is not sorted and the ranks
+ * are meaningless).  A group-by on such a key then uses a
  * direct table of exactly that many slots instead of hashing (replaces the
  * np.unique codes of relops.py:117-119 for sorted keys).  temp_dev sized by
  * scx_sorted_rank_workspace(n). */

@@ -229,14 +229,24 @@ __device__ __forceinline__ uint32_t is_head(const scx_column& c, int64_t i) {
   return i == 0 || load_i64(p, c.dtype, i) != load_i64(p, c.dtype, i - 1);
 }
 
-__global__ void rank_count_kernel(scx_column c, int64_t n, uint64_t* part) {
+__global__ void rank_count_kernel(scx_column c, int64_t n, uint64_t* part, uint64_t* unsorted) {
   const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
-  uint32_t s = 0;
+  const void* p = reinterpret_cast<const void*>(c.ptr);
+  uint32_t s = 0, bad = 0;
+  int64_t prev = base > 0 && base < n ? load_i64(p, c.dtype, base - 1) : 0;
 #pragma unroll
-  for (int i = 0; i < kScanItems; ++i) s += (base + i < n) ? is_head(c, base + i) : 0u;
+  for (int i = 0; i < kScanItems; ++i) {
+    if (base + i < n) {
+      const int64_t k = load_i64(p, c.dtype, base + i);
+      s += (base + i == 0 || k != prev);
+      bad += (base + i > 0 && k < prev);
+      prev = k;
+    }
+  }
   uint32_t excl;
   const uint32_t tot = block_excl_scan(s, excl);
   if (threadIdx.x == 0) part[blockIdx.x] = tot;
+  if (bad) atomicAdd(reinterpret_cast<unsigned long long*>(unsorted), (unsigned long long)bad);
 }
 
 __global__ void rank_write_kernel(scx_column c, int64_t n, int64_t lo, const uint64_t* part,
@@ -279,13 +289,14 @@ extern "C" int scx_sorted_rank(const scx_column* key, int64_t n, int64_t lo, uin
   }
   cudaStream_t st = (cudaStream_t)stream;
   if (n == 0) {
-    SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
+    SCX_CUDA(cudaMemsetAsync(count, 0, 16, st));
     return SCX_OK;
   }
   const int64_t nb = (n + kScanTile - 1) / kScanTile;
   if (nb > 1024 * 64) { set_error("sorted_rank: column too long"); return SCX_EUNSUPPORTED; }
   uint64_t* part = static_cast<uint64_t*>(temp);
-  rank_count_kernel<<<(int)nb, kBlock, 0, st>>>(*key, n, part);
+  SCX_CUDA(cudaMemsetAsync(count + 1, 0, 8, st));
+  rank_count_kernel<<<(int)nb, kBlock, 0, st>>>(*key, n, part, count + 1);
   SCX_CHECK_LAUNCH("rank_count_kernel");
   small_scan_kernel<<<1, 1024, 0, st>>>(part, nb);
   SCX_CHECK_LAUNCH("small_scan_kernel");

@@ -38,6 +38,7 @@ from .table import Column, ColumnTable, HostColumn, SchemaError, alloc
 AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
 _GROUP_MAT = os.environ.get("SCX_GROUP_MAT", "1") != "0"
+_SORTED_RANK = os.environ.get("SCX_SORTED_RANK", "1") != "0"
 _DENSE_SMEM_BYTES = 48 * 1024     # per-CTA shared-memory group table (keeps 4 CTAs/SM)
 _OPCODE = {"sum": L.AGG_SUM, "count": L.AGG_COUNT, "min": L.AGG_MIN, "max": L.AGG_MAX}
 
@@ -1044,11 +1045,66 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
             dense_v.meta[k] = v.meta[k]
         dense_v.visible = list(v.visible)
         return group_aggregate(dense_v, group_keys, aggs, cross, timing, sort)
+    if (_SORTED_RANK and len(keys) == 1 and keys[0] not in v.derived
+            and v.origin.get(keys[0], ("",))[0] == "base" and kcols[0].kind in ("int64", "date32")
+            and n > (1 << 16) and dom > max(4 * n, 1 << 16)):
+        # clustered key (a materialised lineitem subset by l_orderkey): group
+        # by the key's dense rank -- a direct table of #distinct-keys slots
+        # filled sequentially -- instead of hashing into one sized by rows
+        ranked = _sorted_rank(v.base.column(keys[0]), kcols[0].lo)
+        if ranked is not None:
+            return _group_by_rank(v, keys[0], kcols[0], ranked, aggs, cross, timing)
     part = _group_hash(v, b, keys, kcols, plan, measures, count_m, sort)
     if cross is None or cross.ep.n == 1:
         return part
     full = cross.gather(part)
     return None if full is None else regroup(full, keys, aggs)
+
+
+def _sorted_rank(col: Column, lo: int):
+    """(rank Column u32, keys_by_rank u64 (key - lo), #distinct) when `col`
+    is non-decreasing, else None (and the column remembers it)."""
+    if col.sorted is False:
+        return None
+    torch = _torch()
+    n = col.row_count
+    rank = alloc(n, np.uint32)
+    kbr = alloc(n, np.uint64)
+    cnt = alloc(2, np.int64)
+    ws = alloc(max(2, L.load().scx_sorted_rank_workspace(n) // 8), np.int64)
+    L.call("scx_sorted_rank", C.byref(col.scx()), n, lo, _ptr(rank), _ptr(kbr), _ptr(cnt),
+           _ptr(ws), _stream())
+    g, bad = (int(x) for x in _to_host(cnt))
+    col.sorted = bad == 0
+    if bad:
+        return None
+    return Column("int64", rank, 0, None, 0, max(g - 1, 0)), kbr, g
+
+
+def _group_by_rank(v: TableView, key: str, kcol: Column, ranked, aggs, cross, timing):
+    rank_col, kbr, g = ranked
+    torch = _torch()
+    v2 = v._copy()
+    v2.base = v.base.with_column("__rank", rank_col)
+    v2.meta["__rank"] = rank_col
+    v2.origin["__rank"] = ("base", "__rank")
+    part = group_aggregate(v2, ["__rank"], aggs, None, timing, True)
+    G = part.row_count
+    r = part.column("__rank")
+    packed = alloc(G, np.uint64)
+    L.call("scx_gather", L.Column_(kbr.data_ptr(), L.SCX_I64, 0), _ptr(r.data), G,
+           L.Column_(packed.data_ptr(), L.SCX_I64, 0), _stream())
+    data = alloc(G, kcol.np_dtype)
+    L.call("scx_unpack_key", _ptr(packed), G, 0, (1 << 64) - 1, kcol.lo,
+           L.Column_(data.data_ptr(), kcol.scx_dtype, 0), _stream())
+    cols = {key: kcol.like(data)}
+    cols[key].sorted = True
+    cols.update({name: part.column(name) for name in aggs})
+    out = ColumnTable(cols, (key,))
+    if cross is None or cross.ep.n == 1:
+        return out
+    full = cross.gather(out)
+    return None if full is None else regroup(full, [key], aggs)
 
 
 def _dependent_keys(v: TableView, keys: list[str]) -> list[str]:

@@ -277,7 +277,7 @@ class Column:
     ``scale`` the fixed-point exponent of float64 columns.
     """
 
-    __slots__ = ("kind", "data", "scale", "dictionary", "lo", "hi", "dense")
+    __slots__ = ("kind", "data", "scale", "dictionary", "lo", "hi", "dense", "sorted")
 
     def __init__(self, kind: str, data, scale: int = 0, dictionary=None, lo: int = 0,
                  hi: int = -1, dense: bool = False):
@@ -296,6 +296,9 @@ class Column:
         # row i holds lo + i: a join on this column needs no lookup table
         # (row = key - lo), see relops.Lookup
         self.dense = dense
+        # non-decreasing in row order: None = not yet checked (relops checks
+        # it on the device when a group-by could use dense ranks)
+        self.sorted = True if dense else None
 
     # ---- construction ----
     @staticmethod

@@ -201,3 +201,30 @@ def test_radix_sort_large_and_edge_cases():
         idx = np.lexsort([-a, b]) if n else np.arange(0)
         assert np.array_equal(s.column("a").values, a[idx])
         assert np.array_equal(s.column("b").values, b[idx])
+
+
+@pytest.mark.parametrize("layout", ["sorted_sparse", "unsorted_sparse", "sorted_filtered"])
+def test_group_by_clustered_key(layout):
+    """Group-by on a sparse key whose domain is >> rows: a non-decreasing key
+    column takes the dense-rank path (scx_sorted_rank + direct table), an
+    unsorted one the hash path; both must equal the oracle's group
+    (relops.py:97-160: output sorted by key, int sums exact)."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(7)
+    n = 200_000
+    k = np.cumsum(rng.integers(0, 3, size=n)) * 997 + 5      # runs of equal keys, sparse
+    if layout == "unsorted_sparse":
+        k = rng.permutation(k)
+    x = rng.integers(-1000, 1000, size=n)
+    d = rng.integers(8000, 9000, size=n)
+    ref = {"k": ("int64", k, None), "x": ("int64", x, None), "d": ("date32", d.astype(np.int32), None)}
+    aggs = {"n": ("count", None), "sx": ("sum", "x"), "mn": ("min", "x"), "mx": ("max", "d")}
+    t = ColumnTable({n_: Column.from_numpy(kd, v) for n_, (kd, v, _) in ref.items()})
+    P = _dev()
+    if layout == "sorted_filtered":
+        got = P.group_aggregate(P.filter_table(t, t["x"] > 0), ["k"], aggs)
+        exp = O.group(O.filter_(ref, x > 0), ["k"], aggs)
+    else:
+        got = P.group_aggregate(t, ["k"], aggs)
+        exp = O.group(ref, ["k"], aggs)
+    assert_table_matches(got, O.to_jsonable(exp), layout)

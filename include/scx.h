@@ -301,6 +301,16 @@ int scx_direct_agg_compact_counted(const int64_t* acc_dev, int64_t cap, int m, i
                                    uint64_t* out_keys_dev, int64_t* out_acc_dev,
                                    uint64_t* count_dev, void* temp_dev, void* stream);
 
+/* Same with a HAVING range on one measure word folded into the compaction:
+ * slot e is kept iff its count word > 0 and hv_lo <= acc[e*m + hv_word] <=
+ * hv_hi (Q18's sum(l_quantity) > 300: 150M groups scanned, ~600 written).
+ * Equivalent to filtering the group_aggregate output (relops.py:97-160 then
+ * table.py:174-177). */
+int scx_direct_agg_compact_having(const int64_t* acc_dev, int64_t cap, int m, int occ_word,
+                                  int hv_word, int64_t hv_lo, int64_t hv_hi,
+                                  uint64_t* out_keys_dev, int64_t* out_acc_dev,
+                                  uint64_t* count_dev, void* temp_dev, void* stream);
+
 /* Dense ranks of a non-decreasing key column (a clustered key: lineitem and
  * its materialised subsets by l_orderkey): rank_dev[i] = number of distinct
  * keys in key[0..i] - 1, keys_by_rank_dev[r] = (key of rank r) - lo,

@@ -11,6 +11,8 @@
 // memory; across CTAs from a digit-major exclusive scan of the per-CTA
 // histograms.  So every element's output position is the same as a stable
 // sort by digit, which is exactly partition_indices' stable argsort.
+#include <stdlib.h>
+
 #include "common.cuh"
 
 namespace scx {
@@ -76,7 +78,8 @@ __device__ __forceinline__ void scatter_chunk(const DigitSrc& D, int64_t n, int 
     run[d] = d < ndig ? offs[(int64_t)d * nblocks + blockIdx.x] : 0;
   const int64_t base = (int64_t)blockIdx.x * kChunk;
   for (int it = 0; it < kItems; ++it) {
-    for (int j = tid; j < kWarps * kDigits; j += kBlock) (&wc[0][0])[j] = 0;
+    // only the ndig live digit columns (8 for an 8-way partition, 256 for sort)
+    for (int j = tid; j < kWarps * ndig; j += kBlock) wc[j / ndig][j % ndig] = 0;
     __syncthreads();
     const int64_t i = base + it * kBlock + tid;
     const bool valid = i < n;
@@ -86,7 +89,7 @@ __device__ __forceinline__ void scatter_chunk(const DigitSrc& D, int64_t n, int 
     if (valid && rank == 0) wc[warp][d] = __popc(peers);
     __syncthreads();
     // per digit: exclusive scan over warps (thread d owns digit d)
-    for (int dd = tid; dd < kDigits; dd += kBlock) {
+    for (int dd = tid; dd < ndig; dd += kBlock) {
       uint32_t s = 0;
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) { const uint32_t c = wc[w][dd]; wc[w][dd] = s; s += c; }
@@ -135,6 +138,88 @@ __global__ void part_scatter_kernel(DigitSrc D, int64_t n, int nparts, const uin
       }
     }
   });
+}
+
+// ---- warp-segmented partition for few parts (N <= 16: one part per GPU) ----
+// Every warp owns a contiguous segment of kWSeg rows.  Pass 1 counts rows per
+// (part, segment); a part-major exclusive scan gives each warp, for each
+// part, the output position of its first row.  Pass 2: the warp walks its
+// segment 32 rows at a time (coalesced 8-byte loads, 4 steps of loads in
+// flight), ranks each row among equal parts of the step with __match_any_sync
+// (stable: lower lane = earlier row) and stores it at cursor[part] + rank;
+// lane p keeps cursor[p] in a register.  No block-wide barrier anywhere, and
+// each store instruction writes at most N contiguous runs.
+constexpr int kWSeg = 4096;                       // rows per warp segment
+constexpr int kPMaxParts = 16;
+constexpr int kWUnroll = 4;
+
+__global__ void part_hist3_kernel(PartKeys K, int64_t n, int nparts, uint32_t* counts,
+                                  int64_t nseg) {
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const int64_t base = seg * kWSeg;
+  uint32_t mine = 0;                              // lane p: rows of part p
+  for (int s0 = 0; s0 < kWSeg; s0 += 32 * kWUnroll) {
+    uint32_t d[kWUnroll];
+#pragma unroll
+    for (int u = 0; u < kWUnroll; ++u) {
+      const int64_t i = base + s0 + u * 32 + lane;
+      d[u] = i < n ? bucket_of(K, i, (uint32_t)nparts) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < kWUnroll; ++u) {
+      for (int p = 0; p < nparts; ++p) {
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, d[u] == (uint32_t)p));
+        if (lane == p) mine += c;
+      }
+    }
+  }
+  if (lane < nparts) counts[(int64_t)lane * nseg + seg] = mine;
+}
+
+__global__ void part_scatter3_kernel(PartKeys K, int64_t n, int nparts, const uint64_t* offs,
+                                     int64_t nseg, PartCols C) {
+  const int lane = threadIdx.x & 31;
+  const int64_t seg = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  if (seg >= nseg) return;
+  const int64_t base = seg * kWSeg;
+  uint64_t cur = lane < nparts ? offs[(int64_t)lane * nseg + seg] : 0;   // lane p: next slot of part p
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int s0 = 0; s0 < kWSeg; s0 += 32 * kWUnroll) {
+    uint32_t d[kWUnroll];
+#pragma unroll
+    for (int u = 0; u < kWUnroll; ++u) {
+      const int64_t i = base + s0 + u * 32 + lane;
+      d[u] = i < n ? bucket_of(K, i, (uint32_t)nparts) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int u = 0; u < kWUnroll; ++u) {
+      const int64_t i = base + s0 + u * 32 + lane;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d[u]);
+      const uint32_t rank = __popc(peers & lt);
+      const uint64_t start = __shfl_sync(0xffffffffu, cur, d[u] < 32 ? (int)d[u] : 0);
+      if (i < n) {
+        const uint64_t pos = start + rank;
+        for (int c = 0; c < C.n; ++c) {
+          const int w = dtype_size_d(C.in[c].dtype);
+          const char* src = reinterpret_cast<const char*>(C.in[c].ptr);
+          char* dst = reinterpret_cast<char*>(C.out[c].ptr);
+          switch (w) {
+            case 1: dst[pos] = src[i]; break;
+            case 2: reinterpret_cast<int16_t*>(dst)[pos] = reinterpret_cast<const int16_t*>(src)[i]; break;
+            case 4: reinterpret_cast<int32_t*>(dst)[pos] = reinterpret_cast<const int32_t*>(src)[i]; break;
+            default: reinterpret_cast<int64_t*>(dst)[pos] = reinterpret_cast<const int64_t*>(src)[i]; break;
+          }
+        }
+      }
+      // advance the cursors: part p gained popc(ballot(d == p)) rows
+      for (int p = 0; p < nparts; ++p) {
+        const uint32_t c = __popc(__ballot_sync(0xffffffffu, d[u] == (uint32_t)p));
+        if (lane == p) cur += c;
+      }
+    }
+  }
 }
 
 __global__ void part_counts_kernel(const uint64_t* offs, int nparts, int nblocks, uint64_t* counts) {
@@ -279,6 +364,28 @@ extern "C" int scx_partition(const scx_column* keys, int n_keys, const scx_colum
   }
   const uint64_t* offs;
   int nb;
+  // measured on B200 (1 GiB of 16-byte rows, 8 parts): the warp-segmented
+  // path is 1.44 ms vs 1.05 ms for the CTA-ranked path below, so it is opt-in
+  if (n_parts <= kPMaxParts && getenv("SCX_PART_WARPSEG") != nullptr) {
+    // warp-segmented path: per-(part, segment) counts, part-major scan, scatter
+    const int64_t nseg = (n + kWSeg - 1) / kWSeg;
+    const int64_t nblk = (nseg + kWarps - 1) / kWarps;
+    uint32_t* cnts = static_cast<uint32_t*>(temp);
+    uint64_t* o2 = reinterpret_cast<uint64_t*>(static_cast<char*>(temp) +
+                                               ((nseg * n_parts * 4 + 255) / 256) * 256);
+    uint64_t* tmp = o2 + nseg * n_parts + 1;
+    part_hist3_kernel<<<(int)nblk, kBlock, 0, st>>>(D.pk, n, n_parts, cnts, nseg);
+    SCX_CHECK_LAUNCH("part_hist3_kernel");
+    int rc = scan_u32_excl(cnts, o2, nseg * n_parts, tmp, st);
+    if (rc) return rc;
+    part_counts_kernel<<<1, kDigits, 0, st>>>(o2, n_parts, (int)nseg, counts);
+    SCX_CHECK_LAUNCH("part_counts_kernel");
+    if (n_cols > 0) {
+      part_scatter3_kernel<<<(int)nblk, kBlock, 0, st>>>(D.pk, n, n_parts, o2, nseg, C);
+      SCX_CHECK_LAUNCH("part_scatter3_kernel");
+    }
+    return SCX_OK;
+  }
   int rc = counting_pass(D, n, n_parts, temp, st, offs, nb);
   if (rc) return rc;
   part_counts_kernel<<<1, kDigits, 0, st>>>(offs, n_parts, nb, counts);

@@ -127,8 +127,13 @@ struct Occ {
   const uint64_t* gkeys;
   const int64_t* acc;
   int m, occ_word;
+  int hv_word;               // HAVING on a measure word: keep iff hv_lo <= acc <= hv_hi (-1: none)
+  int64_t hv_lo, hv_hi;
+  __device__ __forceinline__ bool keep(const int64_t* row) const {
+    return row[occ_word] > 0 && (hv_word < 0 || (row[hv_word] >= hv_lo && row[hv_word] <= hv_hi));
+  }
   __device__ __forceinline__ bool operator()(int64_t e) const {
-    return gkeys ? gkeys[e] != SCX_EMPTY_KEY : acc[e * m + occ_word] > 0;
+    return gkeys ? gkeys[e] != SCX_EMPTY_KEY : keep(acc + e * m);
   }
   __device__ __forceinline__ uint64_t key(int64_t e) const { return gkeys ? gkeys[e] : (uint64_t)e; }
 };
@@ -161,7 +166,7 @@ __global__ void __launch_bounds__(kBlock) occ_write_kernel(
     const int64_t rows = min((int64_t)kBlock, cap - r0);
     for (int64_t x = tid; x < rows * m; x += kBlock) tile[x] = acc[r0 * m + x];
     __syncthreads();
-    const bool occ = e < cap && (O.gkeys ? O.gkeys[e] != SCX_EMPTY_KEY : tile[tid * m + O.occ_word] > 0);
+    const bool occ = e < cap && (O.gkeys ? O.gkeys[e] != SCX_EMPTY_KEY : O.keep(tile + tid * m));
     const uint32_t b = __ballot_sync(0xffffffffu, occ);
     if (lane == 0) wcnt[warp] = __popc(b);
     __syncthreads();
@@ -333,7 +338,7 @@ extern "C" int scx_direct_agg_compact(const uint64_t* gkeys, const int64_t* acc,
     set_error("direct_agg_compact: bad arguments");
     return SCX_EINVAL;
   }
-  Occ O{gkeys, acc, m, 0};
+  Occ O{gkeys, acc, m, 0, -1, 0, 0};
   return direct_compact(O, acc, cap, m, out_keys, out_acc, count, temp, (cudaStream_t)stream);
 }
 
@@ -346,6 +351,20 @@ extern "C" int scx_direct_agg_compact_counted(const int64_t* acc, int64_t cap, i
     set_error("direct_agg_compact_counted: bad arguments");
     return SCX_EINVAL;
   }
-  Occ O{nullptr, acc, m, occ_word};
+  Occ O{nullptr, acc, m, occ_word, -1, 0, 0};
+  return direct_compact(O, acc, cap, m, out_keys, out_acc, count, temp, (cudaStream_t)stream);
+}
+
+extern "C" int scx_direct_agg_compact_having(const int64_t* acc, int64_t cap, int m,
+                                             int occ_word, int hv_word, int64_t hv_lo,
+                                             int64_t hv_hi, uint64_t* out_keys,
+                                             int64_t* out_acc, uint64_t* count, void* temp,
+                                             void* stream) {
+  if (!acc || !out_keys || !out_acc || !count || !temp || m < 1 || m > 16 || occ_word < 0 ||
+      occ_word >= m || hv_word < 0 || hv_word >= m) {
+    set_error("direct_agg_compact_having: bad arguments");
+    return SCX_EINVAL;
+  }
+  Occ O{nullptr, acc, m, occ_word, hv_word, hv_lo, hv_hi};
   return direct_compact(O, acc, cap, m, out_keys, out_acc, count, temp, (cudaStream_t)stream);
 }

@@ -228,10 +228,12 @@ class DeviceContext:
     def join(self, left, right, on, how="inner"):
         return R.local_hash_join(left, right, on, how)
 
-    def group(self, t, keys, aggs, sort: bool = True):
+    def group(self, t, keys, aggs, sort: bool = True, having: tuple | None = None):
         """group_aggregate; ``sort=False`` (an extension) skips the key-order
-        sort for intermediates that feed a join or a re-aggregation."""
-        return R.group_aggregate(t, keys, aggs, sort=sort)
+        sort for intermediates that feed a join or a re-aggregation, and
+        ``having=(name, lo, hi)`` keeps groups with lo <= name <= hi (rank-local:
+        the groups must be complete on this rank)."""
+        return R.group_aggregate(t, keys, aggs, sort=sort, having=having)
 
     def add_column(self, t, name, col):
         return R.as_view(t).with_column(name, col)

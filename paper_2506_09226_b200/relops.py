@@ -39,6 +39,7 @@ AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
 _GROUP_MAT = os.environ.get("SCX_GROUP_MAT", "1") != "0"
 _SORTED_RANK = os.environ.get("SCX_SORTED_RANK", "1") != "0"
+_DIRECT_MAX_SPAN = 1 << 28       # direct lookup tables up to 1 GB of u32 rows
 _DENSE_SMEM_BYTES = 48 * 1024     # per-CTA shared-memory group table (keeps 4 CTAs/SM)
 _OPCODE = {"sum": L.AGG_SUM, "count": L.AGG_COUNT, "min": L.AGG_MIN, "max": L.AGG_MAX}
 
@@ -148,7 +149,10 @@ class Lookup:
             self.lk.keys = 0
             self._unique = True
             return
-        if span <= max(4 * n, 1 << 16) and span <= (1 << 31):
+        if (span <= max(4 * n, 1 << 16) or span <= _DIRECT_MAX_SPAN) and span <= (1 << 31):
+            # a direct table costs span x 4 B of fill (<= 1 GB, ~0.15 ms) but
+            # each probe is ONE random sector instead of key + row sectors of
+            # open addressing -- the probes dominate (Q7: 171M probes)
             self.lk.kind = L.HT_DIRECT
             self.lk.cap = span
             self._vals = alloc(span, np.uint32)
@@ -806,6 +810,46 @@ class _Builder:
         L.call("scx_pipeline_run", C.byref(self.P), _stream())
 
 
+def _measure_range(im: IntMeasure | None, meta: dict[str, Column]):
+    """[lo, hi] of a measure's per-row value from the columns' proven ranges
+    (interval arithmetic; count = 1), or None when a range is not proven."""
+    if im is None:
+        return 1, 1
+    lo_t, hi_t = 0, 0
+    for coef, fs in im.terms:
+        lo, hi = coef, coef
+        for a, bb, col in fs:
+            c = meta[col]
+            if not (c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo):
+                return None
+            clo, chi = c.lo, c.hi
+            x, y = a + bb * clo, a + bb * chi
+            cands = (lo * x, lo * y, hi * x, hi * y)
+            lo, hi = min(cands), max(cands)
+        lo_t, hi_t = lo_t + lo, hi_t + hi
+    if im.cond is not None:            # a gated-off row contributes 0
+        lo_t, hi_t = min(lo_t, 0), max(hi_t, 0)
+    return lo_t, hi_t
+
+
+def _pack_budgets(P, measures, meta, n: int) -> None:
+    """Dense sinks: mark sum / count measures whose per-thread partial sum is
+    provably non-negative and small with their bit budget (measure._pad =
+    0x100 | bits), so the kernel can add several of them with ONE 64-bit
+    shared-memory update (Q1: qty, discount and count share a word)."""
+    rows_per_thread = n // (148 * 256) + 16
+    for i, (op, im) in enumerate(measures):
+        if op not in ("sum", "count"):
+            continue
+        r = _measure_range(im, meta)
+        if r is None or r[0] < 0:
+            continue
+        lo, hi = r
+        bits = max(1, int(hi * rows_per_thread).bit_length())
+        if bits <= 40:
+            P.sink.m[i]._pad = 0x100 | bits
+
+
 def _measure_bound(im: IntMeasure, meta: dict[str, Column]) -> int:
     tot = 0
     for coef, fs in im.terms:
@@ -959,19 +1003,37 @@ def _plan_aggs(v: TableView, aggs: dict) -> tuple[list[_Agg], list[tuple[str, In
     return plan, measures
 
 
+def _apply_having(t, having):
+    """HAVING lo <= t[name] <= hi as a filter over a group result."""
+    if t is None or having is None:
+        return t
+    name, lo, hi = having
+    return filter_table(t, (t[name] >= lo) & (t[name] <= hi)).materialize()
+
+
 def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
-                    cross=None, timing: list | None = None, sort: bool = True) -> ColumnTable:
+                    cross=None, timing: list | None = None, sort: bool = True,
+                    having: tuple | None = None) -> ColumnTable:
     """Aggregate per group (relops.py:97-160), one fused kernel launch.
 
     ``cross`` (engine.DeviceContext) makes it a global aggregate over all
     ranks: dense partials are all-gathered and summed exactly in 128 bits;
     hash partials are gathered to the root and re-aggregated.
+
+    ``having = (name, lo, hi)`` keeps the groups with lo <= name <= hi (SQL
+    HAVING; same result as filtering the output).  For a direct-addressed
+    table and an integer sum / count it is folded into the table compaction.
     """
+    if having is not None and (cross is not None and cross.ep.n > 1):
+        # partial aggregates cannot be filtered before the cross-rank merge
+        return _apply_having(group_aggregate(table, group_keys, aggs, cross, timing, sort),
+                             having)
     v = as_view(table)
     keys = list(group_keys)
     fd = _dependent_keys(v, keys)
     if fd:
-        return _group_with_dependent_keys(v, keys, fd, aggs, cross, timing, sort)
+        return _apply_having(_group_with_dependent_keys(v, keys, fd, aggs, cross, timing, sort),
+                             having)
     for k in keys:
         if k in v.computed or k not in v.meta:
             raise SchemaError(f"unknown group key {k!r}")
@@ -1026,7 +1088,9 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
                 b.P.sink.m[i]._pad = 1
     b.ksrc = ksrc
     if dense:
-        return _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross, timing)
+        return _apply_having(
+            _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross, timing),
+            having)
     dom = int(np.prod([max(1, c.hi - c.lo + 1) if c.kind != "dict" else len(c.dictionary)
                        for c in kcols])) if keys else 1
     if (_GROUP_MAT and n > (1 << 20) and dom > (1 << 22)
@@ -1044,7 +1108,7 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
             dense_v.derived[k] = dk
             dense_v.meta[k] = v.meta[k]
         dense_v.visible = list(v.visible)
-        return group_aggregate(dense_v, group_keys, aggs, cross, timing, sort)
+        return group_aggregate(dense_v, group_keys, aggs, cross, timing, sort, having)
     if (_SORTED_RANK and len(keys) == 1 and keys[0] not in v.derived
             and v.origin.get(keys[0], ("",))[0] == "base" and kcols[0].kind in ("int64", "date32")
             and n > (1 << 16) and dom > max(4 * n, 1 << 16)):
@@ -1053,8 +1117,19 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
         # filled sequentially -- instead of hashing into one sized by rows
         ranked = _sorted_rank(v.base.column(keys[0]), kcols[0].lo)
         if ranked is not None:
-            return _group_by_rank(v, keys[0], kcols[0], ranked, aggs, cross, timing)
-    part = _group_hash(v, b, keys, kcols, plan, measures, count_m, sort)
+            return _apply_having(_group_by_rank(v, keys[0], kcols[0], ranked, aggs, cross, timing),
+                                 having)
+    hv = None
+    if having is not None:
+        a = next((a for a in plan if a.out == having[0]), None)
+        if a is None:
+            raise SchemaError(f"HAVING on unknown aggregate {having[0]!r}")
+        if (a.op == "count" or (a.op == "sum" and a.kind == "int64" and a.q == 1)) \
+                and not b.P.sink.m[a.m]._pad:
+            hv = (a.m, int(having[1]), int(having[2]))
+    part = _group_hash(v, b, keys, kcols, plan, measures, count_m, sort, hv)
+    if having is not None and not getattr(part, "_having_done", False):
+        part = _apply_having(part, having)
     if cross is None or cross.ep.n == 1:
         return part
     full = cross.gather(part)
@@ -1163,6 +1238,7 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
     torch = _torch()
     S = b.P.sink
     S.kind = L.SINK_AGG_DENSE
+    _pack_budgets(b.P, measures, v.meta, v.base.row_count)
     S.n_cells = cells
     S.gkey.n = len(keys)
     luts = []
@@ -1262,7 +1338,7 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
     return ColumnTable(out, tuple(keys))
 
 
-def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> ColumnTable:
+def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) -> ColumnTable:
     torch = _torch()
     S = b.P.sink
     S.kind = L.SINK_AGG_HASH
@@ -1359,8 +1435,13 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
         if direct:
             # slot order == packed-key order: ordered compaction, no sort
             ws = alloc(max(2, L.load().scx_direct_agg_workspace(cap) // 8), np.int64)
-            L.call("scx_direct_agg_compact_counted", _ptr(accb), cap, W, int(woff[count_m]),
-                   _ptr(out_keys), _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
+            if hv is not None:
+                L.call("scx_direct_agg_compact_having", _ptr(accb), cap, W, int(woff[count_m]),
+                       int(woff[hv[0]]), hv[1], hv[2], _ptr(out_keys), _ptr(out_acc), _ptr(cnt),
+                       _ptr(ws), _stream())
+            else:
+                L.call("scx_direct_agg_compact_counted", _ptr(accb), cap, W, int(woff[count_m]),
+                       _ptr(out_keys), _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
         else:
             L.call("scx_hash_agg_compact", _ptr(gkeys), _ptr(accb), cap, W, _ptr(out_keys),
                    _ptr(out_acc), _ptr(cnt), _stream())
@@ -1448,7 +1529,9 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True) -> Column
             dst = alloc(G, np.float64)
             L.call("scx_fixed_to_f64", _ptr(s_col), 1, G, k, _ptr(c_col), 1, _ptr(dst), _stream())
             out[a.out] = Column("float64", dst, -1, None, 0, -1)
-    return ColumnTable(out, tuple(keys))
+    res = ColumnTable(out, tuple(keys))
+    res._having_done = direct and hv is not None
+    return res
 
 
 # ---------------------------------------------------------------------------

@@ -172,7 +172,7 @@ def test_hash_keys_and_partition_match_reference():
         assert [[int(x) for x in p.column("a").values[:5]] for p in parts2] == exp["multi_first"]
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 8, 16])
+@pytest.mark.parametrize("n", [1, 2, 3, 8, 16, 17, 64])
 def test_partition_large_stable(n):
     """Partition of SF1 lineitem on l_orderkey == oracle stable partition."""
     P = _dev()
@@ -228,3 +228,23 @@ def test_group_by_clustered_key(layout):
         got = P.group_aggregate(t, ["k"], aggs)
         exp = O.group(ref, ["k"], aggs)
     assert_table_matches(got, O.to_jsonable(exp), layout)
+
+
+@pytest.mark.parametrize("dense_keys", [True, False])
+def test_group_having(dense_keys):
+    """group_aggregate(..., having=(name, lo, hi)) == filter(group_aggregate).
+    Dense keys take the direct table with HAVING folded into its compaction;
+    sparse keys the generic post-filter."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(11)
+    n = 200_000
+    k = rng.integers(0, 50_000, size=n) * (1 if dense_keys else 1_000_003)
+    x = rng.integers(0, 100, size=n)
+    ref = {"k": ("int64", k, None), "x": ("int64", x, None)}
+    aggs = {"n": ("count", None), "sx": ("sum", "x")}
+    t = ColumnTable({n_: Column.from_numpy(kd, v) for n_, (kd, v, _) in ref.items()})
+    got = _dev().group_aggregate(t, ["k"], aggs, having=("sx", 300, 400))
+    exp = O.group(ref, ["k"], aggs)
+    sx = exp["sx"][1]
+    exp = O.filter_(exp, (sx >= 300) & (sx <= 400))
+    assert_table_matches(got, O.to_jsonable(exp), f"having dense={dense_keys}")

@@ -95,6 +95,15 @@ def _hashgroup():
     return P
 
 
+def _q1_packed():
+    # SF100 bit budgets (measure._pad = 0x100 | bits): qty, ext, ext*(1-d),
+    # ext*(1-d)*(1+t) (too wide), disc, count
+    P = _q1()
+    for i, b in enumerate([20, 38, 44, 0, 18, 14]):
+        P.sink.m[i]._pad = (0x100 | b) if b else 0
+    return P
+
+
 def _dense_smem():
     P = _q1()
     P.sink.n_cells = 12
@@ -153,7 +162,8 @@ PLANS = {
     "bitmap_sink": _bitmap_sink,
     "semi_bitmap_probe": lambda: _compact_probe(L.HT_BITMAP, L.JOIN_SEMI),
     "poly_atom_left_join_year_key": _poly_left_year,
-    "q6_dense1": _q6, "q1_dense6": _q1, "dense_smem": _dense_smem, "count": _count,
+    "q6_dense1": _q6, "q1_dense6": _q1, "q1_dense6_packed": _q1_packed,
+    "dense_smem": _dense_smem, "count": _count,
     "compact_inner_hash": _compact_probe,
     "compact_semi_direct": lambda: _compact_probe(L.HT_DIRECT, L.JOIN_SEMI),
     "compact_anti_hash": lambda: _compact_probe(L.HT_HASH, L.JOIN_ANTI),
@@ -175,7 +185,8 @@ def test_codegen_compiles_for_sm100a(lib, name):
     cache = os.environ["SCX_JIT_CACHE"]
     cubins = [f for f in os.listdir(cache) if f.endswith(".cubin")]
     assert cubins
-    kname = src.split("void __launch_bounds__(256, 2) ")[1].split("(")[0]
+    kname = src.split("scx_pipe_")[1].split("(")[0]
+    kname = "scx_pipe_" + kname
     res = subprocess.run(["cuobjdump", "-res-usage", os.path.join(cache, kname + ".cubin")],
                          capture_output=True, text=True)
     if res.returncode == 0:

@@ -35,6 +35,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TPC-H 22-query total time (s) at SF100, 1/2/4/8 B200; shuffle GB/s vs NVLink"
 QUERIES = tuple(f"Q{i}" for i in range(1, 23))
+# e2e at N=1: upload order (by first use, biggest consumers first) and the
+# query order that follows table arrival (all 22 queries, each exactly once)
+E2E_TABLE_ORDER = ("lineitem", "orders", "customer", "nation", "region", "supplier", "part",
+                   "partsupp")
+E2E_QUERY_ORDER = ("Q1", "Q6", "Q12", "Q4", "Q18", "Q3", "Q13", "Q22", "Q10", "Q5", "Q7", "Q21",
+                   "Q15", "Q14", "Q19", "Q17", "Q8", "Q9", "Q2", "Q11", "Q16", "Q20")
+assert sorted(E2E_QUERY_ORDER) == sorted(QUERIES)
 
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -300,7 +307,7 @@ def main() -> None:
     import paper_2506_09226_b200 as P
     from paper_2506_09226_b200 import _lib
     from paper_2506_09226_b200.data import cached_generate, load_dataset
-    from paper_2506_09226_b200.engine import DeviceContext, load_tables
+    from paper_2506_09226_b200.engine import DeviceContext, load_tables, upload_tables_async
     from paper_2506_09226_b200.queries import PLAN_FUNCTIONS
 
     ep = P.create_cluster("nccl")
@@ -402,6 +409,13 @@ def main() -> None:
             src = torch.from_numpy(np.ascontiguousarray(hc.values)).pin_memory()
             host_cols[(tname, cname)] = src
     h2d_bytes = sum(t.numel() * t.element_size() for t in host_cols.values())
+    # N=1: tables stream in on a copy stream (largest / most-used first) and
+    # the queries run in the order their tables arrive, each waiting only for
+    # its own tables -- PCIe transfer overlapped with query execution
+    copy_order = [t for t in E2E_TABLE_ORDER if t in names] + \
+        [t for t in names if t not in E2E_TABLE_ORDER]
+    host = {t: {c: (hc, host_cols[(t, c)]) for c, hc in ds.tables[t].columns.items()}
+            for t in names}
     e2e_ms = []
     d2h_bytes = 0
     for i in range(max(1, min(args.steps, 3)) + 1):
@@ -409,18 +423,26 @@ def main() -> None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        dev_tables = {}
-        for tname in names:
-            cols = {}
-            for cname, hc in ds.tables[tname].columns.items():
-                buf = P.table.alloc(hc.row_count, hc.values.dtype)
-                buf.copy_(host_cols[(tname, cname)], non_blocking=True)
-                cols[cname] = P.Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi)
-            dev_tables[tname] = P.ColumnTable(cols)
-        if ep.n > 1:
+        if ep.n == 1:
+            dev_tables, ready = upload_tables_async(host, copy_order)
+            res = {}
+            for q in E2E_QUERY_ORDER:
+                ctx = DeviceContext(ep, dev_tables, "default", "default_keys", timed=False,
+                                    ready=ready)
+                r = PLAN_FUNCTIONS[q](ctx)
+                res[q] = r.materialize() if r is not None else None
+        else:
+            dev_tables = {}
+            for tname in names:
+                cols = {}
+                for cname, hc in ds.tables[tname].columns.items():
+                    buf = P.table.alloc(hc.row_count, hc.values.dtype)
+                    buf.copy_(host_cols[(tname, cname)], non_blocking=True)
+                    cols[cname] = P.Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi)
+                dev_tables[tname] = P.ColumnTable(cols)
             dev_tables = {n: P.hash_partition(t, [P.DEFAULT_PARTITION_KEYS[n]], ep.n)[ep.rank]
                           for n, t in dev_tables.items()}
-        res = suite(dev_tables)
+            res = suite(dev_tables)
         out = {q: (r.to_reference() if r is not None else None) for q, r in res.items()}
         e1.record()
         sync_all()
@@ -429,6 +451,9 @@ def main() -> None:
         d2h_bytes = sum(v.nbytes for r in out.values() if r for _, v, _ in r.values())
         del dev_tables
     e2e_s = max_over_ranks(statistics.mean(e2e_ms)) / 1e3
+    # the streamed e2e pass must reproduce the device-resident results
+    e2e_match = all(P.result_digest(results[q]) == P.result_digest(res[q]) if results[q] is not None
+                    else res[q] is None for q in QUERIES)
 
     # ---- roofline: Q1's fused scan kernel timed alone (dominant single launch) ----
     pk = peaks()
@@ -498,7 +523,8 @@ def main() -> None:
                        "sf": args.sf, "queries": list(QUERIES),
                        "parallelism": f"dp{ep.n}", "l2": "flushed between steps (512 MB write)",
                        "layout": "narrowed fixed-point columns in HBM"},
-            "e2e": {"value": round(e2e_s, 6), "unit": "s", "h2d_bytes_per_step": h2d_bytes,
+            "e2e": {"value": round(e2e_s, 6), "unit": "s", "results_match_device_run": e2e_match,
+                    "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes},
             "roofline": roofline,
             "cpu_baseline": cpu,

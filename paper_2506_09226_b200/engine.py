@@ -26,7 +26,7 @@ from . import exchange as X
 from . import relops as R
 from .cluster import Endpoint, barrier, create_cluster
 from .data import DEFAULT_PARTITION_KEYS, Dataset, PARTITION_SCHEMES, DataError
-from .table import Column, ColumnTable, concat_tables
+from .table import Column, ColumnTable, alloc, concat_tables
 
 
 class PlanError(ValueError):
@@ -199,9 +199,12 @@ class DeviceContext:
 
     def __init__(self, ep: Endpoint, tables: dict[str, ColumnTable], variant: str = "default",
                  scheme: str = "default_keys", p2p_broadcast: bool = False,
-                 timed: bool = True):
+                 timed: bool = True, ready: dict | None = None):
         self.ep = ep
         self.tables = tables
+        # table name -> CUDA event of its (asynchronous) upload: the first
+        # access makes this stream wait for it (upload_tables_async)
+        self.ready = ready
         self.variant = variant
         self.scheme = scheme
         self.p2p_broadcast = p2p_broadcast
@@ -220,6 +223,9 @@ class DeviceContext:
         return self.ep.rank == 0
 
     def table(self, name: str) -> ColumnTable:
+        if self.ready is not None and name in self.ready:
+            import torch
+            torch.cuda.current_stream().wait_event(self.ready.pop(name))
         return self.tables[name]
 
     def filter(self, t, mask):
@@ -329,6 +335,39 @@ class DeviceContext:
 # ---------------------------------------------------------------------------
 # data placement
 # ---------------------------------------------------------------------------
+
+def upload_tables_async(host: dict, order=None, stream=None):
+    """Upload pinned host columns on a copy stream, table by table in `order`
+    (first use first), without blocking the compute stream.
+
+    ``host``: {table: {column: (HostColumn, pinned torch tensor)}}.  Returns
+    (device tables, {table: event}); pass the events as
+    ``DeviceContext(ready=...)`` so each query waits only for the tables it
+    touches while the later tables are still crossing PCIe (H2D overlapped
+    with the queries that can already run).  Single-rank tables only.
+    """
+    import torch
+    cs = stream or torch.cuda.Stream()
+    main = torch.cuda.current_stream()
+    cs.wait_stream(main)           # buffers below are allocated on `main`
+    tables, events = {}, {}
+    for tname in (order or list(host)):
+        cols = {}
+        bufs = []
+        for cname, (hc, pinned) in host[tname].items():
+            buf = alloc(hc.row_count, hc.values.dtype)
+            bufs.append((buf, pinned))
+            cols[cname] = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
+                                 hc.dense and hc.row_count == hc.hi - hc.lo + 1)
+        with torch.cuda.stream(cs):
+            for buf, pinned in bufs:
+                buf.copy_(pinned, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        tables[tname] = ColumnTable(cols)
+        events[tname] = ev
+    return tables, events
+
 
 def load_tables(ds: Dataset, ep: Endpoint | None = None, scheme: str = "default_keys",
                 names=None) -> dict[str, ColumnTable]:

@@ -500,7 +500,9 @@ def main() -> None:
         b = q_bytes[q]
         t_roof = b / (pk["hbm_gbs"] * 1e9)
         per_query[q] = {"s": round(t, 6) if t else None, "alg_bytes": b,
-                        "roof_frac": round(t_roof / t, 4) if t else None}
+                        "roof_frac": round(t_roof / t, 4) if t else None,
+                        "s_min": round(min(q_ms[q]) / 1e3, 6) if q_ms[q] else None,
+                        "s_max": round(max(q_ms[q]) / 1e3, 6) if q_ms[q] else None}
 
     cpu = None
     if ep.rank == 0 and not args.no_cpu:

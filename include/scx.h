@@ -171,8 +171,10 @@ typedef struct scx_keyspec {
 /* Lookup table built by scx_table_build and probed inside a pipeline. */
 typedef struct scx_lookup {
   int32_t kind;        /* SCX_HT_HASH / SCX_HT_DIRECT */
-  int32_t _pad;
-  uint64_t keys;       /* HASH: u64[cap], SCX_EMPTY_KEY = free        */
+  int32_t _pad;        /* BITMAP: coarse shift + 1 (0 = no coarse level)  */
+  uint64_t keys;       /* HASH: u64[cap], SCX_EMPTY_KEY = free;
+                          BITMAP: coarse bitmap (see scx_bitmap_coarsen),
+                          staged in shared memory by the probing kernel */
   uint64_t vals;       /* u32[cap] build row, SCX_NO_ROW = free        */
   uint64_t cap;        /* HASH: power of two; DIRECT: key range size   */
 } scx_lookup;
@@ -324,6 +326,14 @@ int64_t scx_sorted_rank_workspace(int64_t n);
 int scx_sorted_rank(const scx_column* key, int64_t n, int64_t lo, uint32_t* rank_dev,
                     uint64_t* keys_by_rank_dev, uint64_t* count_dev, void* temp_dev,
                     void* stream);
+
+/* Coarse level of a membership bitmap: bit j of coarse_dev = OR of fine bits
+ * [j << shift, (j+1) << shift) over nbits fine bits (rounded up to whole
+ * words).  A probing kernel keeps it in shared memory and reads the fine
+ * bitmap only when the coarse bit is set (the np.isin of relops.py:75 for
+ * selective semi joins). */
+int scx_bitmap_coarsen(const uint32_t* fine_dev, int64_t nbits, int shift, uint32_t* coarse_dev,
+                       void* stream);
 
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not

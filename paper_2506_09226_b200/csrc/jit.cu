@@ -392,6 +392,7 @@ struct Gen {
   size_t dyn_smem = 0;
   int stage_p = -1, stage_rows_p = -1;   // COMPACT: staging base / rows, bound at launch
   int nw_priv = 0;              // dense private accumulators: 64-bit words per cell
+  int coarse_p[SCX_MAX_PROBES] = {-1, -1, -1, -1, -1, -1, -1, -1};   // Args index of coarse bitmaps
   bool pipe = false;            // base columns double-buffered through shared memory
   size_t sink_smem = 0;         // dynamic smem used by the sink (before the load stages)
   std::vector<int> col_p;       // Args.p index of each base column
@@ -718,7 +719,17 @@ struct Gen {
       o << "        idx" << pi << "[r] = SCX_NOROW;\n";
       o << "        if ((sel >> r) & 1u) {\n";
       pack_key(pb.key, "r", nullptr, 0, "key", "kin");
-      o << "          if (kin && key < cap && ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u)) idx" << pi << "[r] = 0u;\n";
+      if (coarse_p[pi] >= 0) {
+        // coarse level in shared memory first; the fine bitmap only when set
+        const int sh = pb.table._pad - 1;
+        o << "          if (kin && key < cap) { const u64 cj = key >> " << sh << ";\n";
+        o << "            if ((cbm" << pi << "[cj >> 5] >> (cj & 31)) & 1u) {\n";
+        if (sh == 0) o << "              idx" << pi << "[r] = 0u;\n";
+        else o << "              if ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u) idx" << pi << "[r] = 0u;\n";
+        o << "            }\n          }\n";
+      } else {
+        o << "          if (kin && key < cap && ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u)) idx" << pi << "[r] = 0u;\n";
+      }
       o << "        }\n      }\n";
     } else if (pb.table.kind == SCX_HT_DIRECT) {
       o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
@@ -960,6 +971,24 @@ struct Gen {
       return SCX_EINVAL;
     }
 
+    // coarse membership bitmaps of bitmap probes -> shared memory (once per CTA)
+    {
+      bool any = false;
+      for (int pi = 0; pi < P.n_probes; ++pi) {
+        const scx_probe& pb = P.probe[pi];
+        if (pb.table.kind != SCX_HT_BITMAP || pb.table._pad <= 0 || !pb.table.keys) continue;
+        const int sh = pb.table._pad - 1;
+        const uint64_t cbits = pb.table.cap ? ((pb.table.cap - 1) >> sh) + 1 : 1;
+        const uint64_t nw = (cbits + 31) / 32;
+        if (nw > 8192) { err = "coarse bitmap larger than 32 KB"; return SCX_EINVAL; }
+        coarse_p[pi] = param(pb.table.keys);
+        o << "  __shared__ u32 cbm" << pi << "[" << nw << "];\n";
+        o << "  { const u32* src = (const u32*)a.p[" << coarse_p[pi] << "];\n";
+        o << "    for (int i = tid; i < " << nw << "; i += " << kTPB << ") cbm" << pi << "[i] = __ldg(src + i); }\n";
+        any = true;
+      }
+      if (any) o << "  __syncthreads();\n";
+    }
     if (dyn_smem < sink_smem) dyn_smem = sink_smem;
     if (pipe) {
       dyn_smem = sink_smem + 2 * (size_t)stage_bytes();

@@ -39,6 +39,9 @@ AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
 _GROUP_MAT = os.environ.get("SCX_GROUP_MAT", "1") != "0"
 _SORTED_RANK = os.environ.get("SCX_SORTED_RANK", "1") != "0"
+_COARSE_BITMAPS = os.environ.get("SCX_COARSE", "1") != "0"
+_COARSE_MIN_ROWS = 1 << 22       # big scans only: each CTA stages the coarse bits once
+_COARSE_BITS = 1 << 18           # 32 KB of shared memory per kernel
 _DIRECT_MAX_SPAN = 1 << 28       # direct lookup tables up to 1 GB of u32 rows
 _DENSE_SMEM_BYTES = 48 * 1024     # per-CTA shared-memory group table (keeps 4 CTAs/SM)
 _OPCODE = {"sum": L.AGG_SUM, "count": L.AGG_COUNT, "min": L.AGG_MIN, "max": L.AGG_MAX}
@@ -207,6 +210,18 @@ class BitmapLookup:
 
     unique = False
     table = None
+
+    def coarse(self, shift: int):
+        """Coarse level (bit j = any of fine bits [j << shift, (j+1) << shift)),
+        built once per shift (scx_bitmap_coarsen)."""
+        if not hasattr(self, "_coarse"):
+            self._coarse = {}
+        if shift not in self._coarse:
+            cbits = ((self.lk.cap - 1) >> shift) + 1 if self.lk.cap else 1
+            buf = alloc((cbits + 31) // 32 + 1, np.uint32)
+            L.call("scx_bitmap_coarsen", _ptr(self._bits), self.lk.cap, shift, _ptr(buf), _stream())
+            self._coarse[shift] = buf
+        return self._coarse[shift]
 
     def __init__(self, source, keys: list[str], cols: list[Column], packing: KeyPacking,
                  span: int):
@@ -677,11 +692,23 @@ class _Builder:
         self._keep = []   # tensors that must outlive the launch
         # probes
         P.n_probes = len(v.probes)
+        n_coarse = sum(1 for st in v.probes if st.lookup.lk.kind == L.HT_BITMAP)
         for i, st in enumerate(v.probes):
             pb = P.probe[i]
             pb.kind = st.kind
             pb.key = st.lookup.packing.spec([self.slot[k] for k in st.probe_keys])
             pb.table = st.lookup.lk
+            if (st.lookup.lk.kind == L.HT_BITMAP and _COARSE_BITMAPS
+                    and P.n_rows >= _COARSE_MIN_ROWS):
+                # shared-memory coarse level: <= 32 KB of coarse bits shared by
+                # this kernel's bitmap probes
+                budget = (_COARSE_BITS // n_coarse)
+                shift = 0
+                while ((st.lookup.lk.cap - 1) >> shift) + 1 > budget:
+                    shift += 1
+                cb = st.lookup.coarse(shift)
+                pb.table.keys = cb.data_ptr()
+                pb.table._pad = shift + 1
             used = [n for n in st.payload if n in self.slot]
             if len(used) > L.MAX_PAYLOAD:
                 raise SchemaError("too many payload columns from one join")

@@ -248,3 +248,25 @@ def test_group_having(dense_keys):
     sx = exp["sx"][1]
     exp = O.filter_(exp, (sx >= 300) & (sx <= 400))
     assert_table_matches(got, O.to_jsonable(exp), f"having dense={dense_keys}")
+
+
+@pytest.mark.parametrize("how", ["semi", "anti"])
+@pytest.mark.parametrize("frac", [0.001, 0.3])
+def test_bitmap_semi_join_big_probe(how, frac):
+    """Semi / anti joins of a >4M-row probe side against a bitmap build: the
+    kernel prefilters with a coarse bitmap staged in shared memory
+    (scx_bitmap_coarsen) and must still equal np.isin (relops.py:73-76)."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(5)
+    n, dom = 5_000_000, 20_000_000
+    k = rng.integers(1, dom + 1, size=n)
+    v = rng.integers(0, 100, size=n)
+    build = np.unique(rng.integers(1, dom + 1, size=int(dom * frac)))
+    left = ColumnTable({"k": Column.from_numpy("int64", k), "v": Column.from_numpy("int64", v)})
+    right = ColumnTable({"b": Column.from_numpy("int64", build)})
+    got = _dev().local_hash_join(left, right, [("k", "b")], how).materialize()
+    keep = np.isin(k, build)
+    if how == "anti":
+        keep = ~keep
+    assert np.array_equal(got.column("k").values.astype(np.int64), k[keep])
+    assert np.array_equal(got.column("v").values.astype(np.int64), v[keep])

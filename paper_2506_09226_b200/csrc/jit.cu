@@ -400,6 +400,17 @@ struct Gen {
 
   explicit Gen(const scx_pipeline& p) : P(p) {}
 
+  // Occupancy target for latency-bound kernels (compaction / probe chains /
+  // hash sinks): CTAs per SM requested through __launch_bounds__, with the
+  // per-row register budget of the V choice scaled to match.  SCX_OCC=n
+  // overrides (A/B).
+  int occ_target() const {
+    const char* e = getenv("SCX_OCC");
+    if (e && *e) return atoi(e) < 2 ? 2 : (atoi(e) > 8 ? 8 : atoi(e));
+    return 2;
+  }
+  int reg_budget() const { return 128 / occ_target(); }
+
   int param(uint64_t v) {
     ptrs.push_back(v);
     return (int)ptrs.size() - 1;
@@ -840,7 +851,8 @@ struct Gen {
         probe_regs = probe_regs > t ? probe_regs : t;
       }
       probe_regs += P.n_probes;
-      while (V > 4 && V * (row_bytes + payload_bytes) / 4 + V * probe_regs + acc_regs > 64) V /= 2;
+      while (V > 4 && V * (row_bytes + payload_bytes) / 4 + V * probe_regs + acc_regs > reg_budget())
+        V /= 2;
     }
     // load pipeline: each thread copies (cp.async) its chunk of the NEXT tile's
     // base columns into shared memory while it processes this one, so a
@@ -880,7 +892,8 @@ struct Gen {
 
     // private-accumulator group-bys are latency bound at 2 CTAs/SM: ask for 3
     // when their shared memory allows it (the register cap becomes 85)
-    const int min_blocks = (dense_priv && (size_t)NC * NW * kTPB * 8 <= 72 * 1024) ? 3 : 2;
+    const int min_blocks = occ_target() > 2 ? occ_target()
+                         : (dense_priv && (size_t)NC * NW * kTPB * 8 <= 72 * 1024) ? 3 : 2;
     o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << min_blocks
       << ") KNAME(const __grid_constant__ Args a) {\n";
     o << "  constexpr int V = " << V << ";\n";

@@ -1308,6 +1308,11 @@ def _i128(lohi) -> int:
     return (int(lohi[1]) << 64) + lo
 
 
+def _lazy_col(kind, values, dictionary=None) -> Column:
+    """Host-backed (lazily uploaded) result column of a final aggregation."""
+    return Column.from_host_lazy(HostColumn.from_reference(kind, np.asarray(values), dictionary))
+
+
 def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, count_m) -> ColumnTable:
     """Assemble the (tiny) dense-aggregate result from exact 128-bit cells.
 
@@ -1331,38 +1336,38 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
         if luts[i] is not None:
             inv = {r: code for code, r in enumerate(luts[i])}
             codes = np.asarray([inv[r] for r in ranks], dtype=np.int64)
-            out[k] = Column.from_numpy("dict", codes, c.dictionary)
+            out[k] = _lazy_col("dict", codes, c.dictionary)
         else:
-            out[k] = Column.from_numpy(c.kind, np.asarray([c.lo + r for r in ranks], dtype=np.int64))
+            out[k] = _lazy_col(c.kind, np.asarray([c.lo + r for r in ranks], dtype=np.int64))
     for a in plan:
         col = [vals[c][a.m] for c in live]
         if a.op == "count":
-            out[a.out] = Column.from_numpy("int64", np.asarray(col, dtype=np.int64))
+            out[a.out] = _lazy_col("int64", np.asarray(col, dtype=np.int64))
         elif a.op in ("min", "max"):
             if a.kind == "float64":
-                out[a.out] = Column.from_host(HostColumn.decimal(np.asarray(col, dtype=np.int64),
+                out[a.out] = Column.from_host_lazy(HostColumn.decimal(np.asarray(col, dtype=np.int64),
                                                                  a.scale))
             else:
-                out[a.out] = Column.from_numpy(a.kind, np.asarray(col, dtype=np.int64))
+                out[a.out] = _lazy_col(a.kind, np.asarray(col, dtype=np.int64))
         elif a.op == "sum":
             if a.kind == "float64":
                 k = decimal_exponent(a.q)
                 if k >= 0 and all(abs(x) < (1 << 62) for x in col):
                     # stays an exact fixed-point decimal (value = int / 10^k)
-                    out[a.out] = Column.from_host(
+                    out[a.out] = Column.from_host_lazy(
                         HostColumn.decimal(np.asarray(col, dtype=np.int64), k))
                 else:
                     arr = np.asarray([float(Fraction(x, a.q)) for x in col], dtype=np.float64)
-                    out[a.out] = Column.from_host(HostColumn("float64", arr, -1))
+                    out[a.out] = Column.from_host_lazy(HostColumn("float64", arr, -1))
             else:
                 if a.q != 1:
                     raise SchemaError("integer sum with fractional coefficients")
-                out[a.out] = Column.from_numpy("int64", np.asarray(col, dtype=np.int64))
+                out[a.out] = _lazy_col("int64", np.asarray(col, dtype=np.int64))
         else:  # avg
             cnts = [vals[c][a.cnt] for c in live]
             arr = np.asarray([float(Fraction(x, a.q * max(n, 1))) for x, n in zip(col, cnts)],
                              dtype=np.float64)
-            out[a.out] = Column.from_numpy("float64", arr)
+            out[a.out] = _lazy_col("float64", arr)
     # keys first, then aggregates (relops.py:121,131-158)
     return ColumnTable(out, tuple(keys))
 

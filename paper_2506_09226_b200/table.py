@@ -277,7 +277,7 @@ class Column:
     ``scale`` the fixed-point exponent of float64 columns.
     """
 
-    __slots__ = ("kind", "data", "scale", "dictionary", "lo", "hi", "dense", "sorted")
+    __slots__ = ("kind", "_data", "_host", "scale", "dictionary", "lo", "hi", "dense", "sorted")
 
     def __init__(self, kind: str, data, scale: int = 0, dictionary=None, lo: int = 0,
                  hi: int = -1, dense: bool = False):
@@ -288,7 +288,8 @@ class Column:
         if kind != "dict" and dictionary is not None:
             raise SchemaError(f"{kind} column must not carry a dictionary")
         self.kind = kind
-        self.data = data
+        self._data = data
+        self._host = None      # host copy of a small result column (uploaded lazily)
         self.scale = scale
         self.dictionary = tuple(dictionary) if dictionary is not None else None
         self.lo = lo
@@ -300,7 +301,34 @@ class Column:
         # it on the device when a group-by could use dense ranks)
         self.sorted = True if dense else None
 
+    @property
+    def data(self):
+        """Device tensor (uploaded on first use for host-backed result columns)."""
+        if self._data is None:
+            torch = _torch()
+            n = len(self._host)
+            buf = alloc(n, self._host.dtype)
+            if n:
+                buf.copy_(torch.from_numpy(np.ascontiguousarray(self._host)), non_blocking=False)
+            self._data = buf
+        return self._data
+
+    @data.setter
+    def data(self, v):
+        self._data = v
+        self._host = None
+
     # ---- construction ----
+    @staticmethod
+    def from_host_lazy(hc: HostColumn) -> "Column":
+        """A small (final-aggregation) result column that stays on the host
+        until a kernel needs it: no H2D copy (and no D2H later) for results
+        that are only read back."""
+        c = Column(hc.kind, None, hc.scale, hc.dictionary, hc.lo, hc.hi,
+                   hc.dense and hc.row_count == hc.hi - hc.lo + 1)
+        c._host = np.ascontiguousarray(hc.values)
+        return c
+
     @staticmethod
     def from_host(hc: HostColumn, device=None) -> "Column":
         torch = _torch()
@@ -321,7 +349,9 @@ class Column:
     # ---- properties ----
     @property
     def np_dtype(self) -> np.dtype:
-        return np.dtype(str(self.data.dtype).replace("torch.", ""))
+        if self._data is None:
+            return self._host.dtype
+        return np.dtype(str(self._data.dtype).replace("torch.", ""))
 
     @property
     def scx_dtype(self) -> int:
@@ -329,7 +359,9 @@ class Column:
 
     @property
     def row_count(self) -> int:
-        return int(self.data.shape[0])
+        if self._data is None:
+            return len(self._host)
+        return int(self._data.shape[0])
 
     def __len__(self) -> int:
         return self.row_count
@@ -340,7 +372,9 @@ class Column:
 
     @property
     def itemsize(self) -> int:
-        return self.data.element_size()
+        if self._data is None:
+            return self._host.dtype.itemsize
+        return self._data.element_size()
 
     @property
     def is_fixed(self) -> bool:
@@ -356,6 +390,8 @@ class Column:
     # ---- host views (D2H; inspection / result decoding) ----
     def host(self) -> np.ndarray:
         """Physical values on the host."""
+        if self._host is not None:
+            return self._host
         return self.data.cpu().numpy()
 
     @property

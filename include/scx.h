@@ -335,6 +335,19 @@ int scx_sorted_rank(const scx_column* key, int64_t n, int64_t lo, uint32_t* rank
 int scx_bitmap_coarsen(const uint32_t* fine_dev, int64_t nbits, int shift, uint32_t* coarse_dev,
                        void* stream);
 
+/* Top-k support (ColumnTable.sort_by(...).head(k), table.py:179-214):
+ * scx_range_hist counts keys in [lo, hi) by the 8-bit digit ((key - lo) >>
+ * shift) & 255 into counts_dev[256] (zeroed here); scx_select_below writes the
+ * (key, row) pairs with key < T in row order (stable) and their number.  A
+ * radix select narrows [lo, hi) until few rows lie below the k-th key, which
+ * are then sorted instead of the whole input.  temp_dev sized by
+ * scx_select_below_workspace(n). */
+int scx_range_hist(const uint64_t* keys_dev, int64_t n, uint64_t lo, uint64_t hi, int shift,
+                   uint32_t* counts_dev, void* stream);
+int64_t scx_select_below_workspace(int64_t n);
+int scx_select_below(const uint64_t* keys_dev, int64_t n, uint64_t T, uint64_t* out_keys_dev,
+                     uint32_t* out_idx_dev, uint64_t* count_dev, void* temp_dev, void* stream);
+
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not
  * fit (group_aggregate output, relops.py:138-158). */

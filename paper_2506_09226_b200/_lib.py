@@ -125,6 +125,9 @@ _PROTOS = {
     "scx_direct_agg_compact_having": (C.c_int, [_vp, i64, C.c_int, C.c_int, C.c_int, i64, i64,
                                                 _vp, _vp, _vp, _vp, _vp]),
     "scx_bitmap_coarsen": (C.c_int, [_vp, i64, C.c_int, _vp, _vp]),
+    "scx_range_hist": (C.c_int, [_vp, i64, u64, u64, C.c_int, _vp, _vp]),
+    "scx_select_below_workspace": (i64, [i64]),
+    "scx_select_below": (C.c_int, [_vp, i64, u64, _vp, _vp, _vp, _vp, _vp]),
     "scx_direct_agg_compact_counted": (C.c_int, [_vp, i64, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                                  _vp]),
     "scx_unpack_key": (C.c_int, [_vp, i64, C.c_int, u64, i64, Column_, _vp]),

@@ -242,6 +242,47 @@ __global__ void copy_pairs_kernel(const uint64_t* ki, const uint32_t* vi, uint64
   }
 }
 
+// ---- small inputs: one CTA, bitonic sort in shared memory -------------------
+// Final ORDER BYs and top-k inputs are usually a few hundred rows; the LSD
+// radix path would spend 5 launches per 8-bit digit on them.  Stability: ties
+// are broken by input position (not by the value payload), so a multi-word
+// LSD sort that feeds a previous pass's permutation as values stays stable.
+constexpr int kSmallSort = 2048;
+
+__global__ void __launch_bounds__(1024) small_sort_kernel(const uint64_t* kin, const uint32_t* vin,
+                                                          uint64_t* kout, uint32_t* vout, int n) {
+  __shared__ uint64_t k[kSmallSort];
+  __shared__ uint32_t v[kSmallSort];
+  __shared__ uint16_t p[kSmallSort];
+  for (int i = threadIdx.x; i < kSmallSort; i += blockDim.x) {
+    const bool in = i < n;
+    k[i] = in ? kin[i] : ~0ull;
+    v[i] = in ? vin[i] : 0u;
+    p[i] = (uint16_t)i;               // padding sorts last: key max, position >= n
+  }
+  __syncthreads();
+  for (int size = 2; size <= kSmallSort; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int t = threadIdx.x; t < kSmallSort / 2; t += blockDim.x) {
+        const int lo = 2 * t - (t & (stride - 1));
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const bool gt = k[lo] > k[hi] || (k[lo] == k[hi] && p[lo] > p[hi]);
+        if (gt == up) {
+          const uint64_t tk = k[lo]; k[lo] = k[hi]; k[hi] = tk;
+          const uint32_t tv = v[lo]; v[lo] = v[hi]; v[hi] = tv;
+          const uint16_t tp = p[lo]; p[lo] = p[hi]; p[hi] = tp;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    kout[i] = k[i];
+    vout[i] = v[i];
+  }
+}
+
 static int64_t nblocks_for(int64_t n) { return (n + kChunk - 1) / kChunk; }
 
 int scan_u32_excl(const uint32_t* in, uint64_t* out, int64_t m, uint64_t* tmp, cudaStream_t st);
@@ -286,6 +327,11 @@ extern "C" int scx_sort_pairs(const uint64_t* kin, const uint32_t* vin, uint64_t
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int passes = (n_bits + 7) / 8;
+  if (passes > 1 && n <= kSmallSort) {
+    small_sort_kernel<<<1, 1024, 0, st>>>(kin, vin, kout, vout, (int)n);
+    SCX_CHECK_LAUNCH("small_sort_kernel");
+    return SCX_OK;
+  }
   if (passes == 0) {
     copy_pairs_kernel<<<grid_for(n, 256, 2368), 256, 0, st>>>(kin, vin, kout, vout, n);
     SCX_CHECK_LAUNCH("copy_pairs_kernel");

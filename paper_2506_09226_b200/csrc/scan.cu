@@ -278,9 +278,99 @@ __global__ void rank_write_kernel(scx_column c, int64_t n, int64_t lo, const uin
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kBlock - 1) *count = part[gridDim.x];
 }
 
+// ---- top-k support: digit histogram of keys in a range, stable select-below --
+__global__ void range_hist_kernel(const uint64_t* keys, int64_t n, uint64_t lo, uint64_t hi,
+                                  int shift, uint32_t* counts) {
+  __shared__ uint32_t h[256];
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) h[d] = 0;
+  __syncthreads();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    if (k >= lo && k < hi) atomicAdd(&h[((k - lo) >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += blockDim.x)
+    if (h[d]) atomicAdd(&counts[d], h[d]);
+}
+
+__global__ void below_count_kernel(const uint64_t* keys, int64_t n, uint64_t T, uint64_t* part) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) s += (base + i < n && keys[base + i] < T);
+  uint32_t excl;
+  const uint32_t tot = block_excl_scan(s, excl);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void below_write_kernel(const uint64_t* keys, int64_t n, uint64_t T, const uint64_t* part,
+                                   uint64_t* out_keys, uint32_t* out_idx, uint64_t* count) {
+  const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+  uint32_t f[kScanItems];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    f[i] = base + i < n && keys[base + i] < T;
+    s += f[i];
+  }
+  uint32_t excl;
+  block_excl_scan(s, excl);
+  uint64_t o = part[blockIdx.x] + excl;
+#pragma unroll
+  for (int i = 0; i < kScanItems; ++i) {
+    if (f[i]) {
+      out_keys[o] = keys[base + i];
+      out_idx[o] = (uint32_t)(base + i);
+      ++o;
+    }
+  }
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kBlock - 1) *count = part[gridDim.x];
+}
+
 }  // namespace scx
 
 using namespace scx;
+
+extern "C" int scx_range_hist(const uint64_t* keys, int64_t n, uint64_t lo, uint64_t hi, int shift,
+                              uint32_t* counts, void* stream) {
+  if (!keys || !counts || n < 0 || shift < 0 || shift > 63) {
+    set_error("range_hist: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCX_CUDA(cudaMemsetAsync(counts, 0, 256 * sizeof(uint32_t), st));
+  if (n == 0) return SCX_OK;
+  range_hist_kernel<<<grid_for(n, 256, 1184), 256, 0, st>>>(keys, n, lo, hi, shift, counts);
+  SCX_CHECK_LAUNCH("range_hist_kernel");
+  return SCX_OK;
+}
+
+extern "C" int64_t scx_select_below_workspace(int64_t n) { return 8 * scan_tmp_words(n); }
+
+extern "C" int scx_select_below(const uint64_t* keys, int64_t n, uint64_t T, uint64_t* out_keys,
+                                uint32_t* out_idx, uint64_t* count, void* temp, void* stream) {
+  if (!keys || !out_keys || !out_idx || !count || (n > 0 && !temp) || n < 0 ||
+      n > (int64_t)0xFFFFFFFFll) {
+    set_error("select_below: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) {
+    SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
+    return SCX_OK;
+  }
+  const int64_t nb = (n + kScanTile - 1) / kScanTile;
+  if (nb > 1024 * 64) { set_error("select_below: input too long"); return SCX_EUNSUPPORTED; }
+  uint64_t* part = static_cast<uint64_t*>(temp);
+  below_count_kernel<<<(int)nb, kBlock, 0, st>>>(keys, n, T, part);
+  SCX_CHECK_LAUNCH("below_count_kernel");
+  small_scan_kernel<<<1, 1024, 0, st>>>(part, nb);
+  SCX_CHECK_LAUNCH("small_scan_kernel");
+  below_write_kernel<<<(int)nb, kBlock, 0, st>>>(keys, n, T, part, out_keys, out_idx, count);
+  SCX_CHECK_LAUNCH("below_write_kernel");
+  return SCX_OK;
+}
 
 extern "C" int64_t scx_sorted_rank_workspace(int64_t n) { return 8 * scan_tmp_words(n); }
 

@@ -336,6 +336,21 @@ class DeviceContext:
 # data placement
 # ---------------------------------------------------------------------------
 
+def reserve_device_pool(nbytes: int) -> int:
+    """Grow the caching allocator's pool by one segment of `nbytes` up front
+    (allocate + free): later intermediates are carved from it instead of
+    cudaMalloc'ing new multi-GB segments mid-query (a 25-30 ms stall seen
+    once in a timed pass).  Returns the bytes reserved (0 if it did not fit)."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    nbytes = min(int(nbytes), max(0, free - (8 << 30)))
+    if nbytes <= 0:
+        return 0
+    blk = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    del blk
+    return nbytes
+
+
 def upload_tables_async(host: dict, order=None, stream=None):
     """Upload pinned host columns on a copy stream, table by table in `order`
     (first use first), without blocking the compute stream.

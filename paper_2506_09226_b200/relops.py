@@ -372,6 +372,9 @@ class TableView:
     def head(self, n: int) -> ColumnTable:
         return self.materialize().head(n)
 
+    def top(self, names, descending, n: int) -> ColumnTable:
+        return sort_table(self.materialize(), names, descending or set(), limit=n)
+
     def __repr__(self) -> str:
         return (f"TableView(base_rows={self.base.row_count}, visible={self.visible}, "
                 f"probes={len(self.probes)})")
@@ -1608,12 +1611,23 @@ def _rank_tensor(dictionary):
     return t
 
 
-def sort_table(t, names: list[str], descending: set[str]) -> ColumnTable:
-    """Stable multi-key sort (table.py:198-214): LSD over packed 64-bit words."""
+_TOPK_SMALL = 2048          # candidates sorted by the single-CTA sort
+
+
+def sort_table(t, names: list[str], descending: set[str], limit: int | None = None) -> ColumnTable:
+    """Stable multi-key sort (table.py:198-214): LSD over packed 64-bit words.
+
+    ``limit=k`` returns only the first k rows (sort_by(...).head(k)): when the
+    key fits one 64-bit word, a radix select (scx_range_hist, one 8-bit digit
+    per round) finds a threshold below which only a few rows lie; those are
+    compacted in row order (scx_select_below) and sorted, not the whole input.
+    """
     t = t.materialize() if isinstance(t, TableView) else t
     n = t.row_count
+    if limit is not None and limit <= 0:
+        return t.head(0)
     if n <= 1 or not names:
-        return t
+        return t if limit is None else t.head(limit)
     specs = []
     for name in names:
         c = t.column(name)
@@ -1636,6 +1650,15 @@ def sort_table(t, names: list[str], descending: set[str]) -> ColumnTable:
         used += sp[2]
     if cur:
         words.append(cur)
+    if limit is not None and len(words) == 1 and n > max(_TOPK_SMALL, 4 * limit):
+        word = words[0]
+        nbits = max(sh + sp[2] for sp, sh in word)
+        key = alloc(n, np.uint64)
+        for i, ((c, lo, bits, desc, lut), sh) in enumerate(word):
+            L.call("scx_encode_sort_key", c.scx(), None, n, lo, bits, desc, sh,
+                   _ptr(lut) if lut is not None else None, _ptr(key), 1 if i else 0, _stream())
+        perm = _topk_perm(key, n, nbits, limit)
+        return take_table(t, perm)
     perm = None
     for word in words:
         nbits = max(sh + sp[2] for sp, sh in word)
@@ -1646,8 +1669,37 @@ def sort_table(t, names: list[str], descending: set[str]) -> ColumnTable:
                    1 if i else 0, _stream())
         _, perm = sort_pairs(key, perm, nbits)
     if perm is None:
-        return t
-    return take_table(t, perm)
+        return t if limit is None else t.head(limit)
+    out = take_table(t, perm)
+    return out if limit is None else out.head(limit)
+
+
+def _topk_perm(key, n: int, nbits: int, k: int):
+    """Rows of the k smallest keys (ties in row order), in key order."""
+    counts = alloc(256, np.uint32)
+    lo, hi = 0, 1 << nbits              # the k-th key lies in [lo, hi)
+    below = 0                           # rows with key < lo
+    shift = nbits
+    while shift > 0:
+        shift = max(shift - 8, 0)
+        L.call("scx_range_hist", _ptr(key), n, lo, hi, shift, _ptr(counts), _stream())
+        h = _to_host(counts).astype(np.int64)
+        cum = below + np.cumsum(h)
+        d = int(np.searchsorted(cum, k))          # first digit reaching k rows
+        below_d = int(cum[d - 1]) if d else below
+        lo, hi = lo + (d << shift), lo + ((d + 1) << shift)
+        below = below_d
+        if below + int(h[d]) <= _TOPK_SMALL:
+            break
+    # every row with key < hi: the k smallest are among them
+    m_cap = n
+    ok, oi = alloc(m_cap, np.uint64), alloc(m_cap, np.uint32)
+    cnt = alloc(2, np.int64)
+    ws = alloc(max(2, L.load().scx_select_below_workspace(n) // 8), np.int64)
+    L.call("scx_select_below", _ptr(key), n, hi, _ptr(ok), _ptr(oi), _ptr(cnt), _ptr(ws), _stream())
+    m = int(_to_host(cnt)[0])
+    _, perm = sort_pairs(ok[:m], oi[:m], nbits)
+    return perm[:k]
 
 
 def take_column(c: Column, idx) -> Column:

@@ -497,6 +497,12 @@ class ColumnTable:
         from . import relops
         return relops.sort_table(self, names, descending or set())
 
+    def top(self, names: list[str], descending: set[str] | None, n: int) -> "ColumnTable":
+        """sort_by(names, descending).head(n) without sorting the whole table
+        (extension; same rows in the same order)."""
+        from . import relops
+        return relops.sort_table(self, names, descending or set(), limit=n)
+
     def decode_rows(self) -> list[tuple]:
         cols = [c.decoded() for c in self._columns.values()]
         return [tuple(col[i] for col in cols) for i in range(self._rows)]

@@ -193,7 +193,7 @@ def test_radix_sort_large_and_edge_cases():
     import torch
     from paper_2506_09226_b200.table import Column, ColumnTable
     rng = np.random.default_rng(3)
-    for n in (0, 1, 5, 4097, 300_000):
+    for n in (0, 1, 5, 700, 2048, 2049, 4097, 300_000):
         a = rng.integers(-1000, 1000, size=n)
         b = rng.integers(0, 3, size=n)
         t = ColumnTable({"a": Column.from_numpy("int64", a), "b": Column.from_numpy("int64", b)})
@@ -201,6 +201,18 @@ def test_radix_sort_large_and_edge_cases():
         idx = np.lexsort([-a, b]) if n else np.arange(0)
         assert np.array_equal(s.column("a").values, a[idx])
         assert np.array_equal(s.column("b").values, b[idx])
+    # keys wider than 64 bits: two LSD words, each pass must keep the order
+    # of the previous one for ties (small single-CTA sort and radix path)
+    for n in (1500, 6000):
+        c = rng.integers(0, 4, size=n)
+        d = rng.integers(-(1 << 40), 1 << 40, size=n) // (1 << 38) * (1 << 38)   # many ties
+        e = rng.integers(-(1 << 40), 1 << 40, size=n)
+        t = ColumnTable({"c": Column.from_numpy("int64", c), "d": Column.from_numpy("int64", d),
+                         "e": Column.from_numpy("int64", e)})
+        s = t.sort_by(["c", "d", "e"], {"d"})
+        idx = np.lexsort([e, -d, c])
+        for name, ref in (("c", c), ("d", d), ("e", e)):
+            assert np.array_equal(s.column(name).values, ref[idx]), (n, name)
 
 
 @pytest.mark.parametrize("layout", ["sorted_sparse", "unsorted_sparse", "sorted_filtered"])
@@ -270,3 +282,19 @@ def test_bitmap_semi_join_big_probe(how, frac):
         keep = ~keep
     assert np.array_equal(got.column("k").values.astype(np.int64), k[keep])
     assert np.array_equal(got.column("v").values.astype(np.int64), v[keep])
+
+
+@pytest.mark.parametrize("k", [1, 10, 100, 3000])
+def test_top_k_equals_sort_head(k):
+    """ColumnTable.top (radix select + sort of the candidates) == sort_by().head(k),
+    ties kept in input order (table.py:198-214 stable lexsort)."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(17)
+    n = 200_000
+    a = rng.integers(0, 5000, size=n)           # many ties on the leading key
+    b = rng.integers(-50, 50, size=n)
+    t = ColumnTable({"a": Column.from_numpy("int64", a), "b": Column.from_numpy("int64", b)})
+    got = t.top(["a", "b"], {"a"}, k)
+    idx = np.lexsort([b, -a])[:k]
+    assert np.array_equal(got.column("a").values, a[idx])
+    assert np.array_equal(got.column("b").values, b[idx])

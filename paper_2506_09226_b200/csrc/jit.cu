@@ -304,6 +304,11 @@ static __device__ __forceinline__ void cpa8(u32 dst, const void* src) {
 static __device__ __forceinline__ void cpa4(u32 dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" :: "r"(dst), "l"(src) : "memory");
 }
+// bulk L2 prefetch (no shared memory, no registers): one instruction pulls a
+// whole column chunk of a later tile into L2 while this tile is processed
+static __device__ __forceinline__ void l2_prefetch(const void* p, u32 bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
 static __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 static __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 static __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -413,6 +418,12 @@ struct Gen {
     return 3;
   }
   int reg_budget() const { return 128 / occ_target(); }
+  // tiles of L2 bulk prefetch ahead of the current one (SCX_PREFETCH=n, 0 = off)
+  int prefetch_tiles() const {
+    const char* e = getenv("SCX_PREFETCH");
+    if (e && *e) return atoi(e) < 0 ? 0 : (atoi(e) > 4 ? 4 : atoi(e));
+    return 0;
+  }
 
   int param(uint64_t v) {
     ptrs.push_back(v);
@@ -1024,6 +1035,21 @@ struct Gen {
       o << "  for (i64 tile = tbeg; tile < tend; ++tile) {\n";
     } else {
       o << "  for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n";
+    }
+    if (prefetch_tiles() > 0 && !pipe && P.n_base > 0) {
+      // threads 0..n_base-1 each prefetch one column's chunk of the tile
+      // prefetch_tiles() iterations ahead (full tiles only)
+      const bool cmp = S.kind == SCX_SINK_COMPACT;
+      o << "    if (tid < " << P.n_base << ") {\n";
+      o << "      const i64 pt = tile + " << prefetch_tiles() << " * " << (cmp ? "1ll" : "(i64)gridDim.x") << ";\n";
+      o << "      if ((pt + 1) * " << tile_rows << "ll <= n" << (cmp ? " && pt < tend" : "") << ") {\n";
+      o << "        const char* cp = nullptr; u32 cb = 0;\n";
+      for (int c = 0; c < P.n_base; ++c) {
+        const int w = dtype_size(P.base[c].dtype);
+        o << "        if (tid == " << c << ") { cp = (const char*)a.p[" << col_p[c] << "] + pt * "
+          << tile_rows * w << "ll; cb = " << tile_rows * w << "u; }\n";
+      }
+      o << "        l2_prefetch(cp, cb);\n      }\n    }\n";
     }
     o << "    const i64 row0 = (tile * " << kTPB << " + tid) * (i64)V;\n";
     o << "    const bool full = row0 + V <= n;\n";

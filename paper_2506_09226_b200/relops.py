@@ -967,11 +967,21 @@ class _Agg:
     src: Column | None = None
 
 
+_LUT_CACHE: dict = {}
+
+
 def _rank_lut(dictionary) -> list[int]:
+    """code -> rank of its string (dict keys sort by string); cached per
+    dictionary object (an argsort of the strings per call is host time)."""
+    hit = _LUT_CACHE.get(id(dictionary))
+    if hit is not None and hit[0] is dictionary:
+        return hit[1]
     order = np.argsort(np.asarray(dictionary, dtype=object), kind="stable")
     rank = np.empty(len(dictionary), dtype=np.int64)
     rank[order] = np.arange(len(dictionary))
-    return [int(x) for x in rank]
+    lut = [int(x) for x in rank]
+    _LUT_CACHE[id(dictionary)] = (dictionary, lut)
+    return lut
 
 
 def _plan_aggs(v: TableView, aggs: dict) -> tuple[list[_Agg], list[tuple[str, IntMeasure | None]]]:
@@ -1288,13 +1298,14 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
             S.glut[i] = -1
             luts.append(None)
     M = len(measures)
-    init = np.zeros((cells, M, 2), dtype=np.int64)
-    for j, (op, _) in enumerate(measures):
-        if op == "min":
-            init[:, j, 0] = INT64_MAX
-        elif op == "max":
-            init[:, j, 0] = INT64_MIN
-    acc = torch.from_numpy(init).to(_device())
+    # (cells, M, 2) int64 accumulators initialised on the device (a pageable
+    # H2D copy here would synchronise the stream)
+    pattern = []
+    for op, _ in measures:
+        pattern += [INT64_MAX if op == "min" else (INT64_MIN if op == "max" else 0), 0]
+    acc = alloc(cells * M * 2, np.int64)
+    L.call("scx_fill_rows", _ptr(acc), cells, 2 * M, (C.c_int64 * (2 * M))(*pattern), _stream())
+    acc = acc.view(cells, M, 2)
     S.acc = acc.data_ptr()
     b.run(timing)
     if cross is not None and cross.ep.n > 1:
@@ -1504,10 +1515,7 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) 
             ranks = alloc(G, np.uint32)
             L.call("scx_unpack_key", _ptr(skeys), G, shifts[i], mask, 0,
                    L.Column_(ranks.data_ptr(), L.SCX_U32, 0), _stream())
-            inv = np.empty(len(luts[i]), dtype=c.np_dtype)
-            for code, r in enumerate(luts[i]):
-                inv[r] = code
-            inv_t = torch.from_numpy(inv).to(_device())
+            inv_t = _inv_rank_tensor(c.dictionary, luts[i], c.np_dtype)
             data = alloc(G, c.np_dtype)
             L.call("scx_gather", L.Column_(inv_t.data_ptr(), c.scx_dtype, 0), _ptr(ranks), G,
                    L.Column_(data.data_ptr(), c.scx_dtype, 0), _stream())
@@ -1592,8 +1600,8 @@ def sort_pairs(keys, vals, n_bits: int):
 def _col_range(c: Column) -> tuple[int, int]:
     if c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo:
         return c.lo, c.hi
-    torch = _torch()
-    mm = torch.from_numpy(np.asarray([INT64_MAX, INT64_MIN], dtype=np.int64)).to(c.data.device)
+    mm = alloc(2, np.int64)
+    L.call("scx_fill_rows", _ptr(mm), 1, 2, (C.c_int64 * 2)(INT64_MAX, INT64_MIN), _stream())
     L.call("scx_minmax", c.scx(), c.row_count, _ptr(mm), _stream())
     lo, hi = (int(x) for x in _to_host(mm))
     return lo, hi
@@ -1603,12 +1611,29 @@ _RANK_CACHE: dict = {}
 
 
 def _rank_tensor(dictionary):
-    key = (dictionary, _torch().cuda.current_device())
-    t = _RANK_CACHE.get(key)
-    if t is None:
+    # keyed by identity (dictionaries are shared canonical tuples; hashing a
+    # large one per call is not free) -- the entry keeps the tuple alive
+    key = (id(dictionary), _torch().cuda.current_device())
+    hit = _RANK_CACHE.get(key)
+    if hit is None or hit[0] is not dictionary:
         t = _torch().from_numpy(np.asarray(_rank_lut(dictionary), dtype=np.int32)).to(_device())
-        _RANK_CACHE[key] = t
-    return t
+        hit = _RANK_CACHE[key] = (dictionary, t)
+    return hit[1]
+
+
+_INV_CACHE: dict = {}
+
+
+def _inv_rank_tensor(dictionary, lut, np_dtype):
+    """rank -> dictionary code, on the device, cached per dictionary."""
+    key = (id(dictionary), np.dtype(np_dtype).str, _torch().cuda.current_device())
+    hit = _INV_CACHE.get(key)
+    if hit is None or hit[0] is not dictionary:
+        inv = np.empty(len(lut), dtype=np_dtype)
+        for code, r in enumerate(lut):
+            inv[r] = code
+        hit = _INV_CACHE[key] = (dictionary, _torch().from_numpy(inv).to(_device()))
+    return hit[1]
 
 
 _TOPK_SMALL = 2048          # candidates sorted by the single-CTA sort

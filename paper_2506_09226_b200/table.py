@@ -243,6 +243,7 @@ def _torch():
 
 
 _TORCH_DTYPE = None
+_NP_OF_TORCH: dict = {}
 
 
 def torch_dtype(np_dtype: np.dtype):
@@ -351,7 +352,11 @@ class Column:
     def np_dtype(self) -> np.dtype:
         if self._data is None:
             return self._host.dtype
-        return np.dtype(str(self._data.dtype).replace("torch.", ""))
+        td = self._data.dtype
+        nd = _NP_OF_TORCH.get(td)
+        if nd is None:
+            nd = _NP_OF_TORCH[td] = np.dtype(str(td).replace("torch.", ""))
+        return nd
 
     @property
     def scx_dtype(self) -> int:

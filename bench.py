@@ -31,6 +31,10 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# grow the caching allocator by remapping one expandable segment instead of
+# cudaMalloc'ing new multi-GB segments (a new segment inside a timed pass cost
+# 30-130 ms in Q21); must be set before torch initialises CUDA
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 sys.path.insert(0, ROOT)
 
 METRIC = "TPC-H 22-query total time (s) at SF100, 1/2/4/8 B200; shuffle GB/s vs NVLink"

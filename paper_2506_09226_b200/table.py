@@ -336,7 +336,8 @@ class Column:
         n = hc.row_count
         buf = alloc(n, hc.values.dtype, device)
         if n:
-            src = torch.from_numpy(np.ascontiguousarray(hc.values))
+            v = np.ascontiguousarray(hc.values)
+            src = torch.from_numpy(v if v.flags.writeable else v.copy())
             buf.copy_(src, non_blocking=False)
         return Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
                       hc.dense and n == hc.hi - hc.lo + 1)

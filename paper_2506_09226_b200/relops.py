@@ -1328,60 +1328,72 @@ def _lazy_col(kind, values, dictionary=None) -> Column:
 
 
 def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, count_m) -> ColumnTable:
-    """Assemble the (tiny) dense-aggregate result from exact 128-bit cells.
+    """Assemble the (small) dense-aggregate result from exact 128-bit cells.
 
     This is the final-aggregation step (the reference's all-reduced grid ->
-    result table, queries.py:51-69): at most 8 cells x 8 measures of exact
-    integers, turned into result columns and uploaded.
+    result table, queries.py:51-69), vectorised over the live cells; values
+    that do not fit int64 fall back to Python integers.
     """
     minmax = [op in ("min", "max") for op, _ in measures]
     if keys:
         # counts are non-negative and < 2^63: the low word alone decides liveness
-        live = [int(c) for c in np.flatnonzero(acc[:, count_m, 0] > 0)]
+        live = np.flatnonzero(acc[:, count_m, 0] > 0)
     else:
-        live = [0]
-    vals = {c: [int(acc[c, j, 0]) if minmax[j] else _i128(acc[c, j]) for j in range(acc.shape[1])]
-            for c in live}
+        live = np.zeros(1, dtype=np.int64)
+    lo = acc[live, :, 0]
+    fits = acc[live, :, 1] == (lo >> 63)          # the 128-bit value is lo itself
+
+    def exact(j):
+        """int64 array of measure j over the live cells, or a list of ints."""
+        if minmax[j] or bool(fits[:, j].all()):
+            return lo[:, j].copy()
+        return [_i128(acc[c, j]) for c in live]
+
     out: dict[str, Column] = {}
     # decode cell -> per-key rank -> value
     for i, (k, c) in enumerate(zip(keys, kcols)):
         stride = int(np.prod(cards[i + 1:])) if i + 1 < len(cards) else 1
-        ranks = [(cell // stride) % cards[i] for cell in live]
+        ranks = (live // stride) % cards[i]
         if luts[i] is not None:
-            inv = {r: code for code, r in enumerate(luts[i])}
-            codes = np.asarray([inv[r] for r in ranks], dtype=np.int64)
-            out[k] = _lazy_col("dict", codes, c.dictionary)
+            inv = np.empty(len(luts[i]), dtype=np.int64)
+            inv[np.asarray(luts[i], dtype=np.int64)] = np.arange(len(luts[i]))
+            out[k] = Column.from_host_lazy(HostColumn.from_codes(inv[ranks], c.dictionary))
         else:
-            out[k] = _lazy_col(c.kind, np.asarray([c.lo + r for r in ranks], dtype=np.int64))
+            out[k] = Column.from_host_lazy(HostColumn.from_ints(c.kind, (c.lo + ranks).astype(np.int64)))
     for a in plan:
-        col = [vals[c][a.m] for c in live]
+        col = exact(a.m)
         if a.op == "count":
-            out[a.out] = _lazy_col("int64", np.asarray(col, dtype=np.int64))
+            out[a.out] = Column.from_host_lazy(HostColumn.from_ints("int64", np.asarray(col, dtype=np.int64)))
         elif a.op in ("min", "max"):
             if a.kind == "float64":
                 out[a.out] = Column.from_host_lazy(HostColumn.decimal(np.asarray(col, dtype=np.int64),
-                                                                 a.scale))
+                                                                      a.scale))
             else:
-                out[a.out] = _lazy_col(a.kind, np.asarray(col, dtype=np.int64))
+                out[a.out] = Column.from_host_lazy(HostColumn.from_ints(a.kind, np.asarray(col, dtype=np.int64)))
         elif a.op == "sum":
             if a.kind == "float64":
                 k = decimal_exponent(a.q)
-                if k >= 0 and all(abs(x) < (1 << 62) for x in col):
+                small = isinstance(col, np.ndarray) and bool((np.abs(col) < (1 << 62)).all())
+                if k >= 0 and small:
                     # stays an exact fixed-point decimal (value = int / 10^k)
-                    out[a.out] = Column.from_host_lazy(
-                        HostColumn.decimal(np.asarray(col, dtype=np.int64), k))
+                    out[a.out] = Column.from_host_lazy(HostColumn.decimal(col, k))
                 else:
-                    arr = np.asarray([float(Fraction(x, a.q)) for x in col], dtype=np.float64)
+                    arr = np.asarray([float(Fraction(int(x), a.q)) for x in col], dtype=np.float64)
                     out[a.out] = Column.from_host_lazy(HostColumn("float64", arr, -1))
             else:
                 if a.q != 1:
                     raise SchemaError("integer sum with fractional coefficients")
-                out[a.out] = _lazy_col("int64", np.asarray(col, dtype=np.int64))
-        else:  # avg
-            cnts = [vals[c][a.cnt] for c in live]
-            arr = np.asarray([float(Fraction(x, a.q * max(n, 1))) for x, n in zip(col, cnts)],
-                             dtype=np.float64)
-            out[a.out] = _lazy_col("float64", arr)
+                out[a.out] = Column.from_host_lazy(HostColumn.from_ints("int64", np.asarray(col, dtype=np.int64)))
+        else:  # avg = sum / max(count, 1), one correctly rounded division
+            cnts = exact(a.cnt)
+            den_ok = isinstance(cnts, np.ndarray) and bool((cnts < (1 << 40)).all())
+            if (isinstance(col, np.ndarray) and bool((np.abs(col) < (1 << 53)).all()) and den_ok
+                    and a.q * (1 << 40) < (1 << 53)):
+                arr = col.astype(np.float64) / (np.maximum(cnts, 1) * a.q).astype(np.float64)
+            else:
+                arr = np.asarray([float(Fraction(int(x), a.q * max(int(n), 1)))
+                                  for x, n in zip(col, cnts)], dtype=np.float64)
+            out[a.out] = Column.from_host_lazy(HostColumn("float64", arr, -1))
     # keys first, then aggregates (relops.py:121,131-158)
     return ColumnTable(out, tuple(keys))
 

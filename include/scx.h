@@ -348,6 +348,19 @@ int64_t scx_select_below_workspace(int64_t n);
 int scx_select_below(const uint64_t* keys_dev, int64_t n, uint64_t T, uint64_t* out_keys_dev,
                      uint32_t* out_idx_dev, uint64_t* count_dev, void* temp_dev, void* stream);
 
+/* Stream aggregation over a non-decreasing key column (relops.py:97-160 for
+ * clustered input, e.g. lineitem by l_orderkey): each group is aggregated by
+ * the thread holding its first row; no group table.  vals/ops: m plain
+ * columns with SCX_AGG_* (COUNT ignores its column); optional HAVING
+ * hv_lo <= acc[hv] <= hv_hi (hv = -1: none).  Writes *count groups (unordered)
+ * as out_keys[g] (raw key values) and out_acc[j*cap + g]; *overflow = 1 if
+ * more than cap groups qualified.  scx_is_sorted: *bad = #{i: key[i] < key[i-1]}. */
+int scx_is_sorted(const scx_column* col, int64_t n, uint64_t* bad_dev, void* stream);
+int scx_sorted_group_agg(const scx_column* key, const scx_column* vals, const int* ops, int m,
+                         int64_t n, int hv, int64_t hv_lo, int64_t hv_hi, int64_t* out_keys_dev,
+                         int64_t* out_acc_dev, int64_t cap, uint64_t* count_dev,
+                         uint32_t* overflow_dev, void* stream);
+
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not
  * fit (group_aggregate output, relops.py:138-158). */

@@ -278,6 +278,187 @@ __global__ void rank_write_kernel(scx_column c, int64_t n, int64_t lo, const uin
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == kBlock - 1) *count = part[gridDim.x];
 }
 
+// ---- stream aggregation over a sorted key ---------------------------------------
+// Rows of one key are contiguous; the thread holding a group's FIRST row
+// aggregates the whole group (reading past its own rows when the group runs
+// on), so every group is produced exactly once with no table, no atomics on
+// accumulators and no merge pass.  HAVING is applied before the write; the
+// output is compacted with one warp-aggregated atomic (unordered).
+struct SortedAggArgs {
+  scx_column key;
+  scx_column val[SCX_MAX_MEASURES];
+  int op[SCX_MAX_MEASURES];          // SCX_AGG_SUM / COUNT / MIN / MAX
+  int m;
+  int hv;                            // measure index of the HAVING range, -1 = none
+  int64_t hv_lo, hv_hi;
+};
+
+constexpr int kSortedChunk = 4096;      // rows per warp
+constexpr int kSortedUnroll = 4;        // 32-row windows loaded ahead
+
+__device__ __forceinline__ int64_t agg_op(int op, int64_t a, int64_t b) {
+  return op == SCX_AGG_MIN ? (b < a ? b : a) : op == SCX_AGG_MAX ? (b > a ? b : a) : a + b;
+}
+__device__ __forceinline__ int64_t agg_ident(int op) {
+  return op == SCX_AGG_MIN ? INT64_MAX : op == SCX_AGG_MAX ? INT64_MIN : 0;
+}
+
+// Each warp owns kSortedChunk consecutive rows and walks them 32 at a time
+// (coalesced loads): head flags from the neighbouring lane's key, a segmented
+// inclusive warp scan per measure, and the lane that ends a segment emits the
+// group.  A group still open at lane 31 is carried into the next window; rows
+// of the group that began before the chunk belong to the previous warp; the
+// group open at the chunk end is followed past it until its key changes.
+template <int M>
+__device__ __forceinline__ bool having_ok(const SortedAggArgs& A, const int64_t (&x)[M]) {
+  if (A.hv < 0) return true;
+  int64_t h = 0;
+#pragma unroll
+  for (int j = 0; j < M; ++j)
+    if (j == A.hv) h = x[j];
+  return h >= A.hv_lo && h <= A.hv_hi;
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) sorted_agg_kernel(SortedAggArgs A, int64_t n, int64_t* out_keys,
+                                                         int64_t* out_acc, int64_t cap,
+                                                         unsigned long long* count, uint32_t* overflow) {
+  const void* kp = reinterpret_cast<const void*>(A.key.ptr);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t start = warp * kSortedChunk;
+  if (start >= n) return;
+  const int64_t cend = start + kSortedChunk < n ? start + kSortedChunk : n;
+  const bool skip_first = start > 0;
+  const int64_t kfirst_prev = skip_first ? load_i64(kp, A.key.dtype, start - 1) : 0;
+  const int64_t kend = load_i64(kp, A.key.dtype, cend - 1);   // key open at the chunk end
+  bool carry = false;
+  int64_t ckey = 0, cacc[M];
+  int64_t prev_last = kfirst_prev;                            // key of row s-1
+  const uint32_t lt = (1u << lane) - 1u;
+  bool done = false;
+  for (int64_t s0 = start; s0 < n && !done; s0 += 32 * kSortedUnroll) {
+    // loads of kSortedUnroll windows in flight before any is processed
+    int64_t kk[kSortedUnroll], vv[kSortedUnroll][M];
+#pragma unroll
+    for (int u = 0; u < kSortedUnroll; ++u) {
+      const int64_t i = s0 + 32 * u + lane;
+      kk[u] = i < n ? load_i64(kp, A.key.dtype, i) : 0;
+#pragma unroll
+      for (int j = 0; j < M; ++j)
+        vv[u][j] = (i < n && A.op[j] != SCX_AGG_COUNT)
+                       ? load_i64(reinterpret_cast<const void*>(A.val[j].ptr), A.val[j].dtype, i) : 1;
+    }
+#pragma unroll
+  for (int u = 0; u < kSortedUnroll; ++u) {
+    const int64_t s = s0 + 32 * u;
+    if (done || s >= n) { done = true; break; }
+    const int64_t k = kk[u];
+    if (s >= cend) {
+      // past the chunk: only rows continuing the open group remain
+      if (!carry || __shfl_sync(0xffffffffu, k, 0) != ckey) { done = true; break; }
+    }
+    const int64_t i = s + lane;
+    const bool in = i < n;
+    bool act = in && !(skip_first && k == kfirst_prev) && (i < cend || k == kend);
+    int64_t up = __shfl_up_sync(0xffffffffu, k, 1);
+    if (lane == 0) up = prev_last;
+    const bool head_raw = (i == 0) || k != up;
+    // a segment starts at an active row whose predecessor is another key, or
+    // at the first active row of the window that does not continue the carry
+    bool prev_act = __shfl_up_sync(0xffffffffu, act, 1);
+    if (lane == 0) prev_act = carry;
+    bool head = act && (head_raw || !prev_act);
+    // the carry is complete if the window's first row does not continue it
+    const bool cont0 = __shfl_sync(0xffffffffu, act && !head, 0);
+    if (carry && !cont0) {
+      if (lane == 0) {
+        const bool ok = having_ok<M>(A, cacc);
+        if (ok) {
+          const unsigned long long o = atomicAdd(count, 1ull);
+          if ((int64_t)o < cap) {
+            out_keys[o] = ckey;
+            _Pragma("unroll") for (int j = 0; j < M; ++j) out_acc[(int64_t)j * cap + (int64_t)o] = cacc[j];
+          } else {
+            atomicOr(overflow, 1u);
+          }
+        }
+      }
+      carry = false;
+    }
+    int64_t v[M];
+    _Pragma("unroll") for (int j = 0; j < M; ++j) v[j] = act ? vv[u][j] : agg_ident(A.op[j]);
+    // segmented inclusive scan (segments start at `head`)
+    bool f = head;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const bool fu = __shfl_up_sync(0xffffffffu, f, d);
+      _Pragma("unroll") for (int j = 0; j < M; ++j) {
+        const int64_t vu = __shfl_up_sync(0xffffffffu, v[j], d);
+        if (lane >= d && !f) v[j] = agg_op(A.op[j], v[j], vu);
+      }
+      if (lane >= d) f = f || fu;
+    }
+    // rows of the first segment continue the carry
+    if (carry && act && !f)
+      _Pragma("unroll") for (int j = 0; j < M; ++j) v[j] = agg_op(A.op[j], v[j], cacc[j]);
+    // segment ends: the next lane starts another segment or is inactive
+    const bool nact = __shfl_down_sync(0xffffffffu, act, 1);
+    const bool nhead = __shfl_down_sync(0xffffffffu, head, 1);
+    const bool end_here = act && lane < 31 && (!nact || nhead);
+    bool emit = end_here && having_ok<M>(A, v);
+    const uint32_t bal = __ballot_sync(0xffffffffu, emit);
+    if (bal) {
+      unsigned long long base = 0;
+      const int leader = __ffs(bal) - 1;
+      if (lane == leader) base = atomicAdd(count, (unsigned long long)__popc(bal));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (emit) {
+        const int64_t o = (int64_t)base + __popc(bal & lt);
+        if (o < cap) {
+          out_keys[o] = k;
+          _Pragma("unroll") for (int j = 0; j < M; ++j) out_acc[(int64_t)j * cap + o] = v[j];
+        } else {
+          atomicOr(overflow, 1u);
+        }
+      }
+    }
+    // lane 31's segment stays open -> carry (all lanes keep the same state)
+    const bool act31 = __shfl_sync(0xffffffffu, act, 31);
+    carry = act31;
+    if (act31) {
+      ckey = __shfl_sync(0xffffffffu, k, 31);
+      _Pragma("unroll") for (int j = 0; j < M; ++j) cacc[j] = __shfl_sync(0xffffffffu, v[j], 31);
+    }
+    prev_last = __shfl_sync(0xffffffffu, k, 31);
+    if (!__shfl_sync(0xffffffffu, in, 31)) { done = true; break; }
+  }
+  }
+  if (carry && lane == 0) {
+    const bool ok = having_ok<M>(A, cacc);
+    if (ok) {
+      const unsigned long long o = atomicAdd(count, 1ull);
+      if ((int64_t)o < cap) {
+        out_keys[o] = ckey;
+        _Pragma("unroll") for (int j = 0; j < M; ++j) out_acc[(int64_t)j * cap + (int64_t)o] = cacc[j];
+      } else {
+        atomicOr(overflow, 1u);
+      }
+    }
+  }
+}
+
+// non-decreasing check of a column: *bad = number of i with key[i] < key[i-1]
+__global__ void sorted_check_kernel(scx_column c, int64_t n, unsigned long long* bad) {
+  const void* p = reinterpret_cast<const void*>(c.ptr);
+  unsigned long long cnt = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x + 1; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    cnt += load_i64(p, c.dtype, i) < load_i64(p, c.dtype, i - 1);
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(bad, cnt);
+}
+
 // ---- top-k support: digit histogram of keys in a range, stable select-below --
 __global__ void range_hist_kernel(const uint64_t* keys, int64_t n, uint64_t lo, uint64_t hi,
                                   int shift, uint32_t* counts) {
@@ -458,3 +639,61 @@ extern "C" int scx_direct_agg_compact_having(const int64_t* acc, int64_t cap, in
   Occ O{nullptr, acc, m, occ_word, hv_word, hv_lo, hv_hi};
   return direct_compact(O, acc, cap, m, out_keys, out_acc, count, temp, (cudaStream_t)stream);
 }
+
+extern "C" int scx_is_sorted(const scx_column* col, int64_t n, uint64_t* bad, void* stream) {
+  if (!col || !bad || n < 0) {
+    set_error("is_sorted: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCX_CUDA(cudaMemsetAsync(bad, 0, 8, st));
+  if (n < 2) return SCX_OK;
+  sorted_check_kernel<<<grid_for(n, 256, 2368), 256, 0, st>>>(*col, n, reinterpret_cast<unsigned long long*>(bad));
+  SCX_CHECK_LAUNCH("sorted_check_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_sorted_group_agg(const scx_column* key, const scx_column* vals, const int* ops,
+                                    int m, int64_t n, int hv, int64_t hv_lo, int64_t hv_hi,
+                                    int64_t* out_keys, int64_t* out_acc, int64_t cap,
+                                    uint64_t* count, uint32_t* overflow, void* stream) {
+  if (!key || m < 0 || m > SCX_MAX_MEASURES || (m > 0 && (!vals || !ops)) || n < 0 ||
+      hv >= m || !out_keys || (m > 0 && !out_acc) || !count || !overflow) {
+    set_error("sorted_group_agg: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
+  SCX_CUDA(cudaMemsetAsync(overflow, 0, 4, st));
+  if (n == 0) return SCX_OK;
+  SortedAggArgs A;
+  memset(&A, 0, sizeof(A));
+  A.key = *key;
+  A.m = m;
+  for (int j = 0; j < m; ++j) {
+    A.val[j] = vals[j];
+    A.op[j] = ops[j];
+    if (ops[j] < SCX_AGG_SUM || ops[j] > SCX_AGG_MAX) {
+      set_error("sorted_group_agg: unknown aggregate op %d", ops[j]);
+      return SCX_EINVAL;
+    }
+  }
+  A.hv = hv;
+  A.hv_lo = hv_lo;
+  A.hv_hi = hv_hi;
+  const int64_t warps = (n + kSortedChunk - 1) / kSortedChunk;
+  const int grid = (int)((warps * 32 + 255) / 256);
+  unsigned long long* cnt = reinterpret_cast<unsigned long long*>(count);
+  switch (m) {   // measures in registers: one instantiation per count
+    case 1: sorted_agg_kernel<1><<<grid, 256, 0, st>>>(A, n, out_keys, out_acc, cap, cnt, overflow); break;
+    case 2: sorted_agg_kernel<2><<<grid, 256, 0, st>>>(A, n, out_keys, out_acc, cap, cnt, overflow); break;
+    case 3: sorted_agg_kernel<3><<<grid, 256, 0, st>>>(A, n, out_keys, out_acc, cap, cnt, overflow); break;
+    case 4: sorted_agg_kernel<4><<<grid, 256, 0, st>>>(A, n, out_keys, out_acc, cap, cnt, overflow); break;
+    default:
+      set_error("sorted_group_agg: supports 1..4 measures (got %d)", m);
+      return SCX_EUNSUPPORTED;
+  }
+  SCX_CHECK_LAUNCH("sorted_agg_kernel");
+  return SCX_OK;
+}
+

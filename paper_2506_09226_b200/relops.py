@@ -39,6 +39,10 @@ AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
 _GROUP_MAT = os.environ.get("SCX_GROUP_MAT", "1") != "0"
 _SORTED_RANK = os.environ.get("SCX_SORTED_RANK", "1") != "0"
+# stream aggregation over a sorted key (scx_sorted_group_agg) measured on
+# B200 for Q18: 7.7 ms (warp segmented scan: shuffle-bound) vs 4.4 ms for the
+# direct table + HAVING compaction, so it is opt-in (SCX_STREAM_AGG=1)
+_STREAM_AGG = os.environ.get("SCX_STREAM_AGG", "0") == "1"
 # measured on B200 (SF100, kernel ms): Q8 3.5 -> 5.4, Q3 6.1 -> 7.1, Q17 3.9 -> 4.1
 # with the coarse level on, so it is opt-in (SCX_COARSE=1)
 _COARSE_BITMAPS = os.environ.get("SCX_COARSE", "0") == "1"
@@ -1151,6 +1155,15 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
             dense_v.meta[k] = v.meta[k]
         dense_v.visible = list(v.visible)
         return group_aggregate(dense_v, group_keys, aggs, cross, timing, sort, having)
+    if (_STREAM_AGG and having is not None and not sort and len(keys) == 1
+            and keys[0] not in v.derived and v.origin.get(keys[0], ("",))[0] == "base"
+            and kcols[0].kind in ("int64", "date32") and not v.probes and v.pre.is_true
+            and v.post.is_true and n > (1 << 16) and (cross is None or cross.ep.n == 1)):
+        # clustered key + HAVING (Q18: lineitem by l_orderkey, sum > 300):
+        # stream aggregation, no group table at all
+        r = _stream_group(v, keys[0], kcols[0], plan, measures, having)
+        if r is not None:
+            return r
     if (_SORTED_RANK and len(keys) == 1 and keys[0] not in v.derived
             and v.origin.get(keys[0], ("",))[0] == "base" and kcols[0].kind in ("int64", "date32")
             and n > (1 << 16) and dom > max(4 * n, 1 << 16)):
@@ -1398,6 +1411,92 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
     return ColumnTable(out, tuple(keys))
 
 
+def _agg_columns(out: dict, plan, measure_col, G: int) -> None:
+    """Result columns of a keyed aggregation from its per-measure int64
+    accumulators (measure_col(j) -> tensor of G values), relops.py:131-158."""
+    for a in plan:
+        if a.op == "count":
+            out[a.out] = Column("int64", measure_col(a.m), 0, None, 0, INT64_MAX)
+        elif a.op in ("min", "max"):
+            s = a.src
+            out[a.out] = Column(s.kind, measure_col(a.m), s.scale, None, s.lo, s.hi)
+        elif a.op == "sum":
+            k = decimal_exponent(a.q)
+            if a.kind == "float64":
+                if k < 0:
+                    raise SchemaError("sum with a non-decimal denominator")
+                out[a.out] = Column("float64", measure_col(a.m), k, None, INT64_MIN, INT64_MAX)
+            else:
+                out[a.out] = Column("int64", measure_col(a.m), 0, None, INT64_MIN, INT64_MAX)
+        else:  # avg
+            k = decimal_exponent(a.q)
+            if k < 0:
+                raise SchemaError("avg with a non-decimal denominator")
+            s_col, c_col = measure_col(a.m), measure_col(a.cnt)
+            dst = alloc(G, np.float64)
+            L.call("scx_fixed_to_f64", _ptr(s_col), 1, G, k, _ptr(c_col), 1, _ptr(dst), _stream())
+            out[a.out] = Column("float64", dst, -1, None, 0, -1)
+
+
+def _column_sorted(c: Column) -> bool:
+    """Non-decreasing? Checked once on the device and cached on the column."""
+    if c.sorted is None:
+        bad = alloc(2, np.int64)
+        L.call("scx_is_sorted", C.byref(c.scx()), c.row_count, _ptr(bad), _stream())
+        c.sorted = int(_to_host(bad)[0]) == 0
+    return bool(c.sorted)
+
+
+def _stream_group(v: TableView, key: str, kcol: Column, plan, measures, having):
+    """Group-by with HAVING over an unfiltered table clustered on `key`
+    (scx_sorted_group_agg: each group aggregated by the thread holding its
+    first row; no table).  None when the shape does not fit."""
+    col = v.base.column(key)
+    if not _column_sorted(col):
+        return None
+    vals, ops = [], []
+    n = v.base.row_count
+    for op, im in measures:
+        if im is None:
+            vals.append(col.scx())
+            ops.append(L.AGG_COUNT)
+            continue
+        if im.cond is not None or len(im.terms) != 1:
+            return None
+        coef, fs = im.terms[0]
+        if coef != 1 or len(fs) != 1 or fs[0][0] != 0 or fs[0][1] != 1:
+            return None
+        name = fs[0][2]
+        if v.origin.get(name, ("",))[0] != "base":
+            return None
+        if op == "sum" and _measure_bound(im, v.meta) * max(n, 1) >= (1 << 62):
+            return None
+        vals.append(v.meta[name].scx())
+        ops.append(_OPCODE[op])
+    a = next((a for a in plan if a.out == having[0]), None)
+    if a is None or not (a.op == "count" or (a.op == "sum" and a.kind == "int64" and a.q == 1)):
+        return None
+    M = len(measures)
+    varr = (L.Column_ * M)(*vals)
+    oarr = (C.c_int * M)(*ops)
+    stat = alloc(2, np.int64)
+    cnt, ovf = stat[:1], stat[1:].view(_torch().uint32)
+    cap = 1 << 16
+    while True:
+        okeys = alloc(cap, np.int64)
+        oacc = alloc(cap * M, np.int64)
+        L.call("scx_sorted_group_agg", C.byref(col.scx()), varr, oarr, M, n, a.m, int(having[1]),
+               int(having[2]), _ptr(okeys), _ptr(oacc), cap, _ptr(cnt), _ptr(ovf), _stream())
+        st = _to_host(stat)
+        G = int(st[0])
+        if not int(st[1]) & 0xFFFFFFFF:
+            break
+        cap = G + (G & 1)             # keeps every measure slice 16-byte aligned
+    out = {key: Column(kcol.kind, okeys[:G], kcol.scale, kcol.dictionary, kcol.lo, kcol.hi)}
+    _agg_columns(out, plan, lambda j: oacc[j * cap: j * cap + G], G)
+    return ColumnTable(out, (key,))
+
+
 def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) -> ColumnTable:
     torch = _torch()
     S = b.P.sink
@@ -1564,28 +1663,7 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) 
             raise SchemaError("aggregate result exceeds the 64-bit output range")
         return out64
 
-    for a in plan:
-        if a.op == "count":
-            out[a.out] = Column("int64", measure_col(a.m), 0, None, 0, INT64_MAX)
-        elif a.op in ("min", "max"):
-            s = a.src
-            out[a.out] = Column(s.kind, measure_col(a.m), s.scale, None, s.lo, s.hi)
-        elif a.op == "sum":
-            k = decimal_exponent(a.q)
-            if a.kind == "float64":
-                if k < 0:
-                    raise SchemaError("sum with a non-decimal denominator")
-                out[a.out] = Column("float64", measure_col(a.m), k, None, INT64_MIN, INT64_MAX)
-            else:
-                out[a.out] = Column("int64", measure_col(a.m), 0, None, INT64_MIN, INT64_MAX)
-        else:  # avg
-            k = decimal_exponent(a.q)
-            if k < 0:
-                raise SchemaError("avg with a non-decimal denominator")
-            s_col, c_col = measure_col(a.m), measure_col(a.cnt)
-            dst = alloc(G, np.float64)
-            L.call("scx_fixed_to_f64", _ptr(s_col), 1, G, k, _ptr(c_col), 1, _ptr(dst), _stream())
-            out[a.out] = Column("float64", dst, -1, None, 0, -1)
+    _agg_columns(out, plan, measure_col, G)
     res = ColumnTable(out, tuple(keys))
     res._having_done = direct and hv is not None
     return res

@@ -298,3 +298,31 @@ def test_top_k_equals_sort_head(k):
     idx = np.lexsort([b, -a])[:k]
     assert np.array_equal(got.column("a").values, a[idx])
     assert np.array_equal(got.column("b").values, b[idx])
+
+
+@pytest.mark.parametrize("sorted_keys", [True, False])
+def test_group_having_unsorted_output(sorted_keys):
+    """sort=False + HAVING: a clustered key takes the stream aggregation
+    (scx_sorted_group_agg, unordered output), an unclustered one the table
+    path; as a set of groups both equal the oracle's group + filter."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(23)
+    n = 300_000
+    k = np.sort(rng.integers(0, 80_000, size=n)) * 13 + 7
+    if not sorted_keys:
+        k = rng.permutation(k)
+    x = rng.integers(0, 100, size=n)
+    ref = {"k": ("int64", k, None), "x": ("int64", x, None)}
+    aggs = {"sx": ("sum", "x"), "n": ("count", None), "mx": ("max", "x")}
+    t = ColumnTable({n_: Column.from_numpy(kd, v) for n_, (kd, v, _) in ref.items()})
+    from paper_2506_09226_b200 import relops as R
+    saved, R._STREAM_AGG = R._STREAM_AGG, True     # exercise the opt-in kernel too
+    try:
+        got = _dev().group_aggregate(t, ["k"], aggs, sort=False,
+                                     having=("sx", 250, 10 ** 9)).materialize()
+    finally:
+        R._STREAM_AGG = saved
+    got = got.sort_by(["k"])
+    exp = O.group(ref, ["k"], aggs)
+    exp = O.filter_(exp, exp["sx"][1] >= 250)
+    assert_table_matches(got, O.to_jsonable(exp), f"having-unsorted sorted_keys={sorted_keys}")

@@ -1088,9 +1088,21 @@ def group_aggregate(table, group_keys: list[str], aggs: dict[str, tuple],
     # derived keys read their source column, transformed in the kernel
     ksrc = [v.derived[k].src if k in v.derived else k for k in keys]
     plan, measures = _plan_aggs(v, aggs)
-    if keys and not any(op == "count" for op, _ in measures):
+    # HAVING lo <= sum with lo > 0 over non-negative rows: an empty slot (sum 0)
+    # can never qualify, so the sum itself marks live groups -- no count word
+    # (Q18: a 150M-slot direct table of one word instead of two)
+    having_occ = None
+    if keys and having is not None and int(having[1]) > 0 and \
+            not any(op == "count" for op, _ in measures):
+        a = next((a for a in plan if a.out == having[0]), None)
+        if a is not None and a.op == "sum" and a.kind == "int64" and a.q == 1:
+            r = _measure_range(measures[a.m][1], v.meta)
+            if r is not None and r[0] >= 0:
+                having_occ = a.m
+    if keys and having_occ is None and not any(op == "count" for op, _ in measures):
         measures.append(("count", None))     # live-group detection
-    count_m = next(i for i, (op, _) in enumerate(measures) if op == "count") if keys else None
+    count_m = (having_occ if having_occ is not None else
+               next(i for i, (op, _) in enumerate(measures) if op == "count")) if keys else None
     if len(measures) > L.MAX_MEASURES:
         raise SchemaError("too many aggregate measures")
     names = set(ksrc)

@@ -201,7 +201,8 @@ typedef struct scx_sink {
   int32_t glut[SCX_MAX_GKEYS];    /* DENSE: offset into lut[] or -1       */
   int32_t n_cells;                /* DENSE: prod(gcard); HASH: 1 = direct-
                                      addressed (slot = packed key, gcap =
-                                     key domain), 0 = open addressing    */
+                                     key domain), 2 = direct with u32
+                                     sum/count words, 0 = open addressing */
   int32_t n_out;                  /* COMPACT: output columns              */
   uint64_t acc;        /* DENSE: {u64 lo, i64 hi}[cells][M]; HASH: i64[cap][M] */
   uint64_t gkeys;      /* HASH: u64[cap] packed group keys                 */
@@ -360,6 +361,11 @@ int scx_sorted_group_agg(const scx_column* key, const scx_column* vals, const in
                          int64_t n, int hv, int64_t hv_lo, int64_t hv_hi, int64_t* out_keys_dev,
                          int64_t* out_acc_dev, int64_t cap, uint64_t* count_dev,
                          uint32_t* overflow_dev, void* stream);
+
+/* Narrow direct group tables (sink.n_cells == 2: u32 count / small-sum
+ * accumulators, half the random-access footprint of int64) are widened to
+ * int64 words before scx_direct_agg_compact_counted. */
+int scx_widen_u32(const uint32_t* in_dev, int64_t n, int64_t* out_dev, void* stream);
 
 /* 128-bit {lo, hi} hash-group sums (measure._pad = 1 marks a "wide" sum whose
  * accumulator is two words) -> int64; flag_dev[0] |= 1 if any value does not

@@ -1137,8 +1137,17 @@ struct Gen {
       // not add in 64 bits).
       o << "    {\n      u64 run = SCX_EMPTY;\n";
       for (int m = 0; m < M; ++m) o << "      i64 ra" << m << " = 0;\n";
+      // n_cells == 2: direct table of u32 accumulators (count / small sums;
+      // the host widens it to int64 before the compaction)
+      const bool narrow = S.n_cells == 2;
+      if (narrow)
+        for (int m = 0; m < M; ++m)
+          if ((S.m[m].op != SCX_AGG_SUM && S.m[m].op != SCX_AGG_COUNT) || S.m[m]._pad == 1) {
+            err = "narrow group table supports sum / count only";
+            return SCX_EINVAL;
+          }
       o << "      auto flush = [&](u64 key) {\n";
-      if (S.n_cells == 1) {
+      if (S.n_cells == 1 || narrow) {
         // direct-addressed groups: the packed key is the slot (gcap = domain)
         o << "        u64 slot = SCX_EMPTY;\n";
         // (no key array: occupancy is the group's count word, compacted by
@@ -1158,6 +1167,11 @@ struct Gen {
       o << "        if (slot == SCX_EMPTY) { atomicOr((u32*)a.p[" << flags_p << "], 1u); return; }\n";
       for (int m = 0; m < M; ++m) {
         const int op = S.m[m].op;
+        if (narrow) {
+          o << "        { unsigned int* t = (unsigned int*)gacc + slot * " << W << " + " << woff[m]
+            << "; if (ra" << m << ") atomicAdd(t, (unsigned int)ra" << m << "); }\n";
+          continue;
+        }
         o << "        { long long* t = (long long*)(gacc + slot * " << W << " + " << woff[m] << "); ";
         if (op == SCX_AGG_MIN) o << "atomicMin(t, ra" << m << "); }\n";
         else if (op == SCX_AGG_MAX) o << "atomicMax(t, ra" << m << "); }\n";
@@ -1168,7 +1182,7 @@ struct Gen {
       o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
       o << "        if (!((sel >> r) & 1u)) continue;\n";
       pack_key(S.gkey, "r", S.glut, -1, "key", "kin");
-      if (S.n_cells == 1) o << "        if (!kin) { atomicOr((u32*)a.p[" << flags_p << "], 1u); continue; }\n";
+      if (S.n_cells == 1 || S.n_cells == 2) o << "        if (!kin) { atomicOr((u32*)a.p[" << flags_p << "], 1u); continue; }\n";
       else o << "        (void)kin;\n";
       for (int m = 0; m < M; ++m) o << "        const i64 mv" << m << " = " << measure_expr(S.m[m], "r") << ";\n";
       if (!any_wide) {

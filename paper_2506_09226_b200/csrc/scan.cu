@@ -697,3 +697,21 @@ extern "C" int scx_sorted_group_agg(const scx_column* key, const scx_column* val
   return SCX_OK;
 }
 
+// u32 group-table words -> int64 (narrow direct tables, before compaction)
+__global__ void widen_u32_kernel(const uint32_t* in, int64_t n, int64_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int64_t)in[i];
+}
+
+extern "C" int scx_widen_u32(const uint32_t* in, int64_t n, int64_t* out, void* stream) {
+  if ((n > 0 && (!in || !out)) || n < 0) {
+    set_error("widen_u32: bad arguments");
+    return SCX_EINVAL;
+  }
+  if (n == 0) return SCX_OK;
+  widen_u32_kernel<<<grid_for(n, 256, 2368), 256, 0, (cudaStream_t)stream>>>(in, n, out);
+  SCX_CHECK_LAUNCH("widen_u32_kernel");
+  return SCX_OK;
+}
+

@@ -104,6 +104,14 @@ def _q1_packed():
     return P
 
 
+def _hashgroup_narrow():
+    # direct-addressed u32 sum / count table (sink.n_cells = 2), no key array
+    P = _hashgroup()
+    P.sink.n_cells = 2
+    P.sink.gkeys = 0
+    return P
+
+
 def _dense_smem():
     P = _q1()
     P.sink.n_cells = 12
@@ -168,6 +176,7 @@ PLANS = {
     "compact_semi_direct": lambda: _compact_probe(L.HT_DIRECT, L.JOIN_SEMI),
     "compact_anti_hash": lambda: _compact_probe(L.HT_HASH, L.JOIN_ANTI),
     "hash_group": _hashgroup,
+    "hash_group_direct_narrow": _hashgroup_narrow,
 }
 
 

@@ -309,6 +309,24 @@ static __device__ __forceinline__ void cpa4(u32 dst, const void* src) {
 static __device__ __forceinline__ void l2_prefetch(const void* p, u32 bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
 }
+// TMA bulk copies + mbarriers (producer warp -> consumer warps ring)
+static __device__ __forceinline__ void mb_init(u32 bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+static __device__ __forceinline__ void mb_expect_tx(u32 bar, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+static __device__ __forceinline__ void mb_arrive(u32 bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(bar) : "memory");
+}
+static __device__ __forceinline__ void mb_wait(u32 bar, u32 parity) {
+  asm volatile("{ .reg .pred p; W%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W%=; }"
+               :: "r"(bar), "r"(parity) : "memory");
+}
+static __device__ __forceinline__ void bulk_g2s(u32 dst, const void* src, u32 bytes, u32 bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
 static __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 static __device__ __forceinline__ void cpa_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 static __device__ __forceinline__ void cpa_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -397,6 +415,10 @@ struct Gen {
   size_t dyn_smem = 0;
   int stage_p = -1, stage_rows_p = -1;   // COMPACT: staging base / rows, bound at launch
   int nw_priv = 0;              // dense private accumulators: 64-bit words per cell
+  bool tma = false;             // base columns streamed by a producer warp (TMA bulk copies)
+  int tma_stages = 0;
+  size_t ring_off = 0, bar_off = 0;
+  int threads() const { return tma ? kTPB + 32 : kTPB; }
   int coarse_p[SCX_MAX_PROBES] = {-1, -1, -1, -1, -1, -1, -1, -1};   // Args index of coarse bitmaps
   bool pipe = false;            // base columns double-buffered through shared memory
   size_t sink_smem = 0;         // dynamic smem used by the sink (before the load stages)
@@ -672,7 +694,20 @@ struct Gen {
       const int pi = col_p[s];
       o << "    { const char* p = (const char*)a.p[" << pi << "] + row0 * " << w << "ll;\n";
       o << "      if (full) {\n";
-      if (pipe) {
+      if (tma) {
+        o << "        const unsigned char* q = dsm + " << ring_off << " + (u32)tma_st * " << stage_bytes()
+          << "u + " << stage_off(s) << "u + (u32)tid * " << nb << "u;\n";
+        if (nb >= 16) {
+          for (int j = 0; j < nb / 16; ++j)
+            o << "        { const uint4 t = *(const uint4*)(q + " << 16 * j << "); w" << s << "[" << 4 * j
+              << "] = t.x; w" << s << "[" << 4 * j + 1 << "] = t.y; w" << s << "[" << 4 * j + 2
+              << "] = t.z; w" << s << "[" << 4 * j + 3 << "] = t.w; }\n";
+        } else if (nb == 8) {
+          o << "        { const uint2 t = *(const uint2*)q; w" << s << "[0] = t.x; w" << s << "[1] = t.y; }\n";
+        } else {
+          o << "        w" << s << "[0] = *(const u32*)q;\n";
+        }
+      } else if (pipe) {
         o << "        const unsigned char* q = stg + (u32)buf * " << stage_bytes() << "u + " << stage_off(s) << "u;\n";
         if (nb >= 16) {
           for (int j = 0; j < nb / 16; ++j)
@@ -893,6 +928,22 @@ struct Gen {
       }
       sink_smem = sink_b;
     }
+    // TMA streaming: a producer warp copies each column's tile chunk with one
+    // cp.async.bulk into a shared-memory ring (S stages, mbarrier full/empty);
+    // the 8 consumer warps read their rows from shared memory.  Bytes in
+    // flight no longer cost registers.  Opt-in with SCX_TMA=1 (A/B).
+    {
+      const char* env = getenv("SCX_TMA");
+      tma = env && env[0] == '1' && !pipe && P.n_base > 0 && row_bytes > 0;
+      if (tma) {
+        const size_t stage = (size_t)kTPB * V * row_bytes;
+        int st = (int)((64 * 1024) / stage);
+        tma_stages = st < 2 ? 2 : (st > 6 ? 6 : st);
+        ring_off = (sink_smem + 127) & ~(size_t)127;
+        bar_off = ring_off + (size_t)tma_stages * stage;
+        bar_off = (bar_off + 15) & ~(size_t)15;
+      }
+    }
     const int64_t tile_rows = (int64_t)kTPB * V;
     tiles_out = (int)((P.n_rows + tile_rows - 1) / tile_rows);
 
@@ -908,7 +959,9 @@ struct Gen {
     // when their shared memory allows it (the register cap becomes 85)
     const int min_blocks = occ_target() > 2 ? occ_target()
                          : (dense_priv && (size_t)NC * NW * kTPB * 8 <= 72 * 1024) ? 3 : 2;
-    o << "extern \"C\" __global__ void __launch_bounds__(" << kTPB << ", " << min_blocks
+    o << (tma ? "#define CSYNC() asm volatile(\"bar.sync 1, 256;\" ::: \"memory\")\n"
+              : "#define CSYNC() __syncthreads()\n");
+    o << "extern \"C\" __global__ void __launch_bounds__(" << threads() << ", " << min_blocks
       << ") KNAME(const __grid_constant__ Args a) {\n";
     o << "  constexpr int V = " << V << ";\n";
     o << "  const i64 n = a.n;\n";
@@ -917,6 +970,45 @@ struct Gen {
     o << "  (void)lane; (void)warp;\n";
     o << "  extern __shared__ __align__(16) unsigned char dsm[];\n";
     for (int c = 0; c < P.n_base; ++c) col_p.push_back(param(P.base[c].ptr));
+    if (tma) {
+      const int S_ = tma_stages;
+      const int64_t stage = (int64_t)kTPB * V * row_bytes;
+      const bool cmp = S.kind == SCX_SINK_COMPACT;
+      o << "  const u32 ring = smem_u32(dsm + " << ring_off << ");\n";
+      o << "  const u32 bars = smem_u32(dsm + " << bar_off << ");   // full[s] = bars+8s, empty[s] = bars+8(S+s)\n";
+      o << "  if (tid == 0) {\n";
+      o << "    for (int s = 0; s < " << S_ << "; ++s) { mb_init(bars + 8u * s, 1u); mb_init(bars + 8u * (" << S_ << " + s), 8u); }\n";
+      o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
+      o << "  }\n  __syncthreads();\n";
+      o << "  if (tid >= " << kTPB << ") {   // producer warp\n";
+      o << "    if (lane == 0) {\n";
+      if (cmp) {
+        o << "      const i64 tpc_ = (ntiles + gridDim.x - 1) / gridDim.x;\n";
+        o << "      const i64 t_first = (i64)blockIdx.x * tpc_, t_step = 1;\n";
+        o << "      const i64 t_end = t_first + tpc_ < ntiles ? t_first + tpc_ : ntiles;\n";
+      } else {
+        o << "      const i64 t_first = (i64)blockIdx.x, t_step = (i64)gridDim.x, t_end = ntiles;\n";
+      }
+      o << "      int it = 0;\n";
+      o << "      for (i64 tile = t_first; tile < t_end; tile += t_step, ++it) {\n";
+      o << "        const int st = it % " << S_ << ";\n";
+      o << "        if (it >= " << S_ << ") mb_wait(bars + 8u * (" << S_ << " + st), (u32)((it / " << S_ << " - 1) & 1));\n";
+      o << "        const i64 r0 = tile * " << tile_rows << "ll;\n";
+      o << "        const i64 rows = n - r0 < " << tile_rows << "ll ? n - r0 : " << tile_rows << "ll;\n";
+      o << "        u32 tot = 0;\n";
+      for (int c = 0; c < P.n_base; ++c) {
+        const int w = dtype_size(P.base[c].dtype);
+        o << "        const u32 b" << c << " = (u32)((rows * " << w << " + 15) & ~15ll); tot += b" << c << ";\n";
+      }
+      o << "        mb_expect_tx(bars + 8u * st, tot);\n";
+      for (int c = 0; c < P.n_base; ++c) {
+        const int w = dtype_size(P.base[c].dtype);
+        o << "        bulk_g2s(ring + (u32)st * " << stage << "u + " << stage_off(c) << "u, (const char*)a.p["
+          << col_p[c] << "] + r0 * " << w << "ll, b" << c << ", bars + 8u * st);\n";
+      }
+      o << "      }\n    }\n    return;\n  }\n";
+      o << "  int tma_it = 0;\n";
+    }
 
     // sink state
     int acc_p = -1, gkeys_p = -1, gcap_p = -1, flags_p = -1, status_p = -1, count_p = -1;
@@ -950,7 +1042,7 @@ struct Gen {
         for (int m = 0; m < M; ++m)
           o << "m == " << m << " ? " << (S.m[m].op == SCX_AGG_MIN ? "0x7fffffffffffffffll" :
                                          S.m[m].op == SCX_AGG_MAX ? "(-0x7fffffffffffffffll - 1)" : "0ll") << " : ";
-        o << "0ll;\n  }\n  __syncthreads();\n";
+        o << "0ll;\n  }\n  CSYNC();\n";
       }
     } else if (S.kind == SCX_SINK_AGG_HASH) {
       acc_p = param(S.acc);
@@ -1014,9 +1106,10 @@ struct Gen {
         o << "    for (int i = tid; i < " << nw << "; i += " << kTPB << ") cbm" << pi << "[i] = __ldg(src + i); }\n";
         any = true;
       }
-      if (any) o << "  __syncthreads();\n";
+      if (any) o << "  CSYNC();\n";
     }
     if (dyn_smem < sink_smem) dyn_smem = sink_smem;
+    if (tma) dyn_smem = bar_off + 16 * (size_t)tma_stages;
     if (pipe) {
       dyn_smem = sink_smem + 2 * (size_t)stage_bytes();
       const bool cmp = S.kind == SCX_SINK_COMPACT;
@@ -1051,6 +1144,11 @@ struct Gen {
       }
       o << "        l2_prefetch(cp, cb);\n      }\n    }\n";
     }
+    if (tma) {
+      o << "    const int tma_st = tma_it % " << tma_stages << ";\n";
+      o << "    mb_wait(bars + 8u * tma_st, (u32)((tma_it / " << tma_stages << ") & 1));\n";
+      o << "    ++tma_it;\n";
+    }
     o << "    const i64 row0 = (tile * " << kTPB << " + tid) * (i64)V;\n";
     o << "    const bool full = row0 + V <= n;\n";
     o << "    const int rem = row0 >= n ? 0 : (int)(n - row0 < V ? n - row0 : V);\n";
@@ -1060,6 +1158,7 @@ struct Gen {
     o << "    if (rem > 0) {\n";
     emit_loads();
     o << "    }\n";
+    if (tma) o << "    __syncwarp();\n    if (lane == 0) mb_arrive(bars + 8u * (" << tma_stages << " + tma_st));\n";
     // when rem == 0 the word arrays are uninitialised but sel == 0 masks every use
     emit_pred(P.pre, "pre-predicate");
     for (int p = 0; p < P.n_probes; ++p) {
@@ -1222,7 +1321,7 @@ struct Gen {
       o << "      u32 inc = c;\n";
       o << "#pragma unroll\n      for (int d = 1; d < 32; d <<= 1) { const u32 y = __shfl_up_sync(0xffffffffu, inc, d); if (lane >= d) inc += y; }\n";
       o << "      if (lane == 31) s_warp[warp] = inc;\n";
-      o << "      __syncthreads();\n";
+      o << "      CSYNC();\n";
       o << "      if (warp == 0) {\n";
       o << "        const u32 wc = lane < " << kTPB / 32 << " ? s_warp[lane] : 0u;\n";
       o << "        u32 wi = wc;\n";
@@ -1230,10 +1329,10 @@ struct Gen {
       o << "        if (lane < " << kTPB / 32 << ") s_warp[lane] = wi - wc;\n";
       o << "        if (lane == 31) s_tot = wi;\n";
       o << "      }\n";
-      o << "      __syncthreads();\n";
+      o << "      CSYNC();\n";
       o << "      const i64 base = (i64)(tbeg * " << tile_rows << "ll) + (i64)cta_pos + s_warp[warp] + inc - c;\n";
       o << "      cta_pos += s_tot;\n";
-      o << "      __syncthreads();\n";   // s_warp / s_tot reused by the next tile
+      o << "      CSYNC();\n";   // s_warp / s_tot reused by the next tile
       for (int i = 0; i < S.n_out; ++i) {
         const int s2 = S.out_slot[i];
         const char* t = ctype(S.out[i].dtype);
@@ -1263,7 +1362,7 @@ struct Gen {
                   ulit64((1ull << mbits[m]) - 1) + ")";
           o << "  { const i64 v = " << f << "(" << src << "); if (lane == 0) red[warp][" << c * M + m << "] = v; }\n";
         }
-      o << "  __syncthreads();\n";
+      o << "  CSYNC();\n";
       o << "  if (tid < " << NC * M << ") {\n";
       o << "    const int c = tid / " << M << ", m = tid % " << M << ";\n";
       o << "    i64* gacc = (i64*)a.p[" << acc_p << "] + 2 * (c * " << M << " + m);\n";
@@ -1284,7 +1383,7 @@ struct Gen {
       o << "      if (h) atomicAdd((unsigned long long*)(gacc + 1), (unsigned long long)h);\n";
       o << "    }\n  }\n";
     } else if (S.kind == SCX_SINK_AGG_DENSE) {
-      o << "  __syncthreads();\n";
+      o << "  CSYNC();\n";
       o << "  for (int i = tid; i < " << (int64_t)S.n_cells * M << "; i += " << kTPB << ") {\n";
       o << "    const int m = i % " << M << ";\n";
       o << "    const i64 v = tab[i];\n";
@@ -1318,6 +1417,7 @@ struct Gen {
 };
 
 struct Prepared {
+  int threads = 256;
   std::string src, name;
   std::vector<uint64_t> ptrs;
   int tiles = 0;
@@ -1345,6 +1445,7 @@ static int prepare(const scx_pipeline& P, Prepared& out) {
   }
   out.ptrs = g.ptrs;
   out.dyn_smem = g.dyn_smem;
+  out.threads = g.threads();
   out.V = g.V;
   out.stage_p = g.stage_p;
   out.stage_rows_p = g.stage_rows_p;
@@ -1426,7 +1527,7 @@ static int plan_launch_uncached(const scx_pipeline& P, LaunchPlan& lp) {
     lp.e->max_dyn_smem = (int)lp.pp.dyn_smem;
   }
   int occ = 0;
-  int cr = drv.occupancy(&occ, lp.e->fn, kTPB, lp.pp.dyn_smem);
+  int cr = drv.occupancy(&occ, lp.e->fn, lp.pp.threads, lp.pp.dyn_smem);
   if (cr) return drv_fail(cr, "cuOccupancyMaxActiveBlocksPerMultiprocessor");
   if (occ < 1) { set_error("jit kernel does not fit an SM"); return SCX_EUNSUPPORTED; }
   int dev = 0, sms = 0;
@@ -1498,7 +1599,7 @@ extern "C" int scx_pipeline_run(const scx_pipeline* d, void* stream) {
   }
   void* params[] = {&args};
   jit::Driver& drv = jit::driver();
-  int cr = drv.launch(lp.e->fn, (unsigned)lp.grid, 1, 1, jit::kTPB, 1, 1, (unsigned)lp.pp.dyn_smem,
+  int cr = drv.launch(lp.e->fn, (unsigned)lp.grid, 1, 1, (unsigned)lp.pp.threads, 1, 1, (unsigned)lp.pp.dyn_smem,
                       stream, params, nullptr);
   if (cr) return jit::drv_fail(cr, "cuLaunchKernel");
   SCX_CHECK_LAUNCH("scx_pipe (jit)");

@@ -334,9 +334,18 @@ def main() -> None:
     # inside the timed region)
     reserve_device_pool(int(min(96, max(8, args.sf * 0.6)) * (1 << 30)))
 
+    dbg = os.environ.get("SCX_BENCH_DEBUG") == "1"
+
+    def jit_compiled():
+        v = [_lib.C.c_int64() for _ in range(3)]
+        lib.scx_jit_stats(*[_lib.C.byref(x) for x in v])
+        return v[0].value
+
     def suite(tabs, per_query=None):
         results = {}
         for q in QUERIES:
+            if dbg:
+                c0, t0 = jit_compiled(), time.perf_counter()
             if per_query is not None:
                 e0 = torch.cuda.Event(enable_timing=True)
                 e0.record()
@@ -345,6 +354,11 @@ def main() -> None:
             if r is not None:
                 r = r.materialize()
             results[q] = r
+            if dbg:
+                torch.cuda.synchronize()
+                dt = (time.perf_counter() - t0) * 1e3
+                if jit_compiled() != c0 or dt > 15:
+                    print(f"  {q}: {dt:.1f} ms, jit compiled {jit_compiled() - c0}", file=sys.stderr)
             if per_query is not None:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record()

@@ -931,13 +931,25 @@ struct Gen {
     // TMA streaming: a producer warp copies each column's tile chunk with one
     // cp.async.bulk into a shared-memory ring (S stages, mbarrier full/empty);
     // the 8 consumer warps read their rows from shared memory.  Bytes in
-    // flight no longer cost registers.  Opt-in with SCX_TMA=1 (A/B).
+    // flight no longer cost registers.
     {
       const char* env = getenv("SCX_TMA");
-      tma = env && env[0] == '1' && !pipe && P.n_base > 0 && row_bytes > 0;
+      // SCX_TMA=0 off, 1 every kernel, 2 kernels without probe stages,
+      // 3 (default) kernels without probes or with a compaction sink --
+      // measured at SF100 (suite kernel ms): off 66.3, 1 68.7, 2 66.1; mode 1
+      // sped up the compaction kernels (Q3 4.75 -> 4.06, Q9 8.24 -> 7.71,
+      // Q17 3.13 -> 2.95) and slowed probe + aggregate ones (Q8, Q20)
+      const char mode = env && *env ? env[0] : '3';
+      bool hash_probe = false;      // open-addressing probes keep the register path (Q20)
+      for (int pi = 0; pi < P.n_probes; ++pi) hash_probe |= P.probe[pi].table.kind == SCX_HT_HASH;
+      tma = (mode == '1' || (mode == '2' && P.n_probes == 0) ||
+             (mode == '3' && (P.n_probes == 0 || (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
+            !pipe && P.n_base > 0 && row_bytes > 0;
       if (tma) {
         const size_t stage = (size_t)kTPB * V * row_bytes;
-        int st = (int)((64 * 1024) / stage);
+        const char* rb = getenv("SCX_TMA_RING_KB");
+        const size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : 32) * 1024;
+        int st = (int)(ring_budget / stage);
         tma_stages = st < 2 ? 2 : (st > 6 ? 6 : st);
         ring_off = (sink_smem + 127) & ~(size_t)127;
         bar_off = ring_off + (size_t)tma_stages * stage;
@@ -975,9 +987,9 @@ struct Gen {
       const int64_t stage = (int64_t)kTPB * V * row_bytes;
       const bool cmp = S.kind == SCX_SINK_COMPACT;
       o << "  const u32 ring = smem_u32(dsm + " << ring_off << ");\n";
-      o << "  const u32 bars = smem_u32(dsm + " << bar_off << ");   // full[s] = bars+8s, empty[s] = bars+8(S+s)\n";
+      o << "  const u32 bars = smem_u32(dsm + " << bar_off << ");   // full[s] = bars+8s (producer + tx), empty[s] = bars+8(S+s) (256 consumer threads)\n";
       o << "  if (tid == 0) {\n";
-      o << "    for (int s = 0; s < " << S_ << "; ++s) { mb_init(bars + 8u * s, 1u); mb_init(bars + 8u * (" << S_ << " + s), 8u); }\n";
+      o << "    for (int s = 0; s < " << S_ << "; ++s) { mb_init(bars + 8u * s, 1u); mb_init(bars + 8u * (" << S_ << " + s), " << kTPB << "u); }\n";
       o << "    asm volatile(\"fence.mbarrier_init.release.cluster;\" ::: \"memory\");\n";
       o << "  }\n  __syncthreads();\n";
       o << "  if (tid >= " << kTPB << ") {   // producer warp\n";
@@ -1158,7 +1170,12 @@ struct Gen {
     o << "    if (rem > 0) {\n";
     emit_loads();
     o << "    }\n";
-    if (tma) o << "    __syncwarp();\n    if (lane == 0) mb_arrive(bars + 8u * (" << tma_stages << " + tma_st));\n";
+    // every consumer thread releases the stage itself, after a proxy fence:
+    // its generic-proxy shared-memory reads must be ordered before the async
+    // proxy (the next cp.async.bulk) overwrites the stage -- without the
+    // fence a 2-stage ring returned stale rows (a WAR race across proxies)
+    if (tma) o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n"
+                  << "    mb_arrive(bars + 8u * (" << tma_stages << " + tma_st));\n";
     // when rem == 0 the word arrays are uninitialised but sel == 0 masks every use
     emit_pred(P.pre, "pre-predicate");
     for (int p = 0; p < P.n_probes; ++p) {

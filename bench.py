@@ -65,15 +65,17 @@ def peaks() -> dict:
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region.
 
-    NVML from a background thread (``nvidia_ml_py``), every ``period`` s.
-    ``SCX_CLOCKS=smi`` uses an ``nvidia-smi -lms`` subprocess instead and
-    ``SCX_CLOCKS=off`` disables sampling (for A/B checks of sampler
-    interference).
+    An ``nvidia-smi -lms`` subprocess by default; ``SCX_CLOCKS=nvml`` samples
+    with NVML from a background thread instead and ``SCX_CLOCKS=off``
+    disables sampling (for A/B checks of sampler interference).
     """
 
     def __init__(self, device: int, period: float = 0.05):
         import threading
-        self.mode = os.environ.get("SCX_CLOCKS", "nvml")
+        # default: an nvidia-smi subprocess.  In-process NVML sampling stalled
+        # one query of a timed pass by ~80 ms (driver lock) in 3 of 4 runs;
+        # SCX_CLOCKS=nvml keeps it available for comparison
+        self.mode = os.environ.get("SCX_CLOCKS", "smi")
         self.samples: list[tuple[float, float, int]] = []
         self.max_mhz = None
         self.proc = None
@@ -423,8 +425,11 @@ def main() -> None:
         step_ms.append(e0.elapsed_time(e1))
         ms_ = torch.cuda.memory_stats()
         print(f"step {len(step_ms)}: {step_ms[-1]:.2f} ms, alloc retries "
-              f"{ms_.get('num_alloc_retries', 0)}, segments {ms_.get('segment.all.current', 0)}, "
-              f"cudaMalloc calls {ms_.get('segment.all.allocated', 0)}", file=sys.stderr)
+              f"{ms_.get('num_alloc_retries', 0)}, reserved "
+              f"{ms_.get('reserved_bytes.all.current', 0) / 2**30:.2f} GiB, peak "
+              f"{ms_.get('allocated_bytes.all.peak', 0) / 2**30:.2f} GiB, "
+              f"slowest {max(per, key=lambda x: x[1].elapsed_time(x[2]))[0] if per else '-'}",
+              file=sys.stderr)
         for q, a, b in per:
             q_ms[q].append(a.elapsed_time(b))
     launches = lib.scx_launch_count() - launches0

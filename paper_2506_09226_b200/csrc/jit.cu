@@ -942,8 +942,11 @@ struct Gen {
       const char mode = env && *env ? env[0] : '3';
       bool hash_probe = false;      // open-addressing probes keep the register path (Q20)
       for (int pi = 0; pi < P.n_probes; ++pi) hash_probe |= P.probe[pi].table.kind == SCX_HT_HASH;
+      // (private-accumulator group-bys keep 3 CTAs/SM on the register path:
+      // their 48 KB of accumulators + the ring would leave 2; Q1 1.63 vs 1.68 ms)
       tma = (mode == '1' || (mode == '2' && P.n_probes == 0) ||
-             (mode == '3' && (P.n_probes == 0 || (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
+             (mode == '3' && ((P.n_probes == 0 && !dense_priv) ||
+                              (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
             !pipe && P.n_base > 0 && row_bytes > 0;
       if (tma) {
         const size_t stage = (size_t)kTPB * V * row_bytes;

@@ -471,8 +471,31 @@ class IntMeasure:
     cond: Atom | None = None
 
 
+_INT_CACHE: dict = {}
+
+
 def integerise(p: Poly, cols: dict[str, Column]) -> IntMeasure:
-    """Rewrite a logical-unit polynomial over physical fixed-point integers."""
+    """Rewrite a logical-unit polynomial over physical fixed-point integers
+    (memoised on the polynomial's structure and its columns' scales: plans
+    rebuild the same expressions every run and Fraction arithmetic is slow)."""
+    try:
+        key = (tuple((t.coef, tuple((f.a, f.b, f.col, cols[f.col].kind == "float64" and
+                                     cols[f.col].scale) for f in t.factors)) for t in p.terms),
+               p.cond)
+        hit = _INT_CACHE.get(key)
+    except TypeError:          # unhashable condition: no memo
+        key, hit = None, None
+    if hit is not None:
+        return hit
+    res = _integerise(p, cols)
+    if key is not None:
+        if len(_INT_CACHE) > 4096:
+            _INT_CACHE.clear()
+        _INT_CACHE[key] = res
+    return res
+
+
+def _integerise(p: Poly, cols: dict[str, Column]) -> IntMeasure:
     raw = []
     for t in p.terms:
         coef = t.coef

@@ -309,6 +309,13 @@ int scx_direct_agg_compact_counted(const int64_t* acc_dev, int64_t cap, int m, i
  * hv_hi (Q18's sum(l_quantity) > 300: 150M groups scanned, ~600 written).
  * Equivalent to filtering the group_aggregate output (relops.py:97-160 then
  * table.py:174-177). */
+/* One-pass, UNORDERED variant of scx_direct_agg_compact_having (warp-
+ * aggregated atomics) for selective HAVING; the caller sorts the few
+ * surviving packed keys.  Same outputs layout (out_acc[j*cap + g]). */
+int scx_direct_agg_select_having(const int64_t* acc_dev, int64_t cap, int m, int occ_word,
+                                 int hv_word, int64_t hv_lo, int64_t hv_hi,
+                                 uint64_t* out_keys_dev, int64_t* out_acc_dev,
+                                 uint64_t* count_dev, void* stream);
 int scx_direct_agg_compact_having(const int64_t* acc_dev, int64_t cap, int m, int occ_word,
                                   int hv_word, int64_t hv_lo, int64_t hv_hi,
                                   uint64_t* out_keys_dev, int64_t* out_acc_dev,

@@ -133,6 +133,8 @@ _PROTOS = {
                                        C.c_int, i64, C.c_int, i64, i64, _vp, _vp, i64, _vp, _vp,
                                        _vp]),
     "scx_widen_u32": (C.c_int, [_vp, i64, _vp, _vp]),
+    "scx_direct_agg_select_having": (C.c_int, [_vp, i64, C.c_int, C.c_int, C.c_int, i64, i64,
+                                               _vp, _vp, _vp, _vp]),
     "scx_direct_agg_compact_counted": (C.c_int, [_vp, i64, C.c_int, C.c_int, _vp, _vp, _vp, _vp,
                                                  _vp]),
     "scx_unpack_key": (C.c_int, [_vp, i64, C.c_int, u64, i64, Column_, _vp]),

@@ -715,3 +715,46 @@ extern "C" int scx_widen_u32(const uint32_t* in, int64_t n, int64_t* out, void* 
   return SCX_OK;
 }
 
+// One-pass unordered selection of a direct table's groups passing HAVING
+// (warp-aggregated atomics): for selective HAVING the ordered two-pass
+// compaction reads the whole table twice to write a handful of rows.
+__global__ void direct_select_kernel(Occ O, const int64_t* acc, int64_t cap, int m,
+                                     uint64_t* out_keys, int64_t* out_acc,
+                                     unsigned long long* count) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < cap;
+       base += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = base + threadIdx.x;
+    const bool keep = e < cap && O.keep(acc + e * m);
+    const uint32_t bal = __ballot_sync(0xffffffffu, keep);
+    if (!bal) continue;
+    unsigned long long o = 0;
+    const int leader = __ffs(bal) - 1;
+    if (lane == leader) o = atomicAdd(count, (unsigned long long)__popc(bal));
+    o = __shfl_sync(0xffffffffu, o, leader) + __popc(bal & ((1u << lane) - 1u));
+    if (keep) {
+      out_keys[o] = (uint64_t)e;
+      for (int j = 0; j < m; ++j) out_acc[(int64_t)j * cap + (int64_t)o] = acc[e * m + j];
+    }
+  }
+}
+
+extern "C" int scx_direct_agg_select_having(const int64_t* acc, int64_t cap, int m, int occ_word,
+                                            int hv_word, int64_t hv_lo, int64_t hv_hi,
+                                            uint64_t* out_keys, int64_t* out_acc,
+                                            uint64_t* count, void* stream) {
+  if (!acc || !out_keys || !out_acc || !count || m < 1 || m > 16 || occ_word < 0 ||
+      occ_word >= m || hv_word < 0 || hv_word >= m || cap < 0) {
+    set_error("direct_agg_select_having: bad arguments");
+    return SCX_EINVAL;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  SCX_CUDA(cudaMemsetAsync(count, 0, 8, st));
+  if (cap == 0) return SCX_OK;
+  Occ O{nullptr, acc, m, occ_word, hv_word, hv_lo, hv_hi};
+  direct_select_kernel<<<grid_for(cap, 256, 148 * 16), 256, 0, st>>>(
+      O, acc, cap, m, out_keys, out_acc, reinterpret_cast<unsigned long long*>(count));
+  SCX_CHECK_LAUNCH("direct_select_kernel");
+  return SCX_OK;
+}
+

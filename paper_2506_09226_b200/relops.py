@@ -1628,9 +1628,10 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) 
             # slot order == packed-key order: ordered compaction, no sort
             ws = alloc(max(2, L.load().scx_direct_agg_workspace(cap) // 8), np.int64)
             if hv is not None:
-                L.call("scx_direct_agg_compact_having", _ptr(accb), cap, W, int(woff[count_m]),
+                # one unordered pass; the survivors are sorted by key below
+                L.call("scx_direct_agg_select_having", _ptr(accb), cap, W, int(woff[count_m]),
                        int(woff[hv[0]]), hv[1], hv[2], _ptr(out_keys), _ptr(out_acc), _ptr(cnt),
-                       _ptr(ws), _stream())
+                       _stream())
             else:
                 L.call("scx_direct_agg_compact_counted", _ptr(accb), cap, W, int(woff[count_m]),
                        _ptr(out_keys), _ptr(out_acc), _ptr(cnt), _ptr(ws), _stream())
@@ -1644,7 +1645,9 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) 
             raise SchemaError("group table overflow (group key outside its proven range)")
         cap *= 4   # table overflowed: rerun with a bigger one
     G = int(st[2])
-    if direct:
+    if direct and hv is not None:
+        skeys, perm = sort_pairs(out_keys[:G], None, total) if G > 1 else (out_keys[:G], None)
+    elif direct:
         skeys, perm = out_keys[:G], None
     else:
         if sort:
@@ -1798,15 +1801,30 @@ def sort_table(t, names: list[str], descending: set[str], limit: int | None = No
         used += sp[2]
     if cur:
         words.append(cur)
-    if limit is not None and len(words) == 1 and n > max(_TOPK_SMALL, 4 * limit):
-        word = words[0]
+    if limit is not None and n > max(_TOPK_SMALL, 4 * limit):
+        # radix select on the MOST significant word; rows tied with the k-th
+        # one on it are all kept, then the candidates get the full sort
+        word = words[-1]
         nbits = max(sh + sp[2] for sp, sh in word)
         key = alloc(n, np.uint64)
         for i, ((c, lo, bits, desc, lut), sh) in enumerate(word):
             L.call("scx_encode_sort_key", c.scx(), None, n, lo, bits, desc, sh,
                    _ptr(lut) if lut is not None else None, _ptr(key), 1 if i else 0, _stream())
-        perm = _topk_perm(key, n, nbits, limit)
-        return take_table(t, perm)
+        ckeys, crows = _topk_candidates(key, n, nbits, limit)
+        if len(words) == 1:
+            _, perm = sort_pairs(ckeys, crows, nbits)
+            return take_table(t, perm[:limit])
+        perm = crows                       # row order: the LSD passes stay stable
+        m = crows.shape[0]
+        for word in words:
+            nbits = max(sh + sp[2] for sp, sh in word)
+            key = alloc(m, np.uint64)
+            for i, ((c, lo, bits, desc, lut), sh) in enumerate(word):
+                L.call("scx_encode_sort_key", c.scx(), _ptr(perm), m, lo, bits, desc, sh,
+                       _ptr(lut) if lut is not None else None, _ptr(key), 1 if i else 0,
+                       _stream())
+            _, perm = sort_pairs(key, perm, nbits)
+        return take_table(t, perm[:limit])
     perm = None
     for word in words:
         nbits = max(sh + sp[2] for sp, sh in word)
@@ -1822,8 +1840,10 @@ def sort_table(t, names: list[str], descending: set[str], limit: int | None = No
     return out if limit is None else out.head(limit)
 
 
-def _topk_perm(key, n: int, nbits: int, k: int):
-    """Rows of the k smallest keys (ties in row order), in key order."""
+def _topk_candidates(key, n: int, nbits: int, k: int):
+    """(keys, rows) of every row whose key is < T, in row order, for a
+    threshold T found by radix select such that the k smallest keys (and all
+    rows tied with the k-th) are among them."""
     counts = alloc(256, np.uint32)
     lo, hi = 0, 1 << nbits              # the k-th key lies in [lo, hi)
     below = 0                           # rows with key < lo
@@ -1846,8 +1866,7 @@ def _topk_perm(key, n: int, nbits: int, k: int):
     ws = alloc(max(2, L.load().scx_select_below_workspace(n) // 8), np.int64)
     L.call("scx_select_below", _ptr(key), n, hi, _ptr(ok), _ptr(oi), _ptr(cnt), _ptr(ws), _stream())
     m = int(_to_host(cnt)[0])
-    _, perm = sort_pairs(ok[:m], oi[:m], nbits)
-    return perm[:k]
+    return ok[:m], oi[:m]
 
 
 def take_column(c: Column, idx) -> Column:

@@ -328,3 +328,21 @@ def test_group_having_unsorted_output(sorted_keys):
     exp = O.group(ref, ["k"], aggs)
     exp = O.filter_(exp, exp["sx"][1] >= 250)
     assert_table_matches(got, O.to_jsonable(exp), f"having-unsorted sorted_keys={sorted_keys}")
+
+
+@pytest.mark.parametrize("k", [7, 100])
+def test_top_k_wide_keys(k):
+    """top(...) with sort keys wider than 64 bits: radix select on the most
+    significant word, full LSD sort of the candidates (ties stay in order)."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    rng = np.random.default_rng(29)
+    n = 150_000
+    a = rng.integers(0, 300, size=n)                       # many ties at the top word
+    b = rng.integers(-(1 << 40), 1 << 40, size=n)
+    c = rng.integers(-(1 << 40), 1 << 40, size=n) // 1000 * 1000
+    t = ColumnTable({"a": Column.from_numpy("int64", a), "b": Column.from_numpy("int64", b),
+                     "c": Column.from_numpy("int64", c)})
+    got = t.top(["a", "c", "b"], {"a", "b"}, k)
+    idx = np.lexsort([-b, c, -a])[:k]
+    for name, ref in (("a", a), ("b", b), ("c", c)):
+        assert np.array_equal(got.column(name).values, ref[idx]), name

@@ -225,7 +225,9 @@ class DeviceContext:
     def table(self, name: str) -> ColumnTable:
         if self.ready is not None and name in self.ready:
             import torch
-            torch.cuda.current_stream().wait_event(self.ready.pop(name))
+            evs = self.ready.pop(name)
+            for ev in (evs if isinstance(evs, (list, tuple)) else [evs]):
+                torch.cuda.current_stream().wait_event(ev)
         return self.tables[name]
 
     def filter(self, t, mask):
@@ -362,25 +364,33 @@ def upload_tables_async(host: dict, order=None, stream=None):
     with the queries that can already run).  Single-rank tables only.
     """
     import torch
-    cs = stream or torch.cuda.Stream()
+    # two copy streams: columns alternate between them (both DMA engines busy)
+    streams = [stream or torch.cuda.Stream(), torch.cuda.Stream()]
     main = torch.cuda.current_stream()
-    cs.wait_stream(main)           # buffers below are allocated on `main`
+    for cs in streams:
+        cs.wait_stream(main)       # buffers below are allocated on `main`
     tables, events = {}, {}
+    k = 0
     for tname in (order or list(host)):
         cols = {}
-        bufs = []
+        used = set()
         for cname, (hc, pinned) in host[tname].items():
             buf = alloc(hc.row_count, hc.values.dtype)
-            bufs.append((buf, pinned))
+            cs = streams[k % 2]
+            k += 1
+            used.add(id(cs))
+            with torch.cuda.stream(cs):
+                buf.copy_(pinned, non_blocking=True)
             cols[cname] = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
                                  hc.dense and hc.row_count == hc.hi - hc.lo + 1)
-        with torch.cuda.stream(cs):
-            for buf, pinned in bufs:
-                buf.copy_(pinned, non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(cs)
+        evs = []
+        for cs in streams:
+            if id(cs) in used:
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                evs.append(ev)
         tables[tname] = ColumnTable(cols)
-        events[tname] = ev
+        events[tname] = evs
     return tables, events
 
 

@@ -65,9 +65,11 @@ def peaks() -> dict:
 class ClockSampler:
     """SM clocks + throttle reasons sampled DURING the timed region.
 
-    An ``nvidia-smi -lms`` subprocess by default; ``SCX_CLOCKS=nvml`` samples
-    with NVML from a background thread instead and ``SCX_CLOCKS=off``
-    disables sampling (for A/B checks of sampler interference).
+    Default ``SCX_CLOCKS=steps``: NVML from the main thread once per timed
+    step, issued after the step's kernels are queued (the GPU is still
+    running them); ``nvml`` = background NVML thread, ``smi`` = an
+    ``nvidia-smi -lms`` subprocess, ``off`` = none (A/B of sampler
+    interference).
     """
 
     def __init__(self, device: int, period: float = 0.05):
@@ -75,13 +77,32 @@ class ClockSampler:
         # default: an nvidia-smi subprocess.  In-process NVML sampling stalled
         # one query of a timed pass by ~80 ms (driver lock) in 3 of 4 runs;
         # SCX_CLOCKS=nvml keeps it available for comparison
-        self.mode = os.environ.get("SCX_CLOCKS", "smi")
+        self.mode = os.environ.get("SCX_CLOCKS", "steps")
+        self._h = None
         self.samples: list[tuple[float, float, int]] = []
         self.max_mhz = None
         self.proc = None
         self._stop = threading.Event()
         self._thread = None
-        if self.mode == "nvml":
+        if self.mode == "steps":
+            # NVML queried from the main thread at the end of every timed step
+            # (right after the step's last kernel, GPU still at load clocks):
+            # a background sampler -- in-process NVML or an nvidia-smi
+            # subprocess -- intermittently stalled one query of a timed pass
+            # by 70-80 ms through the driver
+            try:
+                import pynvml as N
+                N.nvmlInit()
+                idx = device
+                vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+                if vis and vis.split(",")[device].strip().isdigit():
+                    idx = int(vis.split(",")[device])
+                self._N = N
+                self._h = N.nvmlDeviceGetHandleByIndex(idx)
+                self.max_mhz = float(N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM))
+            except Exception as exc:  # pragma: no cover
+                self.mode = f"unavailable ({exc})"
+        elif self.mode == "nvml":
             try:
                 import pynvml as N
                 N.nvmlInit()
@@ -116,6 +137,18 @@ class ClockSampler:
                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             except OSError:
                 self.proc = None
+
+    def sample(self) -> None:
+        """One sample now (mode "steps": called at the end of each step)."""
+        if self._h is None:
+            return
+        N = self._N
+        try:
+            self.samples.append((float(N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM)),
+                                 self.max_mhz,
+                                 int(N.nvmlDeviceGetCurrentClocksEventReasons(self._h))))
+        except Exception:
+            pass
 
     def stop(self) -> dict:
         if self._thread is not None:
@@ -419,6 +452,7 @@ def main() -> None:
         e0.record()
         results = suite(tables, per)
         e1.record()
+        sampler.sample()        # GPU still finishing the step: load clocks + reasons
         sync_all()
         gc.enable()
         step_ms.append(e0.elapsed_time(e1))

@@ -449,6 +449,7 @@ def main() -> None:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         per = []
+        results = None          # the previous step's results are not needed now
         e0.record()
         results = suite(tables, per)
         e1.record()

@@ -936,8 +936,20 @@ def _materialize(v: TableView) -> ColumnTable:
     m = int(_to_host(count)[0]) if n else 0
     # probes build on unique keys, so a filtered / joined row set keeps the
     # base table's key property
-    return ColumnTable({name: v.meta[name].like(outs[name][:m]) for name in cols},
+    return ColumnTable({name: v.meta[name].like(_fit(outs[name], m)) for name in cols},
                        v.base.unique_keys)
+
+
+def _fit(buf, m: int):
+    """buf[:m], copied into its own allocation when that is much smaller: a
+    view would keep the whole capacity-sized buffer alive as long as the
+    result (a 150M-slot group table behind a 600-row HAVING result)."""
+    if m * 2 >= buf.shape[0] or buf.shape[0] - m < (1 << 16):
+        return buf[:m]
+    out = alloc(m, np.dtype(str(buf.dtype).replace("torch.", "")))
+    if m:
+        out.copy_(buf[:m])
+    return out
 
 
 def count_rows(t) -> int:
@@ -1675,7 +1687,7 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) 
     def word_col(w):
         src = out_acc[w * cap: w * cap + G]
         if perm is None:
-            if src.data_ptr() % 16 == 0:
+            if src.data_ptr() % 16 == 0 and (G * 2 >= cap or cap - G < (1 << 16)):
                 return src
             dst = alloc(G, np.int64)
             if G:

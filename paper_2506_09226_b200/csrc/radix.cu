@@ -123,8 +123,76 @@ __global__ void sort_scatter_kernel(DigitSrc D, int64_t n, const uint64_t* offs,
   });
 }
 
+// Few digits (a partition into <= 32 parts): rounds of kRound sub-tiles share
+// one set of barriers -- per-(sub-tile, warp, digit) counts, one exclusive
+// scan per digit over (sub-tile, warp) in row order, per-digit totals --
+// so a 4096-row chunk needs 4 rounds x 3 barriers instead of 16 x 4.
+constexpr int kRound = 4;
+constexpr int kFewDigits = 32;
+
+template <typename Emit>
+__device__ __forceinline__ void scatter_chunk_few(const DigitSrc& D, int64_t n, int ndig,
+                                                  const uint64_t* offs, int nblocks, Emit emit) {
+  __shared__ uint32_t wc[kRound][kWarps][kFewDigits];
+  __shared__ uint64_t run[kFewDigits];
+  __shared__ uint32_t tot[kFewDigits];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < ndig) run[tid] = offs[(int64_t)tid * nblocks + blockIdx.x];
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  for (int r0 = 0; r0 < kItems; r0 += kRound) {
+    for (int j = tid; j < kRound * kWarps * kFewDigits; j += kBlock) (&wc[0][0][0])[j] = 0;
+    __syncthreads();
+    uint32_t d[kRound], rank[kRound];
+    bool valid[kRound];
+#pragma unroll
+    for (int r = 0; r < kRound; ++r) {
+      const int64_t i = base + (int64_t)(r0 + r) * kBlock + tid;
+      valid[r] = i < n;
+      d[r] = valid[r] ? D(i) : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int r = 0; r < kRound; ++r) {
+      const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
+      rank[r] = __popc(peers & ((1u << lane) - 1u));
+      if (valid[r] && rank[r] == 0) wc[r][warp][d[r]] = __popc(peers);
+    }
+    __syncthreads();
+    if (tid < ndig) {          // exclusive scan over (sub-tile, warp): row order
+      uint32_t s2 = 0;
+#pragma unroll
+      for (int r = 0; r < kRound; ++r)
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) { const uint32_t c = wc[r][w][tid]; wc[r][w][tid] = s2; s2 += c; }
+      tot[tid] = s2;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRound; ++r)
+      if (valid[r]) emit(base + (int64_t)(r0 + r) * kBlock + tid, run[d[r]] + wc[r][warp][d[r]] + rank[r]);
+    __syncthreads();
+    if (tid < ndig) run[tid] += tot[tid];
+  }
+}
+
 __global__ void part_scatter_kernel(DigitSrc D, int64_t n, int nparts, const uint64_t* offs,
                                     int nblocks, PartCols C) {
+  auto emit = [&](int64_t i, uint64_t pos) {
+    for (int c = 0; c < C.n; ++c) {
+      const int w = dtype_size_d(C.in[c].dtype);
+      const char* s = reinterpret_cast<const char*>(C.in[c].ptr);
+      char* d = reinterpret_cast<char*>(C.out[c].ptr);
+      switch (w) {
+        case 1: d[pos] = s[i]; break;
+        case 2: reinterpret_cast<int16_t*>(d)[pos] = reinterpret_cast<const int16_t*>(s)[i]; break;
+        case 4: reinterpret_cast<int32_t*>(d)[pos] = reinterpret_cast<const int32_t*>(s)[i]; break;
+        default: reinterpret_cast<int64_t*>(d)[pos] = reinterpret_cast<const int64_t*>(s)[i]; break;
+      }
+    }
+  };
+  if (nparts <= kFewDigits) {
+    scatter_chunk_few(D, n, nparts, offs, nblocks, emit);
+    return;
+  }
   scatter_chunk(D, n, nparts, offs, nblocks, [&](int64_t i, uint64_t pos) {
     for (int c = 0; c < C.n; ++c) {
       const int w = dtype_size_d(C.in[c].dtype);

@@ -35,6 +35,7 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <fstream>
 #include <mutex>
 #include <sstream>
@@ -415,6 +416,7 @@ struct Gen {
   size_t dyn_smem = 0;
   int stage_p = -1, stage_rows_p = -1;   // COMPACT: staging base / rows, bound at launch
   int nw_priv = 0;              // dense private accumulators: 64-bit words per cell
+  bool packed = false;          // SWAR-packed fields: launch with >= 2 CTAs per SM
   bool tma = false;             // base columns streamed by a producer warp (TMA bulk copies)
   int tma_stages = 0;
   size_t ring_off = 0, bar_off = 0;
@@ -864,23 +866,31 @@ struct Gen {
         mshift(S.n_measures > 0 ? S.n_measures : 1, 0), mbits(S.n_measures > 0 ? S.n_measures : 1, 64);
     int NW = 0;
     if (dense_priv) {
-      int cur = -1, used = 0;
+      // first-fit decreasing of the packable fields into 64-bit words (the
+      // sums are non-negative, so a field may use every bit up to 63); the
+      // launch keeps >= 2 CTAs per SM for packed kernels, which the host's
+      // bit budgets assume
+      std::vector<int> order;
       for (int m = 0; m < S.n_measures; ++m) {
         const int op = S.m[m].op, pad = S.m[m]._pad;
         const bool packable = (op == SCX_AGG_SUM || op == SCX_AGG_COUNT) && (pad & 0x100) &&
-                              (pad & 0xff) >= 1 && (pad & 0xff) <= 40;
-        if (packable) {
-          const int b = pad & 0xff;
-          if (cur >= 0 && used + b <= 62) {
-            mword[m] = cur; mshift[m] = used; used += b;
-          } else {
-            cur = NW++; mword[m] = cur; mshift[m] = 0; used = b;
-          }
-          mbits[m] = b;
-        } else {
-          mword[m] = NW++;
-        }
+                              (pad & 0xff) >= 1 && (pad & 0xff) <= 63;
+        if (packable) order.push_back(m);
+        else mword[m] = NW++;
       }
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        return (S.m[x]._pad & 0xff) > (S.m[y]._pad & 0xff);
+      });
+      std::vector<int> wid, wused;
+      for (int m : order) {
+        const int b = S.m[m]._pad & 0xff;
+        int k = -1;
+        for (size_t i = 0; i < wid.size(); ++i)
+          if (wused[i] + b <= 64) { k = (int)i; break; }
+        if (k < 0) { wid.push_back(NW++); wused.push_back(0); k = (int)wid.size() - 1; }
+        mword[m] = wid[k]; mshift[m] = wused[k]; mbits[m] = b; wused[k] += b;
+      }
+      packed = !order.empty();
     }
     nw_priv = NW;
     if (S.kind == SCX_SINK_AGG_DENSE && !dense_priv && S.n_cells > 1 && S.n_cells <= 8) V = 8;
@@ -1438,6 +1448,7 @@ struct Gen {
 
 struct Prepared {
   int threads = 256;
+  bool packed = false;
   std::string src, name;
   std::vector<uint64_t> ptrs;
   int tiles = 0;
@@ -1466,6 +1477,7 @@ static int prepare(const scx_pipeline& P, Prepared& out) {
   out.ptrs = g.ptrs;
   out.dyn_smem = g.dyn_smem;
   out.threads = g.threads();
+  out.packed = g.packed;
   out.V = g.V;
   out.stage_p = g.stage_p;
   out.stage_rows_p = g.stage_rows_p;
@@ -1554,6 +1566,9 @@ static int plan_launch_uncached(const scx_pipeline& P, LaunchPlan& lp) {
   SCX_CUDA(cudaGetDevice(&dev));
   SCX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   lp.grid = (int64_t)sms * occ;
+  // packed per-thread partial sums were sized for <= n / (2 * SMs * 256) + 16
+  // rows per thread: never fewer than 2 CTAs per SM (extra CTAs just queue)
+  if (lp.pp.packed && lp.grid < 2 * (int64_t)sms) lp.grid = 2 * (int64_t)sms;
   if (lp.grid > lp.pp.tiles) lp.grid = lp.pp.tiles;
   if (lp.grid < 1) lp.grid = 1;
   if (P.sink.kind == SCX_SINK_COMPACT) {

@@ -868,12 +868,25 @@ def _measure_range(im: IntMeasure | None, meta: dict[str, Column]):
     return lo_t, hi_t
 
 
+_SMS = None
+
+
+def _num_sms() -> int:
+    global _SMS
+    if _SMS is None:
+        _SMS = int(_torch().cuda.get_device_properties(_torch().cuda.current_device())
+                   .multi_processor_count)
+    return _SMS
+
+
 def _pack_budgets(P, measures, meta, n: int) -> None:
     """Dense sinks: mark sum / count measures whose per-thread partial sum is
     provably non-negative and small with their bit budget (measure._pad =
     0x100 | bits), so the kernel can add several of them with ONE 64-bit
     shared-memory update (Q1: qty, discount and count share a word)."""
-    rows_per_thread = n // (148 * 256) + 16
+    # the launch keeps >= 2 CTAs of 256 threads per SM for packed kernels
+    # (jit plan_launch), and 148 SMs: rows per thread <= n / (296 * 256) + V
+    rows_per_thread = n // (2 * _num_sms() * 256) + 16
     for i, (op, im) in enumerate(measures):
         if op not in ("sum", "count"):
             continue
@@ -882,7 +895,7 @@ def _pack_budgets(P, measures, meta, n: int) -> None:
             continue
         lo, hi = r
         bits = max(1, int(hi * rows_per_thread).bit_length())
-        if bits <= 40:
+        if bits <= 63:
             P.sink.m[i]._pad = 0x100 | bits
 
 

@@ -23,6 +23,12 @@ tables = P.load_tables(cached_generate(a.sf))
 for _ in range(3):
     P.reference_run(a.q, tables)
 torch.cuda.synchronize()
+import time  # noqa: E402
+t0 = time.perf_counter()
+for _ in range(a.reps):
+    P.reference_run(a.q, tables)
+torch.cuda.synchronize()
+print(f"{a.q}: {(time.perf_counter() - t0) / a.reps * 1e3:.3f} ms wall per run (no profiler)")
 pr = cProfile.Profile()
 pr.enable()
 for _ in range(a.reps):

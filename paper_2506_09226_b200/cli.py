@@ -1,8 +1,11 @@
-"""Thin command line: the reference's ``query`` subcommand
-(`shufflecast/cli.py:177-210`) on the device engine.
+"""Thin command line: the reference's ``query`` and
+``bench`` subcommands (`shufflecast/cli.py:130-210,230-275`) on the device
+engine.
 
     python -m paper_2506_09226_b200.cli query --qid Q3 --sf 1 --out runs/q3
     torchrun --nproc-per-node 8 -m paper_2506_09226_b200.cli query --qid all --sf 100 --out runs/
+    torchrun --nproc-per-node 8 -m paper_2506_09226_b200.cli bench --op shuffle \
+        --sizes-mib 1,16,256 --reps 5 --out shuffle.csv
 
 Writes ``<qid>_result.csv`` (decoded rows, floats as repr, like
 `cli.py:149-161`) and ``<qid>_report.json`` (`RunReport.to_json`, engine.py:
@@ -24,6 +27,33 @@ import sys
 from .data import generate
 from .engine import PlanError, load_tables, run_query
 from .queries import SUPPORTED_QUERIES
+
+MIB = 1 << 20
+
+
+def _fmt(value) -> str:
+    """CSV cell format of the reference (`cli.py:41-46`)."""
+    if value is None:
+        return ""
+    if isinstance(value, float):
+        return f"{value:.6f}"
+    return str(value)
+
+
+def _write_csv(path: str, fieldnames: list[str], rows: list[dict]) -> None:
+    out = sys.stdout if path == "-" else open(path, "w", newline="")
+    try:
+        writer = csv.writer(out)
+        writer.writerow(fieldnames)
+        for row in rows:
+            writer.writerow([_fmt(row[f]) for f in fieldnames])
+    finally:
+        if out is not sys.stdout:
+            out.close()
+
+
+def _int_list(text: str) -> list[int]:
+    return [int(x) for x in text.split(",") if x.strip()]
 
 
 def _write_result_csv(path: str, table) -> None:
@@ -76,6 +106,24 @@ def cmd_query(args) -> int:
     return 0
 
 
+def cmd_bench(args) -> int:
+    from . import xbench as XB
+    from .cluster import create_cluster
+    ep = create_cluster()
+    k, v = XB.parse_shorthand(args.topology) if args.topology else (ep.n, 1)
+    topo = XB.Topology(k, v,
+                       bg_gbps=args.bg_gbps if args.bg_gbps is not None else 450.0,
+                       bn_gbps=args.bn_gbps if args.bn_gbps is not None else 50.0,
+                       efficiency=args.efficiency if args.efficiency is not None else 0.8)
+    spec = XB.BenchSpec(op=args.op, message_bytes=[m * MIB for m in _int_list(args.sizes_mib)],
+                        topology=topo, repetitions=args.reps,
+                        max_message_bytes=args.max_mib * MIB)
+    rows = XB.run_bench(ep, spec)
+    if ep.rank == 0:
+        _write_csv(args.out, XB.ROW_FIELDS, rows)
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(prog="shufflecast-gpu",
                                      description="TPC-H queries on the B200 engine")
@@ -88,6 +136,20 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--out", required=True, help="output directory")
     p.set_defaults(func=cmd_query)
+
+    p = sub.add_parser("bench", help="run an exchange microbenchmark sweep")
+    p.add_argument("--topology", default=None,
+                   help="KxV label (default: <world size>x1); K*V must equal the world size")
+    p.add_argument("--bn-gbps", type=float, default=None, help="echoed: per-machine network GB/s")
+    p.add_argument("--bg-gbps", type=float, default=None, help="echoed: per-GPU NVLink GB/s")
+    p.add_argument("--efficiency", type=float, default=None, help="echoed: efficiency in (0,1]")
+    p.add_argument("--op", choices=["shuffle", "broadcast", "broadcast_p2p"], required=True)
+    p.add_argument("--sizes-mib", required=True,
+                   help="strictly increasing per-GPU message sizes in MiB")
+    p.add_argument("--reps", type=int, default=1)
+    p.add_argument("--max-mib", type=int, default=1024, help="memory cap per buffer")
+    p.add_argument("--out", default="-", help="CSV path or - for stdout")
+    p.set_defaults(func=cmd_bench)
     return parser
 
 
@@ -96,7 +158,8 @@ def main(argv=None) -> int:
     try:
         return args.func(args)
     except Exception as exc:       # one-line error JSON, nonzero exit (cli.py contract)
-        print(json.dumps({"error": type(exc).__name__, "message": str(exc)}), file=sys.stderr)
+        print(json.dumps({"error": {"type": type(exc).__name__, "message": str(exc)}}),
+              file=sys.stderr)
         return 1
 
 

@@ -334,6 +334,8 @@ def main() -> None:
     ap.add_argument("--cpu-sample-sf", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--shuffle-gib", type=float, default=1.0)
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("SCX_BENCH_STREAMS", "3")),
+                    help="host threads / CUDA streams running the suite's queries concurrently")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -377,6 +379,8 @@ def main() -> None:
         return v[0].value
 
     def suite(tabs, per_query=None):
+        if n_streams > 1:
+            return suite_concurrent(tabs, per_query)
         results = {}
         for q in QUERIES:
             if dbg:
@@ -399,6 +403,66 @@ def main() -> None:
                 per_query.append((q, e0, e1))
         return results
 
+    def suite_concurrent(tabs, per_query=None):
+        """The same 22 queries, pulled in order by `n_streams` host threads,
+        each issuing on its own CUDA stream: one query's plan building and
+        result finishing overlap another's kernels.  The step's end event
+        waits for every worker stream."""
+        import threading
+        start = torch.cuda.Event()
+        start.record()
+        results, errors, lock = {}, [], threading.Lock()
+        done = [torch.cuda.Event() for _ in worker_streams]
+
+        def work(i):
+            try:
+                torch.cuda.set_device(dev)
+                s = worker_streams[i]
+                with torch.cuda.stream(s):
+                    s.wait_event(start)
+                    for q in assignment[i]:
+                        if per_query is not None:
+                            e0 = torch.cuda.Event(enable_timing=True)
+                            e0.record()
+                        ctx = DeviceContext(ep, tabs, "default", "default_keys", timed=False)
+                        r = PLAN_FUNCTIONS[q](ctx)
+                        results[q] = r.materialize() if r is not None else None
+                        if per_query is not None:
+                            e1 = torch.cuda.Event(enable_timing=True)
+                            e1.record()
+                            with lock:
+                                per_query.append((q, e0, e1))
+                    done[i].record(s)
+            except BaseException as exc:     # re-raised on the main thread
+                errors.append(exc)
+
+        threads = [threading.Thread(target=work, args=(i,)) for i in range(n_streams)]
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
+        if errors:
+            raise errors[0]
+        cur = torch.cuda.current_stream()
+        for ev in done:
+            cur.wait_event(ev)
+        return {q: results[q] for q in QUERIES}
+
+    # collectives on one communicator must be issued in the same order on every
+    # rank, which concurrent host threads cannot promise: N > 1 runs one stream
+    n_streams = max(1, args.streams) if ep.n == 1 else 1
+    # static longest-first assignment of queries to streams (by the round-1
+    # single-stream per-query times, ms) so every step repeats the same
+    # per-stream allocation pattern the warm-up passes already cached
+    q_cost = {'Q1': 2.3, 'Q2': 4.0, 'Q3': 5.3, 'Q4': 1.9, 'Q5': 4.8, 'Q6': 1.0, 'Q7': 5.5, 'Q8': 4.5, 'Q9': 9.9, 'Q10': 3.3, 'Q11': 2.0, 'Q12': 2.3, 'Q13': 3.8, 'Q14': 2.2, 'Q15': 2.1, 'Q16': 4.9, 'Q17': 4.0, 'Q18': 2.9, 'Q19': 3.0, 'Q20': 5.5, 'Q21': 7.8, 'Q22': 1.8}
+    assignment = [[] for _ in range(n_streams)]
+    load = [0.0] * n_streams
+    for q in sorted(QUERIES, key=lambda x: -q_cost.get(x, 1.0)):
+        j = load.index(min(load))
+        assignment[j].append(q)
+        load[j] += q_cost.get(q, 1.0)
+    assignment = [[q for q in QUERIES if q in a] for a in assignment]
+    worker_streams = [torch.cuda.Stream() for _ in range(n_streams)] if n_streams > 1 else []
     flush = P.table.alloc(64 << 20, np.int64)    # 512 MB > 126 MB L2
 
     def flush_l2():
@@ -596,7 +660,8 @@ def main() -> None:
                                    f"14/19 + builder-written 16, one pass = one step)",
                        "sf": args.sf, "queries": list(QUERIES),
                        "parallelism": f"dp{ep.n}", "l2": "flushed between steps (512 MB write)",
-                       "layout": "narrowed fixed-point columns in HBM"},
+                       "layout": "narrowed fixed-point columns in HBM",
+                       "streams": n_streams},
             "e2e": {"value": round(e2e_s, 6), "unit": "s", "results_match_device_run": e2e_match,
                     "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes},
@@ -606,6 +671,9 @@ def main() -> None:
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_total": int(launches),
             "per_query": per_query,
+            "per_query_note": ("s = interval from a query's first to its last event on its own "
+                               "stream; with streams > 1 queries overlap, so the s values sum "
+                               "to more than the step and roof_frac is a lower bound"),
             "shuffle": shuffle,
             "suite_roofline": {"t_roof_s": round(roof_total, 6),
                                "frac": round(roof_total / value, 4),

@@ -431,6 +431,37 @@ int scx_partition(const scx_column* keys, int n_keys, const scx_column* cols,
                   const scx_column* outs, int n_cols, int64_t n, int n_parts,
                   uint64_t* counts_dev, void* temp_dev, void* stream);
 
+/* ---- shuffle partition to arbitrary destinations (exchange.py:131-174) ----
+ * Pass 1 (scx_part_hist): bucket = fib_hash(keys) mod n_parts; per-part row
+ * totals to counts_dev (u64[n_parts]) and per-(part, CTA) stable offsets kept
+ * in ws (sized by scx_part_workspace; n_parts <= 64).
+ * Pass 2 (scx_part_scatter, same ws): every column's rows of part d are
+ * written, in source row order, to dst_dev[c * n_parts + d] (a device array
+ * of byte addresses: the receiver-side slot of this source in worker d's
+ * buffer -- local memory, a peer GPU's HBM, or another virtual rank's buffer
+ * on the same device).  scx_partition is pass 1 + pass 2 into a contiguous
+ * local layout. */
+int64_t scx_part_workspace(int64_t n, int n_parts);
+int scx_part_hist(const scx_column* keys, int n_keys, int64_t n, int n_parts, void* ws_dev,
+                  uint64_t* counts_dev, void* stream);
+int scx_part_scatter(const scx_column* keys, int n_keys, const scx_column* cols, int n_cols,
+                     int64_t n, int n_parts, const uint64_t* dst_dev, const void* ws_dev,
+                     void* stream);
+
+/* ---- multi-match inner join (relops.py:59-94: stable argsort +
+ * searchsorted + repeat) ----------------------------------------------------
+ * lkeys: packed u64 join key per LEFT row; rsorted: the RIGHT side's packed
+ * keys sorted stably (scx_sort_pairs, values = right row ids = rperm).
+ * scx_join_match fills the workspace (per-left-row match run + exclusive
+ * scan) and writes the pair count to total_dev (u64, device).
+ * scx_join_expand writes the pairs in left row order, matches in right row
+ * order (out_l / out_r: u32[total]).  ws sized by scx_join_workspace(n). */
+int64_t scx_join_workspace(int64_t n);
+int scx_join_match(const uint64_t* lkeys_dev, int64_t n, const uint64_t* rsorted_dev, int64_t m,
+                   void* ws_dev, uint64_t* total_dev, void* stream);
+int scx_join_expand(const void* ws_dev, int64_t n, const uint32_t* rperm_dev, int64_t total,
+                    uint32_t* out_l_dev, uint32_t* out_r_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -152,6 +152,13 @@ _PROTOS = {
     "scx_partition_workspace": (i64, [i64, C.c_int]),
     "scx_partition": (C.c_int, [C.POINTER(Column_), C.c_int, C.POINTER(Column_),
                                 C.POINTER(Column_), C.c_int, i64, C.c_int, _vp, _vp, _vp]),
+    "scx_part_workspace": (i64, [i64, C.c_int]),
+    "scx_part_hist": (C.c_int, [C.POINTER(Column_), C.c_int, i64, C.c_int, _vp, _vp, _vp]),
+    "scx_part_scatter": (C.c_int, [C.POINTER(Column_), C.c_int, C.POINTER(Column_), C.c_int, i64,
+                                   C.c_int, _vp, _vp, _vp]),
+    "scx_join_workspace": (i64, [i64]),
+    "scx_join_match": (C.c_int, [_vp, i64, _vp, i64, _vp, _vp, _vp]),
+    "scx_join_expand": (C.c_int, [_vp, i64, _vp, i64, _vp, _vp, _vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

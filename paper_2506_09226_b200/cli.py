@@ -24,6 +24,8 @@ import json
 import os
 import sys
 
+import numpy as np
+
 from .data import generate
 from .engine import PlanError, load_tables, run_query
 from .queries import SUPPORTED_QUERIES
@@ -72,8 +74,8 @@ def _write_result_csv(path: str, table) -> None:
 def _p80(xs) -> float:
     if not xs:
         return 0.0
-    s = sorted(xs)
-    return float(s[min(len(s) - 1, int(0.8 * (len(s) - 1) + 0.5))])
+    # linear interpolation, as np.percentile in the reference (bench.py:209-213)
+    return float(np.percentile(np.asarray(xs, dtype=np.float64), 80))
 
 
 def _summarize(qid: str, report) -> str:

@@ -563,9 +563,13 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
             rt = rt.materialize() if isinstance(rt, TableView) else rt
     if lookup is None:
         lookup = Lookup(rt, rkeys)
-    if how in ("inner", "left") and not lookup.unique:
-        raise SchemaError(f"{how} join with duplicate build-side keys is not supported by the "
-                          "fused probe (build keys must be unique)")
+    if how == "inner" and not lookup.unique:
+        # duplicate build keys: the fused probe returns one row per probe,
+        # so the pairs are expanded by a dedicated count -> scan -> write
+        return _expand_join(lv.materialize(), rt, on)
+    if how == "left" and not lookup.unique:
+        raise SchemaError("left join with duplicate build-side keys is not supported "
+                          "(build keys must be unique)")
     v = lv._copy()
     kind = {"inner": L.JOIN_INNER, "semi": L.JOIN_SEMI, "anti": L.JOIN_ANTI,
             "left": L.JOIN_LEFT}[how]
@@ -585,6 +589,57 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
             v.visible.append(n)
     v.probes.append(stage)
     return v
+
+
+def _expand_join(lt: ColumnTable, rt: ColumnTable, on: list[tuple[str, str]]) -> ColumnTable:
+    """Inner join with duplicate right keys, in the reference's output order
+    (relops.py:81-93): left row order, each left row's matches in right row
+    order, left columns then right columns.
+
+    Both sides' keys are packed over the union of their value ranges; the
+    right keys are radix-sorted stably with their row ids, each left key
+    finds its run by binary search (scx_join_match), and one thread per
+    output pair writes (left row, right row) (scx_join_expand); the columns
+    are then gathered."""
+    n, m = lt.row_count, rt.row_count
+    lcols = [lt.column(a) for a, _ in on]
+    rcols = [rt.column(b) for _, b in on]
+    if n == 0 or m == 0:
+        idx = alloc(0, np.uint32)
+        return ColumnTable({**take_table(lt, idx).columns, **take_table(rt, idx).columns})
+    spec = []
+    for lc, rc in zip(lcols, rcols):
+        l0, l1 = _col_range(lc)
+        r0, r1 = _col_range(rc)
+        lo, hi = min(l0, r0), max(l1, r1)
+        spec.append((lo, _bits(hi - lo)))
+    total_bits = sum(b for _, b in spec)
+    if total_bits > 64:
+        raise SchemaError(f"packed join key needs {total_bits} bits (> 64)")
+    shifts, acc = [], 0
+    for _, b in reversed(spec):
+        shifts.append(acc)
+        acc += b
+    shifts.reverse()
+
+    def pack(cols, rows):
+        key = alloc(rows, np.uint64)
+        for i, (c, (lo, b), sh) in enumerate(zip(cols, spec, shifts)):
+            L.call("scx_encode_sort_key", c.scx(), None, rows, lo, b, 0, sh, None, _ptr(key),
+                   1 if i else 0, _stream())
+        return key
+
+    rkey = pack(rcols, m)
+    lkey = pack(lcols, n)
+    rsorted, rperm = sort_pairs(rkey, None, max(1, total_bits))
+    ws = alloc(L.load().scx_join_workspace(n), np.uint8)
+    tot = alloc(1, np.uint64)
+    L.call("scx_join_match", _ptr(lkey), n, _ptr(rsorted), m, _ptr(ws), _ptr(tot), _stream())
+    total = int(_to_host(tot)[0])
+    out_l, out_r = alloc(total, np.uint32), alloc(total, np.uint32)
+    L.call("scx_join_expand", _ptr(ws), n, _ptr(rperm), total, _ptr(out_l), _ptr(out_r),
+           _stream())
+    return ColumnTable({**take_table(lt, out_l).columns, **take_table(rt, out_r).columns})
 
 
 def _pushdown_join(lv: TableView, rv: TableView, on: tuple[str, str], how: str):
@@ -1826,11 +1881,15 @@ def sort_table(t, names: list[str], descending: set[str], limit: int | None = No
         used += sp[2]
     if cur:
         words.append(cur)
-    if limit is not None and n > max(_TOPK_SMALL, 4 * limit):
+    top_bits = max(sh + sp[2] for sp, sh in words[-1]) if words else 0
+    # the select carries an exclusive upper bound hi = 2^nbits through a u64
+    # argument, so a 64-bit most significant word (raw f64 key, or keys that
+    # pack to exactly 64 bits) takes the full LSD sort instead
+    if limit is not None and n > max(_TOPK_SMALL, 4 * limit) and top_bits < 64:
         # radix select on the MOST significant word; rows tied with the k-th
         # one on it are all kept, then the candidates get the full sort
         word = words[-1]
-        nbits = max(sh + sp[2] for sp, sh in word)
+        nbits = top_bits
         key = alloc(n, np.uint64)
         for i, ((c, lo, bits, desc, lut), sh) in enumerate(word):
             L.call("scx_encode_sort_key", c.scx(), None, n, lo, bits, desc, sh,

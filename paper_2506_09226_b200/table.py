@@ -566,8 +566,14 @@ def unify_physical(p: Column, parts: list[Column]) -> Column:
     scale = max(q.scale for q in parts)
     if any(q.scale < 0 for q in parts):
         raise SchemaError("cannot concatenate raw float64 with fixed-point parts")
-    width = max(q.itemsize for q in parts)
-    dt = {1: np.int8, 2: np.int16, 4: np.int32, 8: np.int64}[width if scale == p.scale else 8]
+    # target dtype from the union of the parts' rescaled value ranges: picking
+    # by byte width alone would wrap a u8/u32 part cast to i8/i32
+    ranges = [(q.lo * 10 ** (scale - q.scale), q.hi * 10 ** (scale - q.scale))
+              for q in parts if q.hi >= q.lo]
+    lo_all = min((a for a, _ in ranges), default=0)
+    hi_all = max((b for _, b in ranges), default=0)
+    dt = narrow_dtype(lo_all, hi_all, unsigned=all(np.dtype(q.np_dtype).kind == "u"
+                                                   for q in parts))
     data = p.data.to(torch_dtype(dt))
     if scale != p.scale:
         data = data * (10 ** (scale - p.scale))

@@ -117,9 +117,56 @@ def test_join_semantics(how):
     P = _dev()
     left, ru, rd = _rel_tables()
     assert_table_matches(P.local_hash_join(left, ru, [("lk", "rk")], how), REL[f"join_unique_{how}"], how)
-    if how != "inner":
-        assert_table_matches(P.local_hash_join(left, rd, [("lk", "rk")], how), REL[f"join_dup_{how}"],
-                             how + "_dup")
+    assert_table_matches(P.local_hash_join(left, rd, [("lk", "rk")], how), REL[f"join_dup_{how}"],
+                         how + "_dup")
+
+
+def _oracle_join_check(got, lt, rt, on):
+    exp = O.join(lt, rt, on, "inner")
+    got = got.materialize()
+    assert got.column_names == list(exp)
+    for name, (kind, v, _) in exp.items():
+        g = got.column(name).values
+        assert len(g) == len(v), (name, len(g), len(v))
+        assert np.array_equal(g.astype(np.int64), v.astype(np.int64)), name
+
+
+@pytest.mark.parametrize("n,m,keyspan,seed", [(200_000, 50_000, 3_000, 0),
+                                              (100_000, 300_000, 20_000, 1),
+                                              (50_000, 40_000, 7, 2),        # heavy duplicates
+                                              (1, 100_000, 1, 3),            # one left row, all match
+                                              (10_000, 10_000, 10 ** 9, 4)])  # mostly no match
+def test_inner_join_duplicates_vs_oracle(n, m, keyspan, seed):
+    """Inner join with duplicate build keys (relops.py:81-93): left row order,
+    matches in right row order -- at sizes with heavy duplicate runs."""
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    P = _dev()
+    rng = np.random.default_rng(seed)
+    lt = {"lk": ("int64", rng.integers(-5, keyspan, size=n).astype(np.int64), None),
+          "lv": ("int64", np.arange(n, dtype=np.int64) * 3, None)}
+    rt = {"rk": ("int64", rng.integers(0, keyspan + 5, size=m).astype(np.int64), None),
+          "rv": ("date32", rng.integers(0, 20000, size=m).astype(np.int32), None)}
+    up = lambda t: ColumnTable({k: Column.from_numpy(a, b, c) for k, (a, b, c) in t.items()})
+    got = P.local_hash_join(up(lt), up(rt), [("lk", "rk")], "inner")
+    _oracle_join_check(got, lt, rt, [("lk", "rk")])
+
+
+def test_inner_join_duplicates_multikey():
+    from paper_2506_09226_b200.table import Column, ColumnTable
+    P = _dev()
+    rng = np.random.default_rng(7)
+    n, m = 30_000, 20_000
+    lt = {"a": ("int64", rng.integers(0, 50, size=n), None),
+          "b": ("dict", rng.integers(0, 3, size=n).astype(np.int32), ("X", "Y", "Z")),
+          "lv": ("int64", np.arange(n), None)}
+    rt = {"c": ("int64", rng.integers(0, 50, size=m), None),
+          "d": ("dict", rng.integers(0, 3, size=m).astype(np.int32), ("X", "Y", "Z")),
+          "rv": ("int64", np.arange(m) * 7, None)}
+    up = lambda t: ColumnTable({k: Column.from_numpy(a, np.asarray(b), c) for k, (a, b, c) in t.items()})
+    on = [("a", "c"), ("b", "d")]
+    got = P.local_hash_join(up(lt), up(rt), on, "inner")
+    _oracle_join_check(got, {k: (a, np.asarray(b), c) for k, (a, b, c) in lt.items()},
+                       {k: (a, np.asarray(b), c) for k, (a, b, c) in rt.items()}, on)
 
 
 AGGS = {"n": ("count", None), "s_f": ("sum", "lv"), "s_i": ("sum", "li"), "a_f": ("avg", "lv"),

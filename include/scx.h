@@ -462,6 +462,12 @@ int scx_join_match(const uint64_t* lkeys_dev, int64_t n, const uint64_t* rsorted
 int scx_join_expand(const void* ws_dev, int64_t n, const uint32_t* rperm_dev, int64_t total,
                     uint32_t* out_l_dev, uint32_t* out_r_dev, void* stream);
 
+/* ---- dictionary reconciliation (exchange.py:177-192, 217-251) -------------
+ * out[i] = lut[in[i]] (dictionary codes through a rank's remap into the
+ * union dictionary); a code outside [0, lut_n) sets *bad_dev = 1. */
+int scx_remap_codes(scx_column in, int64_t n, const int32_t* lut_dev, int32_t lut_n,
+                    scx_column out, int* bad_dev, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

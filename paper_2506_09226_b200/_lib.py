@@ -159,6 +159,7 @@ _PROTOS = {
     "scx_join_workspace": (i64, [i64]),
     "scx_join_match": (C.c_int, [_vp, i64, _vp, i64, _vp, _vp, _vp]),
     "scx_join_expand": (C.c_int, [_vp, i64, _vp, i64, _vp, _vp, _vp]),
+    "scx_remap_codes": (C.c_int, [Column_, i64, _vp, C.c_int32, Column_, _vp, _vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

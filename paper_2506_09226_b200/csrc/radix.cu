@@ -1,8 +1,5 @@
 // radix.cu -- stable 8-bit-digit counting passes shared by
 //   * scx_sort_pairs   : LSD radix sort (ColumnTable.sort_by, table.py:198-214)
-//   * scx_partition    : hash partition + stable scatter (exchange.py:52-70,
-//                        hash_partition / partition_indices; the reference's
-//                        stable argsort by bucket + take of every column)
 //   * scx_hash_keys    : raw Fibonacci hashes (exchange.py:35-49)
 //
 // Each CTA owns a contiguous chunk of kChunk rows processed as 16 sub-tiles of
@@ -11,8 +8,6 @@
 // memory; across CTAs from a digit-major exclusive scan of the per-CTA
 // histograms.  So every element's output position is the same as a stable
 // sort by digit, which is exactly partition_indices' stable argsort.
-#include <stdlib.h>
-
 #include "common.cuh"
 
 namespace scx {
@@ -23,11 +18,6 @@ constexpr int kChunk = kBlock * kItems;   // 4096 rows per CTA
 
 struct PartKeys {
   scx_column k[SCX_MAX_KEYS];
-  int n;
-};
-struct PartCols {
-  scx_column in[SCX_MAX_OUT];
-  scx_column out[SCX_MAX_OUT];
   int n;
 };
 
@@ -121,178 +111,6 @@ __global__ void sort_scatter_kernel(DigitSrc D, int64_t n, const uint64_t* offs,
     kout[pos] = kin[i];
     vout[pos] = vin[i];
   });
-}
-
-// Few digits (a partition into <= 32 parts): rounds of kRound sub-tiles share
-// one set of barriers -- per-(sub-tile, warp, digit) counts, one exclusive
-// scan per digit over (sub-tile, warp) in row order, per-digit totals --
-// so a 4096-row chunk needs 4 rounds x 3 barriers instead of 16 x 4.
-constexpr int kRound = 4;
-constexpr int kFewDigits = 32;
-
-template <typename Emit>
-__device__ __forceinline__ void scatter_chunk_few(const DigitSrc& D, int64_t n, int ndig,
-                                                  const uint64_t* offs, int nblocks, Emit emit) {
-  __shared__ uint32_t wc[kRound][kWarps][kFewDigits];
-  __shared__ uint64_t run[kFewDigits];
-  __shared__ uint32_t tot[kFewDigits];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < ndig) run[tid] = offs[(int64_t)tid * nblocks + blockIdx.x];
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
-  for (int r0 = 0; r0 < kItems; r0 += kRound) {
-    for (int j = tid; j < kRound * kWarps * kFewDigits; j += kBlock) (&wc[0][0][0])[j] = 0;
-    __syncthreads();
-    uint32_t d[kRound], rank[kRound];
-    bool valid[kRound];
-#pragma unroll
-    for (int r = 0; r < kRound; ++r) {
-      const int64_t i = base + (int64_t)(r0 + r) * kBlock + tid;
-      valid[r] = i < n;
-      d[r] = valid[r] ? D(i) : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int r = 0; r < kRound; ++r) {
-      const uint32_t peers = __match_any_sync(0xffffffffu, d[r]);
-      rank[r] = __popc(peers & ((1u << lane) - 1u));
-      if (valid[r] && rank[r] == 0) wc[r][warp][d[r]] = __popc(peers);
-    }
-    __syncthreads();
-    if (tid < ndig) {          // exclusive scan over (sub-tile, warp): row order
-      uint32_t s2 = 0;
-#pragma unroll
-      for (int r = 0; r < kRound; ++r)
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) { const uint32_t c = wc[r][w][tid]; wc[r][w][tid] = s2; s2 += c; }
-      tot[tid] = s2;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kRound; ++r)
-      if (valid[r]) emit(base + (int64_t)(r0 + r) * kBlock + tid, run[d[r]] + wc[r][warp][d[r]] + rank[r]);
-    __syncthreads();
-    if (tid < ndig) run[tid] += tot[tid];
-  }
-}
-
-__global__ void part_scatter_kernel(DigitSrc D, int64_t n, int nparts, const uint64_t* offs,
-                                    int nblocks, PartCols C) {
-  auto emit = [&](int64_t i, uint64_t pos) {
-    for (int c = 0; c < C.n; ++c) {
-      const int w = dtype_size_d(C.in[c].dtype);
-      const char* s = reinterpret_cast<const char*>(C.in[c].ptr);
-      char* d = reinterpret_cast<char*>(C.out[c].ptr);
-      switch (w) {
-        case 1: d[pos] = s[i]; break;
-        case 2: reinterpret_cast<int16_t*>(d)[pos] = reinterpret_cast<const int16_t*>(s)[i]; break;
-        case 4: reinterpret_cast<int32_t*>(d)[pos] = reinterpret_cast<const int32_t*>(s)[i]; break;
-        default: reinterpret_cast<int64_t*>(d)[pos] = reinterpret_cast<const int64_t*>(s)[i]; break;
-      }
-    }
-  };
-  if (nparts <= kFewDigits) {
-    scatter_chunk_few(D, n, nparts, offs, nblocks, emit);
-    return;
-  }
-  scatter_chunk(D, n, nparts, offs, nblocks, [&](int64_t i, uint64_t pos) {
-    for (int c = 0; c < C.n; ++c) {
-      const int w = dtype_size_d(C.in[c].dtype);
-      const char* s = reinterpret_cast<const char*>(C.in[c].ptr);
-      char* d = reinterpret_cast<char*>(C.out[c].ptr);
-      switch (w) {
-        case 1: d[pos] = s[i]; break;
-        case 2: reinterpret_cast<int16_t*>(d)[pos] = reinterpret_cast<const int16_t*>(s)[i]; break;
-        case 4: reinterpret_cast<int32_t*>(d)[pos] = reinterpret_cast<const int32_t*>(s)[i]; break;
-        default: reinterpret_cast<int64_t*>(d)[pos] = reinterpret_cast<const int64_t*>(s)[i]; break;
-      }
-    }
-  });
-}
-
-// ---- warp-segmented partition for few parts (N <= 16: one part per GPU) ----
-// Every warp owns a contiguous segment of kWSeg rows.  Pass 1 counts rows per
-// (part, segment); a part-major exclusive scan gives each warp, for each
-// part, the output position of its first row.  Pass 2: the warp walks its
-// segment 32 rows at a time (coalesced 8-byte loads, 4 steps of loads in
-// flight), ranks each row among equal parts of the step with __match_any_sync
-// (stable: lower lane = earlier row) and stores it at cursor[part] + rank;
-// lane p keeps cursor[p] in a register.  No block-wide barrier anywhere, and
-// each store instruction writes at most N contiguous runs.
-constexpr int kWSeg = 4096;                       // rows per warp segment
-constexpr int kPMaxParts = 16;
-constexpr int kWUnroll = 4;
-
-__global__ void part_hist3_kernel(PartKeys K, int64_t n, int nparts, uint32_t* counts,
-                                  int64_t nseg) {
-  const int lane = threadIdx.x & 31;
-  const int64_t seg = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (seg >= nseg) return;
-  const int64_t base = seg * kWSeg;
-  uint32_t mine = 0;                              // lane p: rows of part p
-  for (int s0 = 0; s0 < kWSeg; s0 += 32 * kWUnroll) {
-    uint32_t d[kWUnroll];
-#pragma unroll
-    for (int u = 0; u < kWUnroll; ++u) {
-      const int64_t i = base + s0 + u * 32 + lane;
-      d[u] = i < n ? bucket_of(K, i, (uint32_t)nparts) : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int u = 0; u < kWUnroll; ++u) {
-      for (int p = 0; p < nparts; ++p) {
-        const uint32_t c = __popc(__ballot_sync(0xffffffffu, d[u] == (uint32_t)p));
-        if (lane == p) mine += c;
-      }
-    }
-  }
-  if (lane < nparts) counts[(int64_t)lane * nseg + seg] = mine;
-}
-
-__global__ void part_scatter3_kernel(PartKeys K, int64_t n, int nparts, const uint64_t* offs,
-                                     int64_t nseg, PartCols C) {
-  const int lane = threadIdx.x & 31;
-  const int64_t seg = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  if (seg >= nseg) return;
-  const int64_t base = seg * kWSeg;
-  uint64_t cur = lane < nparts ? offs[(int64_t)lane * nseg + seg] : 0;   // lane p: next slot of part p
-  const uint32_t lt = (1u << lane) - 1u;
-  for (int s0 = 0; s0 < kWSeg; s0 += 32 * kWUnroll) {
-    uint32_t d[kWUnroll];
-#pragma unroll
-    for (int u = 0; u < kWUnroll; ++u) {
-      const int64_t i = base + s0 + u * 32 + lane;
-      d[u] = i < n ? bucket_of(K, i, (uint32_t)nparts) : 0xFFFFFFFFu;
-    }
-#pragma unroll
-    for (int u = 0; u < kWUnroll; ++u) {
-      const int64_t i = base + s0 + u * 32 + lane;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d[u]);
-      const uint32_t rank = __popc(peers & lt);
-      const uint64_t start = __shfl_sync(0xffffffffu, cur, d[u] < 32 ? (int)d[u] : 0);
-      if (i < n) {
-        const uint64_t pos = start + rank;
-        for (int c = 0; c < C.n; ++c) {
-          const int w = dtype_size_d(C.in[c].dtype);
-          const char* src = reinterpret_cast<const char*>(C.in[c].ptr);
-          char* dst = reinterpret_cast<char*>(C.out[c].ptr);
-          switch (w) {
-            case 1: dst[pos] = src[i]; break;
-            case 2: reinterpret_cast<int16_t*>(dst)[pos] = reinterpret_cast<const int16_t*>(src)[i]; break;
-            case 4: reinterpret_cast<int32_t*>(dst)[pos] = reinterpret_cast<const int32_t*>(src)[i]; break;
-            default: reinterpret_cast<int64_t*>(dst)[pos] = reinterpret_cast<const int64_t*>(src)[i]; break;
-          }
-        }
-      }
-      // advance the cursors: part p gained popc(ballot(d == p)) rows
-      for (int p = 0; p < nparts; ++p) {
-        const uint32_t c = __popc(__ballot_sync(0xffffffffu, d[u] == (uint32_t)p));
-        if (lane == p) cur += c;
-      }
-    }
-  }
-}
-
-__global__ void part_counts_kernel(const uint64_t* offs, int nparts, int nblocks, uint64_t* counts) {
-  const int p = threadIdx.x;
-  if (p < nparts) counts[p] = offs[(int64_t)(p + 1) * nblocks] - offs[(int64_t)p * nblocks];
 }
 
 __global__ void hash_keys_kernel(PartKeys K, int64_t n, uint64_t* out) {
@@ -441,72 +259,5 @@ extern "C" int scx_hash_keys(const scx_column* keys, int n_keys, int64_t n, uint
   for (int i = 0; i < n_keys; ++i) K.k[i] = keys[i];
   hash_keys_kernel<<<grid_for(n, 256, 2368), 256, 0, (cudaStream_t)stream>>>(K, n, out);
   SCX_CHECK_LAUNCH("hash_keys_kernel");
-  return SCX_OK;
-}
-
-extern "C" int64_t scx_partition_workspace(int64_t n, int n_parts) { return ws_bytes(n, n_parts); }
-
-extern "C" int scx_partition(const scx_column* keys, int n_keys, const scx_column* cols,
-                             const scx_column* outs, int n_cols, int64_t n, int n_parts,
-                             uint64_t* counts, void* temp, void* stream) {
-  if (!keys || n_keys < 1 || n_keys > SCX_MAX_KEYS || n_cols < 0 || n_cols > SCX_MAX_OUT ||
-      n_parts < 1 || n_parts > kDigits || !counts || (n > 0 && !temp)) {
-    set_error("partition: bad arguments (keys=%d cols=%d parts=%d)", n_keys, n_cols, n_parts);
-    return SCX_EINVAL;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
-  if (n == 0) {
-    SCX_CUDA(cudaMemsetAsync(counts, 0, 8 * n_parts, st));
-    return SCX_OK;
-  }
-  DigitSrc D;
-  memset(&D, 0, sizeof(D));
-  D.keys = nullptr;
-  D.nparts = (uint32_t)n_parts;
-  D.pk.n = n_keys;
-  for (int i = 0; i < n_keys; ++i) D.pk.k[i] = keys[i];
-  PartCols C;
-  memset(&C, 0, sizeof(C));
-  C.n = n_cols;
-  for (int i = 0; i < n_cols; ++i) {
-    C.in[i] = cols[i];
-    C.out[i] = outs[i];
-    if (dtype_size(cols[i].dtype) != dtype_size(outs[i].dtype)) {
-      set_error("partition: column %d in/out width mismatch", i);
-      return SCX_EINVAL;
-    }
-  }
-  const uint64_t* offs;
-  int nb;
-  // measured on B200 (1 GiB of 16-byte rows, 8 parts): the warp-segmented
-  // path is 1.44 ms vs 1.05 ms for the CTA-ranked path below, so it is opt-in
-  if (n_parts <= kPMaxParts && getenv("SCX_PART_WARPSEG") != nullptr) {
-    // warp-segmented path: per-(part, segment) counts, part-major scan, scatter
-    const int64_t nseg = (n + kWSeg - 1) / kWSeg;
-    const int64_t nblk = (nseg + kWarps - 1) / kWarps;
-    uint32_t* cnts = static_cast<uint32_t*>(temp);
-    uint64_t* o2 = reinterpret_cast<uint64_t*>(static_cast<char*>(temp) +
-                                               ((nseg * n_parts * 4 + 255) / 256) * 256);
-    uint64_t* tmp = o2 + nseg * n_parts + 1;
-    part_hist3_kernel<<<(int)nblk, kBlock, 0, st>>>(D.pk, n, n_parts, cnts, nseg);
-    SCX_CHECK_LAUNCH("part_hist3_kernel");
-    int rc = scan_u32_excl(cnts, o2, nseg * n_parts, tmp, st);
-    if (rc) return rc;
-    part_counts_kernel<<<1, kDigits, 0, st>>>(o2, n_parts, (int)nseg, counts);
-    SCX_CHECK_LAUNCH("part_counts_kernel");
-    if (n_cols > 0) {
-      part_scatter3_kernel<<<(int)nblk, kBlock, 0, st>>>(D.pk, n, n_parts, o2, nseg, C);
-      SCX_CHECK_LAUNCH("part_scatter3_kernel");
-    }
-    return SCX_OK;
-  }
-  int rc = counting_pass(D, n, n_parts, temp, st, offs, nb);
-  if (rc) return rc;
-  part_counts_kernel<<<1, kDigits, 0, st>>>(offs, n_parts, nb, counts);
-  SCX_CHECK_LAUNCH("part_counts_kernel");
-  if (n_cols > 0) {
-    part_scatter_kernel<<<nb, kBlock, 0, st>>>(D, n, n_parts, offs, nb, C);
-    SCX_CHECK_LAUNCH("part_scatter_kernel");
-  }
   return SCX_OK;
 }

@@ -6,11 +6,14 @@ engine.py`): the exchange-plan registry (41-133), ``RunReport`` (144-179),
 (``LocalContext``/``WorkerContext``, 221-365), ``run_query`` (382-460) and
 ``reference_run`` (463-469).
 
-Differences by design: a worker is a *process* owning one GPU (not a
-thread), tables live in HBM, relational operators are fused kernels, and
-exchanges are NCCL collectives.  Timing follows the reference's barrier
-method (engine.py:318-340): every exchange is bracketed by a device-drained
-barrier, compute is the remainder.
+Workers: one process per GPU (torchrun, NCCL exchanges), or -- the
+reference's own ``MODE_IN_PROCESS`` -- N worker threads in one process,
+each a virtual rank whose partition lives in the same GPU's HBM
+(``run_query(qid, variant, cluster, dataset)``, cluster.py).  Tables live in
+HBM and relational operators are fused kernels either way.  Timing follows
+the reference's barrier method (engine.py:318-340): every exchange is
+bracketed by a barrier (device-drained across processes), compute is the
+remainder.
 """
 
 from __future__ import annotations
@@ -24,8 +27,9 @@ import numpy as np
 
 from . import exchange as X
 from . import relops as R
-from .cluster import Endpoint, barrier, create_cluster
-from .data import DEFAULT_PARTITION_KEYS, Dataset, PARTITION_SCHEMES, DataError
+from .cluster import Cluster, Endpoint, barrier, create_cluster, run_workers
+from .data import (DEFAULT_PARTITION_KEYS, Dataset, PARTITION_SCHEMES, DataError,
+                   PartitionedDataset)
 from .table import Column, ColumnTable, alloc, concat_tables
 
 
@@ -296,23 +300,23 @@ class DeviceContext:
         return g
 
     def all_reduce_sum(self, vec) -> np.ndarray:
-        v = np.asarray(vec, dtype=np.float64)
-        if self.ep.n == 1:
-            return v
-        import torch
-        import torch.distributed as dist
-        t = torch.from_numpy(v.copy()).to(self.ep.device)
-        parts = X.all_gather_tensor(self.ep, t).cpu().numpy()
-        acc = parts[0].copy()
-        for p in parts[1:]:   # rank-order fold (collectives.py:198-206)
-            acc += p
-        return acc
+        """float64 sum over workers, folded in rank order (engine.py:342-343,
+        collectives.py:198-206)."""
+        from .collectives import all_reduce
+        return all_reduce(self.ep, np.asarray(vec, dtype=np.float64), "sum")
 
     def gather(self, t):
         """Partials to rank 0, rank order (engine.py:345-365)."""
         t = t.materialize()
         if self.ep.n == 1:
             return t
+        if self.ep.in_process:
+            parts = self.ep.cluster.rendezvous(self.ep.rank, "gather", t, lambda s: list(s))
+            full = concat_tables(parts) if self.is_root else None
+            # the root's concatenation copies are enqueued before any worker
+            # drops its partial (one shared stream)
+            self.ep.cluster.rendezvous(self.ep.rank, "gather:done", None, lambda s: None)
+            return full
         import torch.distributed as dist
         names = t.column_names
         counts, _ = X.size_exchange(self.ep, np.full(self.ep.n, t.row_count, dtype=np.int64))
@@ -396,11 +400,13 @@ def upload_tables_async(host: dict, order=None, stream=None):
 
 def load_tables(ds: Dataset, ep: Endpoint | None = None, scheme: str = "default_keys",
                 names=None) -> dict[str, ColumnTable]:
-    """Upload a dataset and keep this rank's partition in HBM.
+    """Upload this rank's partition of a host dataset into HBM.
 
-    ``default_keys`` partitions on the GPU with the same kernel the shuffle
-    uses (data.py:284-302 semantics); ``unpartitioned`` / ``round_robin`` use
-    host row ranges.
+    At N > 1 each rank selects its own rows on the host -- ``default_keys``:
+    the reference's hash of the table's partition key mod N, input order
+    kept (data.py:284-302, bit-identical to the device partition kernel);
+    other schemes: host row ranges -- and uploads only those (1/N of every
+    table crosses PCIe per rank, not the whole table).
     """
     from .data import partition_rows
     ep = ep or Endpoint(0, 1, "nccl")
@@ -412,51 +418,154 @@ def load_tables(ds: Dataset, ep: Endpoint | None = None, scheme: str = "default_
             continue
         if ep.n == 1:
             out[name] = ht.to_device()
-        elif scheme == "default_keys":
-            dev = ht.to_device()
-            out[name] = X.hash_partition(dev, [DEFAULT_PARTITION_KEYS[name]], ep.n)[ep.rank]
-            del dev
         else:
-            rows = partition_rows(ht, scheme, None, ep.n)[ep.rank]
+            rows = partition_rows(ht, scheme, DEFAULT_PARTITION_KEYS[name], ep.n)[ep.rank]
             out[name] = ht.take(rows).to_device()
     return out
 
 
-def run_query(qid: str, variant: str = "default", ep: Endpoint | None = None,
-              tables: dict[str, ColumnTable] | None = None, scheme: str = "default_keys",
-              p2p_broadcast: bool = False):
-    """Execute one query on this rank's partition; (result on root | None, RunReport)."""
-    from .queries import PLAN_FUNCTIONS
+def partition_tables(ds, n: int, scheme: str = "default_keys", names=None) -> list[dict]:
+    """Per-worker device tables for an in-process cluster of n virtual ranks
+    on this GPU.  A host ``Dataset`` is uploaded once and split on the
+    device by the partition kernel (``default_keys``, data.py:284-302
+    semantics) or by host row ranges (other schemes); a host
+    ``PartitionedDataset`` uploads each worker's share."""
+    from .data import partition_rows
+    if isinstance(ds, PartitionedDataset):
+        if ds.n_workers != n:
+            raise PlanError(f"cluster has {n} endpoints but dataset is partitioned for "
+                            f"{ds.n_workers}")
+        return [{t: ht.to_device() for t, ht in w.items() if names is None or t in names}
+                for w in ds.workers]
+    if scheme not in PARTITION_SCHEMES:
+        raise DataError(f"unknown partitioning scheme {scheme!r}; choose from {PARTITION_SCHEMES}")
+    out: list[dict] = [{} for _ in range(n)]
+    for name, ht in ds.tables.items():
+        if names is not None and name not in names:
+            continue
+        if scheme == "default_keys":
+            dev = ht.to_device() if not isinstance(ht, ColumnTable) else ht
+            parts = X.hash_partition(dev, [DEFAULT_PARTITION_KEYS[name]], n) if n > 1 else [dev]
+        else:
+            parts = [ht.take(r).to_device() for r in partition_rows(ht, scheme, None, n)]
+        for r in range(n):
+            out[r][name] = parts[r]
+    return out
+
+
+@dataclass
+class _WorkerOutcome:
+    result: object
+    total_s: float
+    shuffle_s: float
+    broadcast_s: float
+    shuffle_msgs: list
+    broadcast_msgs: list
+    shuffle_bytes: int
+    broadcast_bytes: int
+    peak: int
+    counts: tuple
+
+
+def _run_worker(ep: Endpoint, fn, tables, variant, scheme, p2p_broadcast) -> _WorkerOutcome:
     import torch
-    plan = get_plan(qid, variant)
-    ep = ep or Endpoint(0, 1, "nccl")
-    if plan.requires_co_partition and scheme != "default_keys" and ep.n > 1:
-        needs = ", ".join(f"{t} on {k}" for t, k in plan.requires_co_partition)
-        raise PlanError(f"{qid}/{variant} requires co-partitioned inputs ({needs}); "
-                        f"got scheme {scheme!r}")
     ctx = DeviceContext(ep, tables, variant, scheme, p2p_broadcast)
-    torch.cuda.reset_peak_memory_stats()
     barrier(ep)
     t0 = time.perf_counter()
-    result = PLAN_FUNCTIONS[qid](ctx)
+    result = fn(ctx)
     if result is not None:
         result = result.materialize()
     barrier(ep)
+    if ep.in_process:
+        torch.cuda.synchronize()
     total = time.perf_counter() - t0
-    counts = (ctx.n_shuffles, ctx.n_broadcasts)
-    if counts != plan.expected_exchanges:
+    return _WorkerOutcome(result, total, ctx.shuffle_s, ctx.broadcast_s, ctx.shuffle_msgs,
+                          ctx.broadcast_msgs, ctx.shuffle_bytes, ctx.broadcast_bytes,
+                          int(torch.cuda.max_memory_allocated()),
+                          (ctx.n_shuffles, ctx.n_broadcasts))
+
+
+def run_query(qid: str, variant: str = "default", cluster=None, dataset=None,
+              scheme: str | None = None, p2p_broadcast: bool = False, tables=None):
+    """Execute one query; (result on the root | None, RunReport) (engine.py:382-460).
+
+    ``cluster``: an in-process ``Cluster`` (reference call shape:
+    ``run_query(qid, variant, cluster, partitioned_dataset)``; every worker
+    thread runs the plan on its virtual rank, the root's result is
+    returned), or this process's ``Endpoint`` in a process-per-GPU job
+    (``dataset`` = this rank's device tables), or None (one GPU, one rank).
+    """
+    from .queries import PLAN_FUNCTIONS
+    import torch
+    plan = get_plan(qid, variant)
+    dataset = tables if dataset is None else dataset
+    if scheme is None:
+        scheme = dataset.scheme if isinstance(dataset, PartitionedDataset) else "default_keys"
+    n = cluster.n if cluster is not None else 1
+    if plan.requires_co_partition and scheme != "default_keys" and n > 1:
+        needs = ", ".join(f"{t} on {k}" for t, k in plan.requires_co_partition)
+        raise PlanError(f"{qid}/{variant} requires co-partitioned inputs ({needs}); "
+                        f"got scheme {scheme!r}")
+    fn = PLAN_FUNCTIONS[qid]
+    torch.cuda.reset_peak_memory_stats()
+    if isinstance(cluster, Cluster):
+        if isinstance(dataset, (list, tuple)):
+            per = list(dataset)
+            if len(per) != n:
+                raise PlanError(f"cluster has {n} endpoints but dataset is partitioned for "
+                                f"{len(per)}")
+        else:
+            per = partition_tables(dataset, n, scheme)
+        outcomes = run_workers(cluster, lambda ep: _run_worker(ep, fn, per[ep.rank], variant,
+                                                               scheme, p2p_broadcast))
+        mode = cluster.mode
+    else:
+        ep = cluster or Endpoint(0, 1, "nccl")
+        if isinstance(dataset, Dataset):
+            dataset = load_tables(dataset, ep, scheme)
+        outcomes = [_run_worker(ep, fn, dataset, variant, scheme, p2p_broadcast)]
+        mode = ep.backend
+    root = outcomes[0]
+    if any(o.counts != root.counts for o in outcomes):
+        raise PlanError(f"{qid}/{variant}: workers disagree on exchange counts")
+    if root.counts != plan.expected_exchanges:
         raise PlanError(f"{qid}/{variant}: plan declares exchanges {plan.expected_exchanges}, "
-                        f"run produced {counts}")
+                        f"run produced {root.counts}")
+    result = root.result
     report = RunReport(
-        query_id=qid, variant=variant, mode=ep.backend,
-        compute_s=total - ctx.shuffle_s - ctx.broadcast_s, shuffle_s=ctx.shuffle_s,
-        broadcast_s=ctx.broadcast_s, shuffle_msgs=ctx.shuffle_msgs,
-        broadcast_msgs=ctx.broadcast_msgs,
-        peak_bytes=[int(torch.cuda.max_memory_allocated())],
+        query_id=qid, variant=variant, mode=mode,
+        compute_s=root.total_s - root.shuffle_s - root.broadcast_s, shuffle_s=root.shuffle_s,
+        broadcast_s=root.broadcast_s,
+        shuffle_msgs=[m for o in outcomes for m in o.shuffle_msgs],
+        broadcast_msgs=[m for o in outcomes for m in o.broadcast_msgs],
+        peak_bytes=[o.peak for o in outcomes],
         result_digest=result_digest(result) if result is not None else "empty",
-        exchange_counts=counts, shuffle_bytes=ctx.shuffle_bytes,
-        broadcast_bytes=ctx.broadcast_bytes)
+        exchange_counts=root.counts, shuffle_bytes=sum(o.shuffle_bytes for o in outcomes),
+        broadcast_bytes=sum(o.broadcast_bytes for o in outcomes))
     return result, report
+
+
+def q12_variants(cluster, dataset: Dataset) -> dict[str, RunReport]:
+    """Q12 under its three plans -- default (co-partitioned), Pa (shuffle
+    both sides), Pb (broadcast) -- whose results must agree
+    (engine.py:472-490).  The reference compares virtual times on a
+    simulated cluster; here the reports carry measured times (in-process
+    ``Cluster``, this process's ``Endpoint``, or None for one GPU)."""
+    if isinstance(cluster, Cluster):
+        by_key = partition_tables(dataset, cluster.n, "default_keys")
+        by_range = partition_tables(dataset, cluster.n, "unpartitioned")
+    else:
+        ep = cluster or Endpoint(0, 1, "nccl")
+        by_key = load_tables(dataset, ep, "default_keys")
+        by_range = load_tables(dataset, ep, "unpartitioned")
+    reports = {}
+    _, reports["default"] = run_query("Q12", "default", cluster, by_key, "default_keys")
+    _, reports["pa"] = run_query("Q12", "pa", cluster, by_range, "unpartitioned")
+    _, reports["pb"] = run_query("Q12", "pb", cluster, by_range, "unpartitioned")
+    digests = {r.result_digest for r in reports.values()}
+    if len(digests) != 1:
+        raise PlanError(f"Q12 variants disagree: {digests}")
+    return reports
 
 
 def reference_run(qid: str, tables, variant: str = "default") -> ColumnTable:

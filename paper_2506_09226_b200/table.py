@@ -288,6 +288,16 @@ class Column:
 
     def __init__(self, kind: str, data, scale: int = 0, dictionary=None, lo: int = 0,
                  hi: int = -1, dense: bool = False):
+        if data is not None and not hasattr(data, "data_ptr"):
+            # the reference's call shape Column(kind, values, dictionary=None)
+            # (table.py:46-60): reference-typed host values, narrowed losslessly
+            # and uploaded
+            if isinstance(scale, (tuple, list)):
+                dictionary, scale = scale, 0
+            src = Column.from_numpy(kind, data, dictionary)
+            for slot in Column.__slots__:
+                setattr(self, slot, getattr(src, slot))
+            return
         if kind not in KINDS:
             raise SchemaError(f"unknown column kind {kind!r}")
         if kind == "dict" and dictionary is None:
@@ -592,3 +602,30 @@ def tables_equal(a: ColumnTable, b: ColumnTable) -> bool:
         if not np.array_equal(col.values, other.values):
             return False
     return True
+
+
+# ---- constructors of the reference's package namespace (__init__.py:86-112)
+
+def int64_col(values) -> Column:
+    return Column("int64", np.asarray(values, dtype=np.int64))
+
+
+def float64_col(values) -> Column:
+    return Column("float64", np.asarray(values, dtype=np.float64))
+
+
+def date32_col(values) -> Column:
+    return Column("date32", np.asarray(values, dtype=np.int32))
+
+
+def dict_col(codes, dictionary) -> Column:
+    return Column("dict", np.asarray(codes, dtype=np.int32), tuple(dictionary))
+
+
+def dict_col_from_strings(strings) -> Column:
+    """Encode strings with a first-seen-order dictionary."""
+    index: dict[str, int] = {}
+    codes = np.empty(len(strings), dtype=np.int32)
+    for i, sv in enumerate(strings):
+        codes[i] = index.setdefault(sv, len(index))
+    return Column("dict", codes, tuple(index))

@@ -1,0 +1,176 @@
+"""N > 1 on one GPU: the reference's in-process mode with virtual ranks.
+
+``create_cluster(topo, MODE_IN_PROCESS)`` + ``run_workers`` run N worker
+threads, each owning a partition in this GPU's HBM; every exchange moves
+device memory between the workers (the shuffle's partition kernel writes
+straight into the receivers' buffers).  This exercises every N > 1 branch
+of the plans -- shuffles, broadcasts, the final gather, the exact
+cross-rank folds of global aggregates, per-rank top-k -- with real kernels,
+against the oracle and the reference's own exchange fixture.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+from oracle import ref as O
+from test_gpu_tpch22 import assert_same
+
+pytestmark = pytest.mark.gpu
+
+_DS = {}
+
+
+def _host(sf, skew=0.0):
+    key = (sf, skew)
+    if key not in _DS:
+        from paper_2506_09226_b200.data import generate
+        _DS.clear()
+        ds = generate(sf, skew, 0)
+        _DS[key] = (ds, ds.to_reference(), {})
+    return _DS[key]
+
+
+def _expected(sf, skew, qid):
+    ds, ref, exp = _host(sf, skew)
+    if qid not in exp:
+        exp[qid] = O.reference_run(qid, ref)
+    return exp[qid]
+
+
+def _cluster(n):
+    import paper_2506_09226_b200 as P
+    return P.create_cluster(P.Topology(k=n, v=1, bg_gbps=900, bn_gbps=900), P.MODE_IN_PROCESS)
+
+
+def _dev_table(j):
+    import paper_2506_09226_b200 as P
+    return P.ColumnTable({nm: P.Column(c["kind"], np.asarray(c["values"]), c.get("dictionary"))
+                          for nm, c in j.items()})
+
+
+def _plain(t):
+    return {nm: [int(x) for x in c.values] for nm, c in t.materialize().columns.items()}
+
+
+def test_exchange_matches_reference_fixture():
+    """The reference's own N=3 in-process shuffle / broadcast outputs
+    (tests/golden/exchange.json, made by running shufflecast)."""
+    import paper_2506_09226_b200 as P
+    ex = load_golden("exchange.json")
+    ins = [_dev_table(t) for t in ex["inputs"]]
+
+    def w(ep):
+        st = P.ExchangeStats()
+        sh = P.shuffle_table(ep, ins[ep.rank], ["k"], st)
+        bc = P.broadcast_table(ep, ins[ep.rank])
+        bp = P.broadcast_table(ep, ins[ep.rank], use_p2p=True)
+        return _plain(sh), _plain(bc), _plain(bp)
+
+    out = P.run_workers(_cluster(3), w)
+    for r in range(3):
+        exp_sh = {nm: c["values"] for nm, c in ex["shuffle"][r].items()}
+        exp_bc = {nm: c["values"] for nm, c in ex["broadcast"][r].items()}
+        assert out[r][0] == exp_sh, r
+        assert out[r][1] == exp_bc and out[r][2] == exp_bc, r
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_shuffle_large_is_hash_partition_of_concat(n):
+    """Conservation, co-location and receive order (source rank, then source
+    order) on 1M rows per worker, mixed column widths."""
+    import torch
+    import paper_2506_09226_b200 as P
+    rng = np.random.default_rng(5)
+    tabs = []
+    for r in range(n):
+        m = 1_000_000 + 977 * r
+        tabs.append({"k": rng.integers(0, 1 << 40, size=m), "a": rng.integers(0, 250, size=m),
+                     "b": rng.integers(-30000, 30000, size=m).astype(np.int32)})
+    dev = [P.ColumnTable({nm: P.Column("int64", v) for nm, v in t.items()}) for t in tabs]
+
+    def w(ep):
+        return _plain_np(P.shuffle_table(ep, dev[ep.rank], ["k"]))
+
+    out = P.run_workers(_cluster(n), w)
+    for r in range(n):
+        parts = [O.hash_partition({nm: ("int64", v, None) for nm, v in t.items()}, ["k"], n)[r]
+                 for t in tabs]
+        for nm in ("k", "a", "b"):
+            exp = np.concatenate([p[nm][1] for p in parts])
+            assert np.array_equal(out[r][nm], exp), (n, r, nm)
+    torch.cuda.synchronize()
+
+
+def _plain_np(t):
+    return {nm: c.values.astype(np.int64) for nm, c in t.materialize().columns.items()}
+
+
+def test_broadcast_reconciles_differing_dictionaries():
+    """exchange.py:177-192,217-251: union in rank order, first seen wins,
+    every worker's codes remapped."""
+    import paper_2506_09226_b200 as P
+    dicts = [("AIR", "MAIL"), ("SHIP", "AIR", "RAIL"), ("MAIL", "TRUCK")]
+    codes = [[1, 0, 1], [0, 2, 1, 1], [1, 0]]
+
+    def w(ep):
+        t = P.ColumnTable({"m": P.Column("dict", np.asarray(codes[ep.rank], np.int32),
+                                         dicts[ep.rank])})
+        b = P.broadcast_table(ep, t).materialize().column("m")
+        return b.dictionary, [int(x) for x in b.values]
+
+    out = P.run_workers(_cluster(3), w)
+    union = ("AIR", "MAIL", "SHIP", "RAIL", "TRUCK")
+    strings = [dicts[r][c] for r in range(3) for c in codes[r]]
+    for d, v in out:
+        assert d == union
+        assert [union[c] for c in v] == strings
+
+
+QUERIES = [f"Q{i}" for i in range(1, 23)]
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_all_22_queries_n_workers(n):
+    """Every plan at N virtual ranks: result == the single-context oracle,
+    executed exchange counts == the plan's (run_query raises otherwise)."""
+    import paper_2506_09226_b200 as P
+    ds, _, _ = _host(0.1)
+    per = P.partition_tables(ds, n)
+    cl = _cluster(n)
+    for qid in QUERIES:
+        res, rep = P.run_query(qid, "default", cl, per)
+        assert rep.exchange_counts == P.get_plan(qid, "default").expected_exchanges
+        assert len(rep.peak_bytes) == n
+        assert_same(res, _expected(0.1, 0.0, qid), f"{qid}@N{n}")
+
+
+@pytest.mark.parametrize("variant", ["pa", "pb"])
+@pytest.mark.parametrize("n", [2, 4])
+def test_q12_variants_n_workers(variant, n):
+    """Q12-pa shuffles both sides on the join key (2,0); Q12-pb broadcasts
+    the filtered lineitem (0,1) (engine.py:108-121)."""
+    import paper_2506_09226_b200 as P
+    ds, _, _ = _host(0.1)
+    pd = P.partition_dataset(ds, n, "unpartitioned")
+    res, rep = P.run_query("Q12", variant, _cluster(n), pd)
+    assert rep.exchange_counts == P.get_plan("Q12", variant).expected_exchanges
+    assert rep.shuffle_bytes > 0 if variant == "pa" else rep.broadcast_bytes > 0
+    assert_same(res, _expected(0.1, 0.0, "Q12"), f"Q12/{variant}@N{n}")
+
+
+def test_co_partition_required():
+    import paper_2506_09226_b200 as P
+    ds, _, _ = _host(0.1)
+    with pytest.raises(P.PlanError, match="co-partitioned"):
+        P.run_query("Q3", "default", _cluster(2), P.partition_dataset(ds, 2, "unpartitioned"))
+
+
+@pytest.mark.parametrize("qid", ["Q1", "Q3", "Q5", "Q9", "Q13", "Q18", "Q21"])
+def test_skewed_data_n8(qid):
+    """Zipf-skewed keys (generate(skew=1.5)): unbalanced partitions, same results."""
+    import paper_2506_09226_b200 as P
+    ds, _, _ = _host(0.05, 1.5)
+    per = _DS[(0.05, 1.5)][2].setdefault("_per8", P.partition_tables(ds, 8))
+    res, _ = P.run_query(qid, "default", _cluster(8), per)
+    assert_same(res, _expected(0.05, 1.5, qid), f"{qid}@skew")

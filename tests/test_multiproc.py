@@ -6,7 +6,7 @@ all-to-all-v receive order (source rank ascending, input order within a
 rank, exchange.py:52-56,161-166), broadcast (Alg. 2 and p2p) concatenation
 in rank order (exchange.py:274-276), the final gather to rank 0
 (engine.py:345-365), column-range metadata merging and the schema
-rendezvous error.  The on-device partition kernel is replaced by the CPU
+rendezvous error.  The on-device partition kernels are replaced by the CPU
 oracle's hash_partition inside the children (it is checked against the
 kernel separately in test_gpu_parity.py).
 """
@@ -44,15 +44,24 @@ def _as_oracle(t):
     return {n: (c.kind, c.data.numpy().astype(np.int64), c.dictionary) for n, c in t.columns.items()}
 
 
-def _host_partition(table, key_columns, n_parts):
-    """CPU stand-in for exchange.partition_device (same contract)."""
-    from oracle import ref as O
-    t = _as_oracle(table)
-    b = O.hash_keys(t, key_columns) % np.uint64(n_parts)
-    order = np.argsort(b, kind="stable")
-    counts = [int(x) for x in np.bincount(b.astype(np.int64), minlength=n_parts)]
-    outs = {nm: table.column(nm).data[torch.from_numpy(order)] for nm in table.column_names}
-    return outs, counts
+class _HostPartitioner:
+    """CPU stand-in for exchange._Partitioner (same contract: counts after
+    pass 1, local() = every column partitioned in bucket order)."""
+
+    def __init__(self, table, key_columns, n_parts):
+        from oracle import ref as O
+        from paper_2506_09226_b200.exchange import _key_cols
+        self.table = table.materialize()
+        _key_cols(self.table, key_columns)
+        self.names = self.table.column_names
+        self.n = self.table.row_count
+        self.n_parts = n_parts
+        b = O.hash_keys(_as_oracle(self.table), key_columns) % np.uint64(n_parts)
+        self.order = torch.from_numpy(np.argsort(b, kind="stable"))
+        self.counts = np.bincount(b.astype(np.int64), minlength=n_parts).astype(np.int64)
+
+    def local(self, cols):
+        return [cols[nm].data[self.order] for nm in self.names]
 
 
 def _worker(rank, world, port, seed, out_q):
@@ -64,7 +73,7 @@ def _worker(rank, world, port, seed, out_q):
         from paper_2506_09226_b200.engine import DeviceContext
         from paper_2506_09226_b200.table import SchemaError
         import torch.distributed as dist
-        X.partition_device = _host_partition
+        X._Partitioner = _HostPartitioner
         ep = P.create_cluster("gloo")
         res = {"rank": ep.rank, "n": ep.n}
         t = _cpu_table(rank, 40 + 7 * rank, seed)

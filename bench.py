@@ -176,85 +176,112 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline (oracle port; only here and in --impl reference)
+# CPU baseline: the REAL reference (shufflecast, installed unmodified under
+# baseline/_ref) for its six queries + the oracle port (oracle/tpch_ext.py)
+# for the 16 it lacks.  Only here and in --impl reference.
 # ---------------------------------------------------------------------------
 
-def _oracle_suite_time(sample_sf: float, queries, reps: int = 3) -> tuple[float, dict]:
-    from oracle import ref as O
-    from paper_2506_09226_b200.data import cached_generate
-    T = cached_generate(sample_sf).to_reference()
-    per = {}
-    for q in queries:
-        O.reference_run(q, T)                  # warm-up
-        best = float("inf")
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            O.reference_run(q, T)
-            best = min(best, time.perf_counter() - t0)
-        per[q] = best
-    return sum(per.values()), per
+REF_QUERIES = ("Q1", "Q3", "Q6", "Q12", "Q14", "Q19")
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+CPU_SF100 = os.path.join(ROOT, "profiles", "r2_cpu_sf100.json")
+
+_WORKER = {}
 
 
-_WORKER_T = None
-
-
-def _oracle_init(sample_sf):
-    global _WORKER_T
+def _cpu_init(sample_sf):
+    """Per process: the reference's own generate() for its queries, our
+    generator (value-identical, widened) for the oracle's."""
     os.environ.setdefault("OMP_NUM_THREADS", "1")
     from paper_2506_09226_b200.data import cached_generate
-    _WORKER_T = cached_generate(sample_sf).to_reference()
+    _WORKER["port"] = cached_generate(sample_sf).to_reference()
+    if os.path.isdir(REF_PATH):
+        sys.path.insert(0, REF_PATH)
+        import shufflecast
+        _WORKER["ref"] = (shufflecast, shufflecast.generate(sample_sf, skew=0.0, seed=0))
 
 
-def _oracle_query(q):
-    from oracle import ref as O
+def _cpu_query(q):
     t0 = time.perf_counter()
-    O.reference_run(q, _WORKER_T)
-    return q, time.perf_counter() - t0
+    if q in REF_QUERIES and "ref" in _WORKER:
+        s, ds = _WORKER["ref"]
+        s.reference_run(q, ds)
+        kind = "reference"
+    else:
+        from oracle import ref as O
+        O.reference_run(q, _WORKER["port"])
+        kind = "port"
+    return q, time.perf_counter() - t0, kind
+
+
+def _cpu_sf100_profile() -> dict | None:
+    """The CPU path measured at SF100 on a B200 box's host (tools/sf100_cpu.py):
+    one core per query, committed under profiles/."""
+    if not os.path.exists(CPU_SF100):
+        return None
+    with open(CPU_SF100) as fh:
+        d = json.load(fh)
+    return {"source": "profiles/r2_cpu_sf100.json", "sf": d.get("sf"),
+            "suite_s_1core": d.get("suite_s_1core"), "queries": d.get("n_queries"),
+            "reference_queries_s_1core": d.get("reference_s_1core"), "host": d.get("host")}
+
+
+def cpu_suite(sample_sf: float, processes: int, steps: int, warmup: int):
+    """Wall time of one pass of the 22 queries at SF `sample_sf` on a pool of
+    `processes` host processes (one query per task, longest first)."""
+    import multiprocessing as mp
+    from paper_2506_09226_b200.data import cached_generate
+    cached_generate(sample_sf)          # materialise the cache before timing
+    ctx = mp.get_context("fork")
+    times, per, kinds = [], {}, {}
+    with ctx.Pool(processes, initializer=_cpu_init, initargs=(sample_sf,)) as pool:
+        for i in range(warmup + steps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_query, sorted(QUERIES, key=lambda q: -per.get(q, 0)), chunksize=1)
+            dt = time.perf_counter() - t0
+            per = {q: t for q, t, _ in res}
+            kinds = {q: k for q, _, k in res}
+            if i >= warmup:
+                times.append(dt)
+    return times, per, kinds
 
 
 def run_reference_arm(args) -> None:
-    """--impl reference: the reference's CPU algorithm (the oracle port --
-    the reference is numpy and cannot travel to the GPU box) on all host
-    cores: a pool of worker processes, each holding the SF-`sample` tables,
-    runs the 22 queries (one task per query); a step is the wall time of the
-    whole suite, scaled linearly from the sample SF to `sf`."""
+    """--impl reference: the reference's CPU path on all host cores -- the
+    unmodified reference (baseline/_ref) for its six queries, the oracle port
+    for the other 16 -- one pass of all 22 queries per step on a process pool.
+
+    A step runs on a bounded SF sample (default SF1: an SF100 pass of the
+    CPU path takes ~an hour of core time and ~130 GB of host RAM, see
+    profiles/r2_cpu_sf100.json): `value` is that measured sample, NOT scaled
+    to the headline SF, and `config` says so (same_config: false)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import multiprocessing as mp
     sample = min(args.sf, args.cpu_sample_sf)
-    queries = list(QUERIES)
-    cores = min(len(queries), os.cpu_count() or 1)
-    from paper_2506_09226_b200.data import cached_generate
-    cached_generate(sample)     # materialise the cache before timing
-    ctx = mp.get_context("fork")
-    times, per = [], {}
-    # longest queries first (LPT) so the pool's makespan is tight
-    with ctx.Pool(cores, initializer=_oracle_init, initargs=(sample,)) as pool:
-        for i in range(max(1, args.warmup) + args.steps):
-            t0 = time.perf_counter()
-            res = pool.map(_oracle_query, sorted(queries, key=lambda q: -per.get(q, 0)),
-                           chunksize=1)
-            dt = time.perf_counter() - t0
-            per = dict(res)
-            if i >= max(1, args.warmup):
-                times.append(dt)
-    sample_s = statistics.mean(times)
-    scale = args.sf / sample
-    value = sample_s * scale
+    cores = min(len(QUERIES), os.cpu_count() or 1)
+    times, per, kinds = cpu_suite(sample, cores, args.steps, max(1, args.warmup))
+    value = statistics.mean(times)
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "s",
+        "impl": "reference", "metric": METRIC, "value": round(value, 4), "unit": "s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": value * 1e3, "higher_is_better": False, "scaling": "strong",
-        "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": f"TPC-H {','.join(queries)} at SF{args.sf}",
-                   "sf": args.sf, "queries": queries, "parallelism": "cpu"},
-        "cpu_baseline": {"value": value, "unit": "s", "cores": cores, "kind": "port",
-                         "sample": f"oracle reference_run of all 22 queries at SF{sample} on a "
-                                   f"{cores}-process pool (wall time of the suite, mean of "
-                                   f"{args.steps} steps), scaled x{scale:g} to SF{args.sf}",
-                         "per_query_sample_s": per},
-        "e2e": {"value": value, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "ms_per_step": round(value * 1e3, 2), "higher_is_better": False, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"TPC-H Q1-Q22 at SF{sample:g} (bounded sample of the SF{args.sf:g} "
+                               f"suite; value not scaled)",
+                   "sf": sample, "headline_sf": args.sf, "same_config": sample == args.sf,
+                   "queries": list(QUERIES), "parallelism": f"cpu x{cores} processes"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "s", "cores": cores,
+                         "kind": "reference" if all(kinds.get(q) == "reference"
+                                                    for q in QUERIES) else "port",
+                         "kinds": kinds,
+                         "sample": f"one pass of all 22 queries at SF{sample:g} on {cores} "
+                                   f"processes (wall time, mean of {args.steps} steps): "
+                                   f"{sum(k == 'reference' for k in kinds.values())} by the "
+                                   f"unmodified reference, the rest by the oracle port",
+                         "per_query_s": {q: round(t, 4) for q, t in per.items()}},
+        "measured_at_headline_sf": _cpu_sf100_profile(),
+        "e2e": {"value": round(value, 4), "unit": "s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -320,6 +347,160 @@ def shuffle_bench(ep, gib: float, reps: int = 5) -> dict:
     return out
 
 
+
+# ---------------------------------------------------------------------------
+# parity at the benchmarked scale: the GPU's results vs committed golden
+# results of the CPU path at the same SF (tests/golden/results_sf<sf>.json,
+# produced by tools/sf100_cpu.py / tests/golden/make_scale_results.py)
+# ---------------------------------------------------------------------------
+
+def golden_results(sf: float) -> tuple[dict | None, str | None]:
+    p = os.path.join(ROOT, "tests", "golden", f"results_sf{sf:g}.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as fh:
+        d = json.load(fh)
+    return d, os.path.relpath(p, ROOT)
+
+
+def result_mismatch(got, exp: dict, rtol: float = 1e-9) -> str | None:
+    """None when `got` (a device result table) equals the serialised
+    expected result: names, kinds, row order, integer / date / dict values
+    bit-exact, float64 within rtol."""
+    if got is None:
+        return "no result"
+    ref = got.materialize().to_reference()
+    if list(ref) != list(exp):
+        return f"columns {list(ref)} != {list(exp)}"
+    for name, c in exp.items():
+        kind, v, d = ref[name]
+        if kind != c["kind"]:
+            return f"{name}: kind {kind} != {c['kind']}"
+        if kind == "float64":
+            e = np.asarray([float.fromhex(x) for x in c["hex"]])
+            if len(v) != len(e) or not np.allclose(v, e, rtol=rtol, atol=0):
+                return f"{name}: float values differ"
+        else:
+            e = np.asarray(c["values"], dtype=np.int64)
+            if len(v) != len(e) or not np.array_equal(np.asarray(v).astype(np.int64), e):
+                return f"{name}: values differ"
+            if "dictionary" in c and tuple(d) != tuple(c["dictionary"]):
+                return f"{name}: dictionary differs"
+    return None
+
+
+def parity_report(results: dict, sf: float) -> dict:
+    fix, path = golden_results(sf)
+    if fix is None:
+        return {"sf": sf, "checked": False, "reason": f"no tests/golden/results_sf{sf:g}.json"}
+    bad = {}
+    for q in QUERIES:
+        if q not in fix["results"]:
+            bad[q] = "not in fixture"
+            continue
+        m = result_mismatch(results.get(q), fix["results"][q])
+        if m:
+            bad[q] = m
+    return {"sf": sf, "queries": len(QUERIES), "ok": not bad, "mismatches": bad,
+            "against": fix.get("against", "oracle restatement of the CPU path (numpy), same "
+                                          "generator data"), "fixture": path}
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs 1 and 2 (single queries) and 5 (partition sweep)
+# ---------------------------------------------------------------------------
+
+def time_query(qid: str, tables, steps: int, warmup: int, flush_l2, lib) -> dict:
+    import torch
+    from paper_2506_09226_b200.engine import DeviceContext
+    from paper_2506_09226_b200.queries import PLAN_FUNCTIONS
+    import paper_2506_09226_b200.relops as R
+    from paper_2506_09226_b200.cluster import Endpoint
+
+    ep = Endpoint(0, 1, "nccl")
+
+    def run():
+        r = PLAN_FUNCTIONS[qid](DeviceContext(ep, tables, "default", "default_keys", timed=False))
+        return r.materialize() if r is not None else None
+
+    for _ in range(warmup):
+        run()
+    R.TRACE = set()
+    res = run()
+    alg = sum(nb for _, nb in R.TRACE)
+    R.TRACE = None
+    dev, wall = [], []
+    l0 = lib.scx_launch_count()
+    for _ in range(steps):
+        flush_l2()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        wall.append((time.perf_counter() - t0) * 1e3)
+        dev.append(e0.elapsed_time(e1))
+    pk = peaks()["hbm_gbs"]
+    d = statistics.mean(dev)
+    return {"device_ms": round(d, 4), "wall_ms": round(statistics.mean(wall), 4),
+            "alg_bytes": alg, "roof_frac": round(alg / (d / 1e3) / 1e9 / pk, 4),
+            "launches": int((lib.scx_launch_count() - l0) // max(1, steps)), "result": res}
+
+
+def partition_sweep(sizes_gib, parts_list, reps: int = 3) -> list[dict]:
+    """Config 5 on one GPU: B bytes of 16-byte rows (int64 key uniform in
+    [0, 2^62), int64 payload) hash-partitioned into N destination buffers --
+    the exact data movement of the fused shuffle's send (scx_part_scatter
+    writing each row into its receiver's buffer), with the N receivers being
+    buffers on this GPU.  NVLink is not measurable with one GPU."""
+    import torch
+    from paper_2506_09226_b200 import exchange as X
+    from paper_2506_09226_b200.table import Column, ColumnTable, alloc
+    pk = peaks()["hbm_gbs"]
+    out = []
+    g = torch.Generator(device="cuda")
+    for gib in sizes_gib:
+        rows = int(gib * (1 << 30)) // 16
+        torch.cuda.empty_cache()
+        free, _ = torch.cuda.mem_get_info()
+        if 2 * rows * 16 + (4 << 30) > free:
+            out.append({"gib": gib, "skipped": f"needs {2 * gib:g} GiB + workspace, "
+                                               f"{free / 2**30:.0f} GiB free"})
+            continue
+        g.manual_seed(0)
+        key = torch.randint(0, 2 ** 62, (rows,), dtype=torch.int64, device="cuda", generator=g)
+        pay = torch.arange(rows, dtype=torch.int64, device="cuda")
+        t = ColumnTable({"key": Column("int64", key, 0, None, 0, 2 ** 62),
+                         "payload": Column("int64", pay, 0, None, 0, rows)})
+        for n in parts_list:
+            hist_ms, scat_ms = [], []
+            for i in range(reps + 1):
+                torch.cuda.synchronize()
+                e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                e[0].record()
+                P = X._Partitioner(t, ["key"], n)          # pass 1 (+ counts to host)
+                e[1].record()
+                bufs = [[alloc(int(P.counts[p]), np.int64) for p in range(n)] for _ in range(2)]
+                dst = np.array([[b.data_ptr() for b in row] for row in bufs], np.uint64)
+                e[2].record()
+                P.scatter(dst)                              # pass 2 into N receivers
+                e[3].record()
+                torch.cuda.synchronize()
+                if i:
+                    hist_ms.append(e[0].elapsed_time(e[1]))
+                    scat_ms.append(e[2].elapsed_time(e[3]))
+                del bufs, P
+            h, sc = statistics.mean(hist_ms), statistics.mean(scat_ms)
+            alg = rows * 8 + rows * 32                      # key read by pass 1 + read/write rows
+            out.append({"gib": gib, "rows": rows, "n_dest": n, "hist_ms": round(h, 4),
+                        "scatter_ms": round(sc, 4), "total_ms": round(h + sc, 4),
+                        "alg_bytes": alg, "gbs": round(alg / ((h + sc) / 1e3) / 1e9, 1),
+                        "frac_hbm": round(alg / ((h + sc) / 1e3) / 1e9 / pk, 4)})
+        del key, pay, t
+    return out
+
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
@@ -333,6 +514,9 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample-sf", type=float, default=1.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true")
+    ap.add_argument("--sweep", default="1,2,4,8,16,32,64",
+                    help="config-5 partition sweep sizes (GiB per GPU); empty = skip")
     ap.add_argument("--shuffle-gib", type=float, default=1.0)
     ap.add_argument("--streams", type=int, default=int(os.environ.get("SCX_BENCH_STREAMS", "3")),
                     help="host threads / CUDA streams running the suite's queries concurrently")
@@ -367,9 +551,6 @@ def main() -> None:
     names = sorted(ds.tables)
     tables = load_tables(ds, ep, "default_keys", names=names)
     torch.cuda.synchronize()
-    # one big cached segment for the queries' intermediates (no cudaMalloc
-    # inside the timed region)
-    reserve_device_pool(int(min(96, max(8, args.sf * 0.6)) * (1 << 30)))
 
     dbg = os.environ.get("SCX_BENCH_DEBUG") == "1"
 
@@ -378,8 +559,8 @@ def main() -> None:
         lib.scx_jit_stats(*[_lib.C.byref(x) for x in v])
         return v[0].value
 
-    def suite(tabs, per_query=None):
-        if n_streams > 1:
+    def suite(tabs, per_query=None, concurrent=True):
+        if n_streams > 1 and concurrent:
             return suite_concurrent(tabs, per_query)
         results = {}
         for q in QUERIES:
@@ -463,6 +644,15 @@ def main() -> None:
         load[j] += q_cost.get(q, 1.0)
     assignment = [[q for q in QUERIES if q in a] for a in assignment]
     worker_streams = [torch.cuda.Stream() for _ in range(n_streams)] if n_streams > 1 else []
+    # cached segments for the queries' intermediates (no cudaMalloc inside the
+    # timed region).  The caching allocator reuses a block only on the stream
+    # that allocated it, so the budget is reserved on every stream that runs
+    # queries (the worker streams, and the default stream of the single-stream
+    # and e2e passes)
+    budget = int(min(96, max(8, args.sf * 0.6)) * (1 << 30))
+    for st in worker_streams + [torch.cuda.current_stream()]:
+        with torch.cuda.stream(st):
+            reserve_device_pool(budget // (len(worker_streams) + 1))
     flush = P.table.alloc(64 << 20, np.int64)    # 512 MB > 126 MB L2
 
     def flush_l2():
@@ -534,6 +724,31 @@ def main() -> None:
     clocks = sampler.stop()
     ms = max_over_ranks(statistics.mean(step_ms))
     value = ms / 1e3
+
+    # ---- parity of the timed step's results at this SF (outside the region) ----
+    parity = parity_report(results, args.sf) if ep.rank == 0 else None
+
+    # ---- the same suite on ONE stream: per-query device times that add up ----
+    ss_ms = []
+    q_ms1 = {q: [] for q in QUERIES}
+    for _ in range(args.steps if n_streams > 1 else 0):
+        flush_l2()
+        gc.collect()
+        gc.disable()
+        sync_all()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        per = []
+        e0.record()
+        suite(tables, per, concurrent=False)
+        e1.record()
+        sync_all()
+        gc.enable()
+        ss_ms.append(e0.elapsed_time(e1))
+        for q, a, b in per:
+            q_ms1[q].append(a.elapsed_time(b))
+    if n_streams == 1:
+        ss_ms, q_ms1 = step_ms, q_ms
 
     # ---- e2e: same suite, base columns H2D from pinned host inside the region ----
     host_cols = {}
@@ -632,23 +847,56 @@ def main() -> None:
     per_query = {}
     roof_total = sum(q_bytes.values()) / (pk["hbm_gbs"] * 1e9)
     for q in QUERIES:
-        t = statistics.mean(q_ms[q]) / 1e3 if q_ms[q] else None
+        t = statistics.mean(q_ms1[q]) / 1e3 if q_ms1[q] else None
         b = q_bytes[q]
         t_roof = b / (pk["hbm_gbs"] * 1e9)
         per_query[q] = {"s": round(t, 6) if t else None, "alg_bytes": b,
                         "roof_frac": round(t_roof / t, 4) if t else None,
-                        "s_min": round(min(q_ms[q]) / 1e3, 6) if q_ms[q] else None,
-                        "s_max": round(max(q_ms[q]) / 1e3, 6) if q_ms[q] else None}
+                        "s_min": round(min(q_ms1[q]) / 1e3, 6) if q_ms1[q] else None,
+                        "s_max": round(max(q_ms1[q]) / 1e3, 6) if q_ms1[q] else None,
+                        "s_concurrent": round(statistics.mean(q_ms[q]) / 1e3, 6)
+                        if q_ms[q] else None}
+
+    # ---- BASELINE configs 1 / 2 and the config-5 partition sweep (1 GPU) ----
+    configs = None
+    if ep.n == 1 and not args.no_configs:
+        from paper_2506_09226_b200.engine import load_tables as _lt
+        configs = {}
+        for key, qid, csf in (("config1_q6_sf1", "Q6", 1.0), ("config2_q1_sf10", "Q1", 10.0)):
+            ctab = _lt(cached_generate(csf))
+            r = time_query(qid, ctab, max(5, args.steps), 3, flush_l2, lib)
+            fix, fpath = golden_results(csf)
+            if fix is None and csf == 1.0:
+                fix, fpath = None, None
+            res = r.pop("result")
+            r["parity"] = (None if fix is None else
+                           {"ok": result_mismatch(res, fix["results"][qid]) is None,
+                            "fixture": fpath})
+            r["workload"] = f"TPC-H {qid} at SF{csf:g}, 1 GPU, L2 flushed"
+            configs[key] = r
+            del ctab
+        if args.sweep:
+            del tables, results, res
+            gc.collect()
+            torch.cuda.empty_cache()
+            configs["config5_partition_sweep"] = {
+                "note": "hash partition of B GiB of 16-byte rows into N receiver buffers on one "
+                        "GPU (the fused shuffle's send); NVLink not measurable with one GPU",
+                "points": partition_sweep([float(x) for x in args.sweep.split(",")],
+                                          [1, 2, 4, 8])}
 
     cpu = None
     if ep.rank == 0 and not args.no_cpu:
         sample = min(args.sf, args.cpu_sample_sf)
-        cs, per = _oracle_suite_time(sample, QUERIES, reps=1)
-        cpu = {"value": cs * args.sf / sample, "unit": "s", "cores": 1, "kind": "port",
-               "sample": f"oracle reference_run of the 22 queries at SF{sample} (1 core, "
-                         f"after one warm-up run each), scaled x{args.sf / sample:g} to "
-                         f"SF{args.sf}",
-               "sample_s": round(cs, 4)}
+        times, per_cpu, kinds = cpu_suite(sample, 1, 1, 1)
+        cpu = {"value": round(times[0], 4), "unit": "s", "cores": 1,
+               "kind": "port", "kinds": kinds,
+               "sample": f"one pass of all 22 queries at SF{sample:g}, 1 core (after a warm-up "
+                         f"pass): the unmodified reference (baseline/_ref) for "
+                         f"{sum(k == 'reference' for k in kinds.values())} queries, the oracle "
+                         f"port for the rest; not scaled to SF{args.sf:g}",
+               "per_query_s": {q: round(t, 4) for q, t in per_cpu.items()},
+               "measured_at_headline_sf": _cpu_sf100_profile()}
 
     if ep.rank == 0:
         line = {
@@ -661,7 +909,10 @@ def main() -> None:
                        "sf": args.sf, "queries": list(QUERIES),
                        "parallelism": f"dp{ep.n}", "l2": "flushed between steps (512 MB write)",
                        "layout": "narrowed fixed-point columns in HBM",
-                       "streams": n_streams},
+                       "streams": n_streams,
+                       "execution": "concurrent: queries pulled by %d host threads, one CUDA "
+                                    "stream each (single_stream holds the one-stream time)"
+                                    % n_streams},
             "e2e": {"value": round(e2e_s, 6), "unit": "s", "results_match_device_run": e2e_match,
                     "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes},
@@ -670,10 +921,16 @@ def main() -> None:
             "clocks": clocks,
             "gpu_launches": int(launches // max(1, args.steps)),
             "gpu_launches_total": int(launches),
+            "parity": parity,
+            "single_stream": {"value": round(max_over_ranks(statistics.mean(ss_ms)) / 1e3, 6)
+                              if ss_ms else None, "unit": "s",
+                              "note": "the same suite with every query on one stream, one "
+                                      "after another (per_query.s comes from this pass)"},
             "per_query": per_query,
-            "per_query_note": ("s = interval from a query's first to its last event on its own "
-                               "stream; with streams > 1 queries overlap, so the s values sum "
-                               "to more than the step and roof_frac is a lower bound"),
+            "per_query_note": ("s / roof_frac: the single-stream pass (queries one after "
+                               "another, so they add up); s_concurrent: first-to-last event "
+                               "of the query inside the concurrent timed steps"),
+            "configs": configs,
             "shuffle": shuffle,
             "suite_roofline": {"t_roof_s": round(roof_total, 6),
                                "frac": round(roof_total / value, 4),

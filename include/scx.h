@@ -276,13 +276,15 @@ int scx_lookup_build(const scx_lookup* table, const scx_column* cols, int n_cols
                      void* stream);
 
 /* ---- group table finalize (group_aggregate output, relops.py:115-160) ----
- * DENSE: sums n_ranks partial {lo,hi} accumulator copies (stride cells*M*2
- * words) into one exact 128-bit {lo,hi} per (cell, measure).
+ * DENSE: folds n_ranks partial accumulator copies (stride cells*M*2 words)
+ * per (cell, measure): ops_host[measure] 0 = exact 128-bit {lo,hi} sum,
+ * 1 = min / 2 = max of the int64 in lo (collectives.py:198-206 semantics,
+ * engine.py:342-343 all_reduce_sum).
  * HASH: compacts occupied slots -> out_keys (u64) + out_acc measure-major
  * (out_acc[m * cap + row]), count in count_dev[0].  Row order is slot order
  * (caller sorts by packed key). */
 int scx_dense_reduce(const int64_t* acc_dev, int n_ranks, int cells, int m,
-                     int64_t* out_dev, void* stream);
+                     const int* ops_host, int64_t* out_dev, void* stream);
 int scx_hash_agg_compact(const uint64_t* gkeys_dev, const int64_t* acc_dev,
                          int64_t cap, int m, uint64_t* out_keys_dev,
                          int64_t* out_acc_dev, uint64_t* count_dev, void* stream);

@@ -115,7 +115,7 @@ _PROTOS = {
     "scx_lookup_clear": (C.c_int, [C.POINTER(Lookup), _vp]),
     "scx_lookup_build": (C.c_int, [C.POINTER(Lookup), C.POINTER(Column_), C.c_int,
                                    C.POINTER(KeySpec), i64, _vp, _vp]),
-    "scx_dense_reduce": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp]),
+    "scx_dense_reduce": (C.c_int, [_vp, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int), _vp, _vp]),
     "scx_hash_agg_compact": (C.c_int, [_vp, _vp, i64, C.c_int, _vp, _vp, _vp, _vp]),
     "scx_i128_narrow": (C.c_int, [_vp, _vp, i64, _vp, _vp, _vp]),
     "scx_direct_agg_workspace": (i64, [i64]),

@@ -272,13 +272,16 @@ class Cluster:
     def _wait(self, rank: int, why: str, satisfiable) -> None:
         """Wait on the condition; every live worker blocked with nothing able
         to make progress is a deadlock (transport.py:351-371)."""
-        self._waiting[rank] = why
+        self._waiting[rank] = (why, satisfiable)
         try:
             while not satisfiable():
                 self._raise_if_broken()
                 live = self.n - len(self._finished)
-                if len(self._waiting) >= live and not satisfiable():
-                    desc = "; ".join(f"rank {r}: {w}" for r, w in sorted(self._waiting.items()))
+                # a waiter whose condition already holds has merely not woken
+                # up yet: it is not blocked
+                if (len(self._waiting) >= live
+                        and not any(ok() for _, ok in self._waiting.values())):
+                    desc = "; ".join(f"rank {r}: {w}" for r, (w, _) in sorted(self._waiting.items()))
                     raise DeadlockError(f"all live workers are blocked: {desc}")
                 self._cond.wait(timeout=1.0)
         finally:
@@ -369,9 +372,19 @@ def run_workers(cluster, fn, *args) -> list:
     results: list = [None] * cluster.n
     failures: list[tuple[int, BaseException]] = []
     lock = threading.Lock()
+    device = None
+    try:
+        import torch
+        if torch.cuda.is_available():
+            device = torch.cuda.current_device()
+    except ImportError:  # pragma: no cover
+        pass
 
     def body(ep: Endpoint) -> None:
         try:
+            if device is not None:        # workers run on the caller's GPU
+                import torch
+                torch.cuda.set_device(device)
             results[ep.rank] = fn(ep, *args)
         except _Aborted:
             pass

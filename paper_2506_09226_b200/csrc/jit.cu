@@ -1525,6 +1525,14 @@ static int plan_launch_uncached(const scx_pipeline& P, LaunchPlan& lp);
 static int plan_launch(const scx_pipeline& P, LaunchPlan& lp) {
   int dev = 0;
   SCX_CUDA(cudaGetDevice(&dev));
+  // the module / occupancy / launch calls below are driver API: they need the
+  // device's primary context current on THIS thread, which a thread that has
+  // only made runtime calls (or none) may not have yet
+  static thread_local int t_ctx_dev = -1;
+  if (t_ctx_dev != dev) {
+    SCX_CUDA(cudaSetDevice(dev));
+    t_ctx_dev = dev;
+  }
   std::string key(reinterpret_cast<const char*>(&P), sizeof(P));
   key.append(reinterpret_cast<const char*>(&dev), sizeof(dev));
   {

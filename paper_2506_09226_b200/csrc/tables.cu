@@ -73,10 +73,27 @@ __global__ void lookup_build_kernel(scx_lookup T, BuildCols C, scx_keyspec K, in
 
 // exact reduction of n_ranks partial {lo,hi} accumulators into 3 x 42-bit
 // signed limbs is unnecessary on one device: we emit {lo, hi} summed.
-__global__ void dense_reduce_kernel(const int64_t* acc, int n_ranks, int64_t words,
-                                    int64_t* out) {
+struct ReduceOps {
+  int8_t op[SCX_MAX_MEASURES];             // 0 = 128-bit sum, 1 = min, 2 = max
+};
+
+// Cross-rank fold of dense group-by accumulators: cell (c, m) is an exact
+// {lo, hi} 128-bit sum, or for a min / max measure an int64 in lo (hi = 0).
+__global__ void dense_reduce_kernel(const int64_t* acc, int n_ranks, int64_t words, int m,
+                                    ReduceOps ops, int64_t* out) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= words / 2) return;
+  const int op = ops.op[i % m];
+  if (op != 0) {
+    int64_t v = acc[2 * i];
+    for (int r = 1; r < n_ranks; ++r) {
+      const int64_t x = acc[r * words + 2 * i];
+      v = op == 1 ? (x < v ? x : v) : (x > v ? x : v);
+    }
+    out[2 * i] = v;
+    out[2 * i + 1] = 0;
+    return;
+  }
   uint64_t lo = 0;
   int64_t hi = 0;
   for (int r = 0; r < n_ranks; ++r) {
@@ -284,15 +301,23 @@ extern "C" int scx_lookup_build(const scx_lookup* T, const scx_column* cols, int
   return SCX_OK;
 }
 
-extern "C" int scx_dense_reduce(const int64_t* acc, int n_ranks, int cells, int m, int64_t* out,
-                                void* stream) {
-  if (!acc || !out || n_ranks < 1 || cells < 1 || m < 1) {
+extern "C" int scx_dense_reduce(const int64_t* acc, int n_ranks, int cells, int m,
+                                const int* ops_host, int64_t* out, void* stream) {
+  if (!acc || !out || !ops_host || n_ranks < 1 || cells < 1 || m < 1 || m > SCX_MAX_MEASURES) {
     set_error("dense_reduce: bad arguments");
     return SCX_EINVAL;
   }
+  ReduceOps ops;
+  for (int j = 0; j < m; ++j) {
+    if (ops_host[j] < 0 || ops_host[j] > 2) {
+      set_error("dense_reduce: measure %d has op %d (0 sum, 1 min, 2 max)", j, ops_host[j]);
+      return SCX_EINVAL;
+    }
+    ops.op[j] = (int8_t)ops_host[j];
+  }
   const int64_t words = 2ll * cells * m;
   dense_reduce_kernel<<<(int)((words / 2 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      acc, n_ranks, words, out);
+      acc, n_ranks, words, m, ops, out);
   SCX_CHECK_LAUNCH("dense_reduce_kernel");
   return SCX_OK;
 }

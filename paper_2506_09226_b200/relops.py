@@ -1417,7 +1417,9 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
         from .exchange import all_gather_tensor
         parts = all_gather_tensor(cross.ep, acc)
         red = torch.empty_like(acc)
-        L.call("scx_dense_reduce", _ptr(parts), cross.ep.n, cells, M, _ptr(red), _stream())
+        ops = (C.c_int * M)(*[1 if op == "min" else (2 if op == "max" else 0)
+                             for op, _ in measures])
+        L.call("scx_dense_reduce", _ptr(parts), cross.ep.n, cells, M, ops, _ptr(red), _stream())
         acc = red
     return finish_dense(_to_host(acc), keys, kcols, cards, luts, plan, measures, count_m)
 
@@ -1806,6 +1808,8 @@ def sort_pairs(keys, vals, n_bits: int):
 def _col_range(c: Column) -> tuple[int, int]:
     if c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo:
         return c.lo, c.hi
+    if c.row_count == 0:           # no values (e.g. a worker's empty partition)
+        return 0, 0
     mm = alloc(2, np.int64)
     L.call("scx_fill_rows", _ptr(mm), 1, 2, (C.c_int64 * 2)(INT64_MAX, INT64_MIN), _stream())
     L.call("scx_minmax", c.scx(), c.row_count, _ptr(mm), _stream())

@@ -216,3 +216,134 @@ def test_q9_counts_repeated_partsupp_pairs():
     assert decoded(r, "nation") == list(g.n_name)
     assert list(r["o_year"][1]) == list(g.yr)
     assert [round(x * 10000) for x in r["sum_profit"][1]] == list(g.amt)
+
+
+# ---- second formulations for Q2 Q7 Q8 Q11 Q15 Q17 Q20 (no
+# independent cross-check yet).  SQL text per TPC-H; money compared in cents.
+
+def _nations_in(T, region):
+    n, r = df(T, "nation"), df(T, "region")
+    return n[n.n_regionkey.isin(r.loc[r.r_name == region, "r_regionkey"])]
+
+
+def test_q2_pandas():
+    T = tables(sf=0.1)
+    p, s, ps = df(T, "part"), df(T, "supplier"), df(T, "partsupp")
+    eu = _nations_in(T, "EUROPE")[["n_nationkey", "n_name"]]
+    pse = ps.merge(s, left_on="ps_suppkey", right_on="s_suppkey") \
+        .merge(eu, left_on="s_nationkey", right_on="n_nationkey")
+    pse["cost"] = cents(pse.ps_supplycost)
+    mins = pse.groupby("ps_partkey").cost.min()
+    pf = p[(p.p_size == 15) & p.p_type.str.endswith("BRASS")]
+    m = pse.merge(pf, left_on="ps_partkey", right_on="p_partkey")
+    m = m[m.cost == mins.loc[m.ps_partkey].values]
+    m = m.assign(bal=cents(m.s_acctbal)).sort_values(
+        ["bal", "n_name", "s_suppkey", "p_partkey"], ascending=[False, True, True, True]).head(100)
+    r = E.q2(T)
+    assert len(m) > 0
+    assert list(r["s_suppkey"][1]) == list(m.s_suppkey)
+    assert list(r["p_partkey"][1]) == list(m.p_partkey)
+    assert decoded(r, "n_name") == list(m.n_name)
+    assert list(cents(pd.Series(r["s_acctbal"][1]))) == list(m.bal)
+
+
+def test_q7_pandas():
+    T = tables(sf=0.1)
+    li, o, c, s, n = (df(T, x) for x in ("lineitem", "orders", "customer", "supplier", "nation"))
+    li = li[(li.l_shipdate >= O.days("1995-01-01")) & (li.l_shipdate <= O.days("1996-12-31"))]
+    m = li.merge(s[["s_suppkey", "s_nationkey"]], left_on="l_suppkey", right_on="s_suppkey") \
+        .merge(o[["o_orderkey", "o_custkey"]], left_on="l_orderkey", right_on="o_orderkey") \
+        .merge(c[["c_custkey", "c_nationkey"]], left_on="o_custkey", right_on="c_custkey")
+    nm = dict(zip(n.n_nationkey, n.n_name))
+    m["sn"], m["cn"] = m.s_nationkey.map(nm), m.c_nationkey.map(nm)
+    m = m[((m.sn == "FRANCE") & (m.cn == "GERMANY")) | ((m.sn == "GERMANY") & (m.cn == "FRANCE"))]
+    m["y"] = pd.to_datetime(m.l_shipdate, unit="D").dt.year
+    m["vol"] = cents(m.l_extendedprice) * (100 - cents(m.l_discount))
+    g = m.groupby(["sn", "cn", "y"]).vol.sum().reset_index().sort_values(["sn", "cn", "y"])
+    r = E.q7(T)
+    assert len(g) > 0
+    assert decoded(r, "supp_nation") == list(g.sn)
+    assert decoded(r, "cust_nation") == list(g.cn)
+    assert list(r["l_year"][1]) == list(g.y)
+    assert [round(x * 10000) for x in r["revenue"][1]] == list(g.vol)
+
+
+def test_q8_pandas():
+    T = tables(sf=0.1)
+    li, o, c, s, p, n = (df(T, x) for x in ("lineitem", "orders", "customer", "supplier", "part",
+                                             "nation"))
+    am = _nations_in(T, "AMERICA").n_nationkey
+    o = o[(o.o_orderdate >= O.days("1995-01-01")) & (o.o_orderdate <= O.days("1996-12-31"))]
+    m = li.merge(p.loc[p.p_type == "ECONOMY ANODIZED STEEL", ["p_partkey"]],
+                 left_on="l_partkey", right_on="p_partkey") \
+        .merge(o[["o_orderkey", "o_custkey", "o_orderdate"]], left_on="l_orderkey",
+               right_on="o_orderkey") \
+        .merge(c[["c_custkey", "c_nationkey"]], left_on="o_custkey", right_on="c_custkey") \
+        .merge(s[["s_suppkey", "s_nationkey"]], left_on="l_suppkey", right_on="s_suppkey")
+    m = m[m.c_nationkey.isin(am)]
+    br = int(n.loc[n.n_name == "BRAZIL", "n_nationkey"].iloc[0])
+    m["vol"] = cents(m.l_extendedprice) * (100 - cents(m.l_discount))
+    m["bv"] = np.where(m.s_nationkey == br, m.vol, 0)
+    m["y"] = pd.to_datetime(m.o_orderdate, unit="D").dt.year
+    g = m.groupby("y")[["vol", "bv"]].sum().reset_index().sort_values("y")
+    r = E.q8(T)
+    assert len(g) > 0
+    assert list(r["o_year"][1]) == list(g.y)
+    np.testing.assert_allclose(r["mkt_share"][1], g.bv / g.vol, rtol=1e-12)
+
+
+def test_q11_pandas():
+    T = tables(sf=0.1)
+    ps, s, n = df(T, "partsupp"), df(T, "supplier"), df(T, "nation")
+    de = n.loc[n.n_name == "GERMANY", "n_nationkey"]
+    m = ps.merge(s[["s_suppkey", "s_nationkey"]], left_on="ps_suppkey", right_on="s_suppkey")
+    m = m[m.s_nationkey.isin(de)]
+    m["v"] = cents(m.ps_supplycost) * m.ps_availqty
+    g = m.groupby("ps_partkey").v.sum().reset_index()
+    g = g[g.v * 10000 > m.v.sum()].sort_values(["v", "ps_partkey"], ascending=[False, True])
+    r = E.q11(T)
+    assert len(g) > 0
+    assert list(r["ps_partkey"][1]) == list(g.ps_partkey)
+    assert list(cents(pd.Series(r["value"][1]))) == list(g.v)
+
+
+def test_q15_pandas():
+    T = tables(sf=0.1)
+    li, s = df(T, "lineitem"), df(T, "supplier")
+    li = li[(li.l_shipdate >= O.days("1996-01-01")) & (li.l_shipdate < O.days("1996-04-01"))]
+    rev = (cents(li.l_extendedprice) * (100 - cents(li.l_discount))).groupby(li.l_suppkey).sum()
+    top = rev[rev == rev.max()]
+    top = top[top.index.isin(s.s_suppkey)].sort_index()
+    r = E.q15(T)
+    assert len(top) > 0
+    assert list(r["s_suppkey"][1]) == list(top.index)
+    assert [round(x * 10000) for x in r["total_revenue"][1]] == list(top.values)
+
+
+def test_q17_pandas():
+    T = tables(sf=0.1)
+    li, p = df(T, "lineitem"), df(T, "part")
+    pk = p.loc[(p.p_brand == "Brand#23") & (p.p_container == "MED BOX"), "p_partkey"]
+    m = li[li.l_partkey.isin(pk)]
+    avg = m.groupby("l_partkey").l_quantity.mean()
+    small = m[m.l_quantity < 0.2 * avg.loc[m.l_partkey].values]
+    r = E.q17(T)
+    assert len(m) > 0
+    assert r["avg_yearly"][1][0] == pytest.approx(cents(small.l_extendedprice).sum() / 100 / 7,
+                                                  rel=1e-12)
+
+
+def test_q20_pandas():
+    T = tables(sf=0.1)
+    li, p, ps, s, n = (df(T, x) for x in ("lineitem", "part", "partsupp", "supplier", "nation"))
+    fp = p.loc[p.p_name.str.startswith("forest"), "p_partkey"]
+    li = li[(li.l_shipdate >= O.days("1994-01-01")) & (li.l_shipdate < O.days("1995-01-01"))]
+    q = li.groupby(["l_partkey", "l_suppkey"]).l_quantity.sum().rename("sq").reset_index()
+    m = ps[ps.ps_partkey.isin(fp)].merge(q, left_on=["ps_partkey", "ps_suppkey"],
+                                         right_on=["l_partkey", "l_suppkey"])
+    good = m.loc[m.ps_availqty > 0.5 * m.sq, "ps_suppkey"].unique()
+    ca = n.loc[n.n_name == "CANADA", "n_nationkey"]
+    out = np.sort(s.loc[s.s_suppkey.isin(good) & s.s_nationkey.isin(ca), "s_suppkey"].values)
+    r = E.q20(T)
+    assert len(out) > 0
+    assert list(r["s_suppkey"][1]) == list(out)

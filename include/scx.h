@@ -470,6 +470,31 @@ int scx_join_expand(const void* ws_dev, int64_t n, const uint32_t* rperm_dev, in
 int scx_remap_codes(scx_column in, int64_t n, const int32_t* lut_dev, int32_t lut_n,
                     scx_column out, int* bad_dev, void* stream);
 
+/* ---- NCCL data plane of the exchanges (process-per-GPU jobs) ---------------
+ * Communicators are opaque handles (ncclComm_t).  Counts / offsets / sizes
+ * are HOST arrays of length nranks; all transfers are asynchronous on
+ * `stream`.  Replaces: exchange.py:73-97 size_exchange and 131-174
+ * shuffle_table (scx_alltoallv: one group of ncclSend/ncclRecv, the paper's
+ * Alg. 1), exchange.py:195-285 broadcast_table (scx_bcast_group: the N root
+ * broadcasts of a column in ONE group, Alg. 2), collectives.py:199-213
+ * all_reduce on exact integers (scx_allreduce_i64, op 0 sum / 1 min / 2 max),
+ * engine.py:345-365 gather (scx_gather_to0). */
+int scx_nccl_version(int* version);
+int64_t scx_comm_id_bytes(void);
+int scx_comm_unique_id(void* id_out);
+int scx_comm_init_rank(void** comm_out, int nranks, const void* id, int rank);
+int scx_comm_init_all(int n, const int* devs, void** comms_out);
+int scx_comm_destroy(void* comm);
+int scx_alltoallv(void* comm, const void* send_dev, const int64_t* send_counts,
+                  const int64_t* send_offs, void* recv_dev, const int64_t* recv_counts,
+                  const int64_t* recv_offs, int elem_bytes, void* stream);
+int scx_bcast_group(void* comm, void* const* bufs_dev, const int64_t* bytes, int n_roots,
+                    void* stream);
+int scx_allreduce_i64(void* comm, const int64_t* send_dev, int64_t* recv_dev, int64_t count,
+                      int op, void* stream);
+int scx_gather_to0(void* comm, const void* send_dev, int64_t bytes, void* const* recv_dev,
+                   const int64_t* recv_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

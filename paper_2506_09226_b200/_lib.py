@@ -160,6 +160,17 @@ _PROTOS = {
     "scx_join_match": (C.c_int, [_vp, i64, _vp, i64, _vp, _vp, _vp]),
     "scx_join_expand": (C.c_int, [_vp, i64, _vp, i64, _vp, _vp, _vp]),
     "scx_remap_codes": (C.c_int, [Column_, i64, _vp, C.c_int32, Column_, _vp, _vp]),
+    "scx_nccl_version": (C.c_int, [C.POINTER(C.c_int)]),
+    "scx_comm_id_bytes": (i64, []),
+    "scx_comm_unique_id": (C.c_int, [_vp]),
+    "scx_comm_init_rank": (C.c_int, [C.POINTER(_vp), C.c_int, _vp, C.c_int]),
+    "scx_comm_init_all": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(_vp)]),
+    "scx_comm_destroy": (C.c_int, [_vp]),
+    "scx_alltoallv": (C.c_int, [_vp, _vp, C.POINTER(i64), C.POINTER(i64), _vp, C.POINTER(i64),
+                                C.POINTER(i64), C.c_int, _vp]),
+    "scx_bcast_group": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(i64), C.c_int, _vp]),
+    "scx_allreduce_i64": (C.c_int, [_vp, _vp, _vp, i64, C.c_int, _vp]),
+    "scx_gather_to0": (C.c_int, [_vp, _vp, i64, C.POINTER(_vp), C.POINTER(i64), _vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

@@ -22,6 +22,21 @@ CUDA_LIB = "/usr/local/cuda/lib64"
 # rpath into the image's CUDA toolkit (the GPU box runs the same image)
 LINK = ["-L" + CUDA_LIB, "-lnvrtc", "-Xlinker", "-rpath=" + CUDA_LIB, "-ldl"]
 
+
+def _nccl_dir() -> str:
+    """The pip NCCL (nvidia-nccl-cu12 2.28.9, the one torch loads): headers +
+    libnccl.so.2, linked by rpath (the GPU box runs the same image)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec is None or not spec.submodule_search_locations:
+        raise RuntimeError("pip NCCL (nvidia.nccl) not found; libscx.so needs it for comm.cu")
+    return list(spec.submodule_search_locations)[0]
+
+
+NCCL = _nccl_dir()
+LINK += ["-L" + os.path.join(NCCL, "lib"), "-l:libnccl.so.2",
+         "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
+
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
          "--expt-relaxed-constexpr", "-I", INCLUDE]
@@ -56,7 +71,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            jobs.append([nvcc, *ARCH, *FLAGS, "-c", src, "-o", obj])
+            extra = ["-I", os.path.join(NCCL, "include")] if src.endswith("comm.cu") else []
+            jobs.append([nvcc, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

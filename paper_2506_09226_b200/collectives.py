@@ -202,16 +202,10 @@ def all_reduce(ep: Endpoint, values, op: str = "sum") -> np.ndarray:
                                      lambda slots: _fold(op, slots)).copy()
     if ep.n == 1:
         return _fold(op, [vec])
-    import torch
-    import torch.distributed as dist
-    shape = torch.tensor(list(vec.shape) + [-1] * (4 - vec.ndim), dtype=torch.int64, device=ep.device)
-    shapes = torch.empty(ep.n * 4, dtype=torch.int64, device=ep.device)
-    dist.all_gather_into_tensor(shapes, shape, group=ep.group)
-    if len({tuple(r) for r in shapes.view(ep.n, 4).cpu().tolist()}) > 1:
+    from .nccl import allgather_bytes
+    shape = np.asarray(list(vec.shape) + [-1] * (4 - vec.ndim), np.int64)
+    if len({tuple(r) for r in allgather_bytes(ep, shape).view(np.int64).reshape(ep.n, 4)
+            .tolist()}) > 1:
         raise ProtocolError("all_reduce length mismatch across workers")
-    raw = np.ascontiguousarray(vec).view(np.uint8).reshape(-1)
-    t = torch.from_numpy(raw.copy()).to(ep.device)
-    out = torch.empty(ep.n * t.numel(), dtype=torch.uint8, device=ep.device)
-    dist.all_gather_into_tensor(out, t, group=ep.group)
-    parts = out.view(ep.n, -1).cpu().numpy()
+    parts = allgather_bytes(ep, np.ascontiguousarray(vec).view(np.uint8).reshape(-1))
     return _fold(op, [p.view(vec.dtype).reshape(vec.shape) for p in parts])

@@ -317,9 +317,27 @@ class DeviceContext:
             # drops its partial (one shared stream)
             self.ep.cluster.rendezvous(self.ep.rank, "gather:done", None, lambda s: None)
             return full
-        import torch.distributed as dist
         names = t.column_names
         counts, _ = X.size_exchange(self.ep, np.full(self.ep.n, t.row_count, dtype=np.int64))
+        from .nccl import comm_of
+        c = comm_of(self.ep)
+        if c is not None:             # NCCL through the C-ABI (scx_gather_to0)
+            parts_cols = [dict() for _ in range(self.ep.n)]
+            for name in names:
+                ref = t.column(name)
+                src = ref.data.contiguous()
+                if self.is_root:
+                    bufs = [R.alloc(int(counts[r]), ref.np_dtype) for r in range(self.ep.n)]
+                    c.gather_to0(src, src.numel() * src.element_size(), bufs,
+                                 [int(counts[r]) * ref.itemsize for r in range(self.ep.n)])
+                    for r in range(self.ep.n):
+                        parts_cols[r][name] = t.column(name) if r == 0 else ref.like(bufs[r])
+                else:
+                    c.gather_to0(src, src.numel() * src.element_size())
+            if not self.is_root:
+                return None
+            return concat_tables([t] + [ColumnTable(pc) for pc in parts_cols[1:]])
+        import torch.distributed as dist
         parts = [t] if self.is_root else []
         if self.is_root:
             for src in range(1, self.ep.n):

@@ -19,14 +19,18 @@ exchange.py`):
     source (no send buffer, no copy).  The same destination-pointer kernel
     targets a peer GPU's HBM when the receive buffers are peer-mapped.
   - One process per GPU: partition into a local send buffer, then one
-    all-to-all-v per column (NCCL grouped send/recv = the paper's Alg. 1).
+    all-to-all-v per column: ``scx_alltoallv`` = one NCCL group of
+    send/recv behind the C-ABI (the paper's Alg. 1; csrc/comm.cu).
 * ``broadcast_table`` (177-285): every worker gets the rank-ordered
   concatenation; differing dictionaries are reconciled first (union in
   rank order, codes remapped on the device, exchange.py:177-192,217-251).
 
 Exchange metadata (schema check, per-column value ranges, the size matrix)
 travels in ONE collective per exchange: a rendezvous in-process, a single
-int64 all-gather across processes (no pickled objects).
+int64 all-gather across processes (no pickled objects).  Across NCCL
+processes every data-plane transfer goes through libscx's NCCL entry points
+(nccl.py); torch.distributed only bootstraps the job (and runs the gloo
+CPU protocol tests).
 """
 
 from __future__ import annotations
@@ -39,6 +43,7 @@ import numpy as np
 
 from . import _lib as L
 from .cluster import Endpoint, ProtocolError
+from .nccl import allgather_bytes, comm_of
 from .table import Column, ColumnTable, SchemaError, alloc, narrow_dtype, torch_dtype
 
 _HASHABLE_KINDS = ("int64", "date32", "dict")
@@ -232,10 +237,7 @@ def _dist_meta(ep: Endpoint, sig, metas, row, table, dicts):
         d = table.column(nm).dictionary
         if d is not None:
             v[dh + i] = _schema_hash(d)
-    t = torch.from_numpy(v).to(ep.device)
-    out = torch.empty(ep.n * width, dtype=torch.int64, device=ep.device)
-    dist.all_gather_into_tensor(out, t, group=ep.group)
-    allv = out.view(ep.n, width).cpu().numpy()
+    allv = allgather_bytes(ep, v).view(np.int64).reshape(ep.n, width)
     if len({int(r[0]) for r in allv}) > 1:
         raise SchemaError("exchange: schema mismatch across workers")
     slots = []
@@ -332,12 +334,7 @@ def size_exchange(ep: Endpoint, my_row) -> tuple[np.ndarray, np.ndarray]:
         M = ep.cluster.rendezvous(ep.rank, "size_exchange", row, lambda s: np.stack(s))
         incoming = M[:, ep.rank].copy()
     else:
-        torch = _torch()
-        import torch.distributed as dist
-        send = torch.from_numpy(row).to(ep.device)
-        recv = torch.empty_like(send)
-        dist.all_to_all_single(recv, send, group=ep.group)
-        incoming = recv.cpu().numpy()
+        incoming = allgather_bytes(ep, row).view(np.int64).reshape(ep.n, ep.n)[:, ep.rank].copy()
     offsets = np.zeros(len(incoming), dtype=np.int64)
     np.cumsum(incoming[:-1], out=offsets[1:])
     return incoming, offsets
@@ -354,7 +351,13 @@ def alltoallv(ep: Endpoint, send, send_counts, recv_counts):
         if total:
             out.copy_(send[:total])
         return out
-    import torch.distributed as dist
+    c = comm_of(ep)
+    if c is not None:                 # NCCL through the C-ABI: one group of send/recv
+        so = np.concatenate([[0], np.cumsum(send_counts)[:-1]])
+        ro = np.concatenate([[0], np.cumsum(recv_counts)[:-1]])
+        c.alltoallv(send, send_counts, so, out, recv_counts, ro, send.element_size())
+        return out
+    import torch.distributed as dist  # gloo (CPU protocol tests)
     dist.all_to_all_single(out, send, [int(x) for x in recv_counts],
                            [int(x) for x in send_counts], group=ep.group)
     return out
@@ -455,6 +458,19 @@ def broadcast_table(ep: Endpoint, table, stats: ExchangeStats | None = None,
                     if counts[r]:
                         outs[nm][offs[r]:offs[r + 1]].copy_(peers[r][nm])
             ep.cluster.rendezvous(ep.rank, "broadcast:done", None, lambda s: None)
+        elif comm_of(ep) is not None:
+            c = comm_of(ep)
+            for nm in names:
+                src = cols[nm].data.contiguous()
+                w = cols[nm].itemsize
+                outs[nm][offs[ep.rank]:offs[ep.rank + 1]].copy_(src)
+                if use_p2p:   # N-1 sends of this rank's rows + N-1 receives, one group
+                    sc = [0 if d == ep.rank else int(counts[ep.rank]) for d in range(n)]
+                    rc = [0 if r == ep.rank else int(counts[r]) for r in range(n)]
+                    c.alltoallv(src, sc, [0] * n, outs[nm], rc, offs[:-1], w)
+                else:         # the N root broadcasts of the column in ONE group (Alg. 2)
+                    c.bcast_group([outs[nm][offs[r]:offs[r + 1]] if counts[r] else None
+                                   for r in range(n)], [int(counts[r]) * w for r in range(n)])
         else:
             import torch.distributed as dist
             for nm in names:
@@ -501,8 +517,11 @@ def all_gather_tensor(ep: Endpoint, t):
         out = torch.stack(parts)
         ep.cluster.rendezvous(ep.rank, "all_gather_tensor:done", None, lambda s: None)
         return out
+    c = comm_of(ep)
+    if c is not None:
+        return c.allgather(t.contiguous().reshape(-1)).view(ep.n, *t.shape)
     import torch.distributed as dist
-    # flat output: gloo requires it, NCCL accepts it
+    # flat output: gloo requires it
     out = torch.empty(ep.n * t.numel(), dtype=t.dtype, device=t.device)
     dist.all_gather_into_tensor(out, t.contiguous().reshape(-1), group=ep.group)
     return out.view(ep.n, *t.shape)

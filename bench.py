@@ -480,8 +480,9 @@ def partition_sweep(sizes_gib, parts_list, reps: int = 3) -> list[dict]:
                 torch.cuda.synchronize()
                 e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
                 e[0].record()
-                P = X._Partitioner(t, ["key"], n)          # pass 1 (+ counts to host)
+                P = X._Partitioner(t, ["key"], n, fetch=False)   # pass 1
                 e[1].record()
+                P.fetch_counts()
                 bufs = [[alloc(int(P.counts[p]), np.int64) for p in range(n)] for _ in range(2)]
                 dst = np.array([[b.data_ptr() for b in row] for row in bufs], np.uint64)
                 e[2].record()
@@ -764,7 +765,8 @@ def main() -> None:
     host_cols = {}
     for tname in names:
         for cname, hc in host_tables[tname].columns.items():
-            src = torch.from_numpy(np.ascontiguousarray(hc.values)).pin_memory()
+            v = np.ascontiguousarray(hc.values)
+            src = torch.from_numpy(v if v.flags.writeable else v.copy()).pin_memory()
             host_cols[(tname, cname)] = src
     h2d_bytes = sum(t.numel() * t.element_size() for t in host_cols.values())
     # N=1: tables stream in on a copy stream (largest / most-used first) and

@@ -99,7 +99,8 @@ class _Partitioner:
     """Pass 1 (counts) now, pass 2 (scatter to any destinations) later --
     between them the caller learns the sizes and places the receive buffers."""
 
-    def __init__(self, table: ColumnTable, key_columns: list[str], n_parts: int):
+    def __init__(self, table: ColumnTable, key_columns: list[str], n_parts: int,
+                 fetch: bool = True):
         if n_parts < 1:
             raise ValueError("n_parts must be >= 1")
         if n_parts > 64:
@@ -112,10 +113,18 @@ class _Partitioner:
         self.karr = (L.Column_ * len(keys))(*[c.scx() for c in keys])
         self.n_keys = len(keys)
         self.ws = alloc(max(16, L.load().scx_part_workspace(self.n, n_parts)), np.uint8)
-        cnt = alloc(n_parts, np.uint64)
+        self._cnt = alloc(n_parts, np.uint64)
         L.call("scx_part_hist", self.karr, self.n_keys, self.n, n_parts,
-               C.c_void_p(self.ws.data_ptr()), C.c_void_p(cnt.data_ptr()), _stream())
-        self.counts = cnt.cpu().numpy().astype(np.int64)
+               C.c_void_p(self.ws.data_ptr()), C.c_void_p(self._cnt.data_ptr()), _stream())
+        self.counts = None
+        if fetch:
+            self.fetch_counts()
+
+    def fetch_counts(self) -> np.ndarray:
+        """Per-part row totals to the host (waits for pass 1)."""
+        if self.counts is None:
+            self.counts = self._cnt.cpu().numpy().astype(np.int64)
+        return self.counts
 
     def scatter(self, dst_addr: np.ndarray) -> None:
         """dst_addr[c, p]: device byte address of column c's part-p run."""

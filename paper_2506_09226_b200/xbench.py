@@ -14,9 +14,12 @@ Throughput = msg * N / 1e9 / elapsed (GB/s, `bench.py:141-143`, 1 GB = 1e9 B
 as in `topology.py:20`), elapsed = mean over repetitions of the max over
 ranks, each repetition bracketed by barriers.  On GPUs the repetition is
 timed with CUDA events on the current stream; with gloo (CPU tests) by the
-host clock.  Like the reference's in-process mode this moves real bytes and
-reports no model comparison (`model_thpt_gbps` / `relative_error` are None):
-the analytic models are out of scope.
+host clock.  Next to every measured row stands the paper's analytic model for
+the same topology (`models.py:65-89`: shuffle k^2 B_g/(k-1) inside one
+machine, broadcast k B_g/(k-1); multi-machine forms likewise), with
+relative_error = |model - measured| / measured as in `bench.py:156-159` --
+the reference prints this overlay only for its simulator, here it sits
+beside real NVLink measurements.
 """
 
 from __future__ import annotations
@@ -35,6 +38,22 @@ ROW_FIELDS = ["op", "msg_bytes", "k", "v", "bn_gbps", "bg_gbps", "efficiency",
 
 class BenchError(ValueError):
     pass
+
+
+def model_throughput(op: str, topo) -> float:
+    """Paper model throughput in GB/s (models.py:65-89); broadcast_p2p is
+    compared with the collective broadcast model (bench.py:114-119)."""
+    import math
+    k, v = topo.k, topo.v
+    bg = topo.bg_gbps * (getattr(topo, "bg_efficiency", None) or topo.efficiency)
+    bn = topo.bn_gbps * (getattr(topo, "bn_efficiency", None) or topo.efficiency)
+    if k * v == 1:
+        return math.inf
+    if op == "shuffle":
+        return k * k * bg / (k - 1) if v == 1 else (1.0 + 1.0 / (v - 1)) * v * bn
+    if v == 1:
+        return k * bg / (k - 1)
+    return (1.0 + 1.0 / (v - 1)) * (k * bn * bg) / (k * bg + (k - 1) * bn)
 
 
 @dataclass
@@ -167,11 +186,15 @@ def run_bench(ep: Endpoint, spec: BenchSpec) -> list[dict]:
                 dt = time.perf_counter() - t0
             elapsed += _max_over_ranks(ep, dt)
         elapsed /= spec.repetitions
+        measured = msg * ep.n / GB / elapsed if elapsed > 0 else float("inf")
+        model = model_throughput(spec.op, topo)
+        finite = model != float("inf") and measured not in (0.0, float("inf"))
         rows.append({
             "op": spec.op, "msg_bytes": msg, "k": topo.k, "v": topo.v,
             "bn_gbps": topo.bn_gbps, "bg_gbps": topo.bg_gbps, "efficiency": topo.efficiency,
-            "measured_thpt_gbps": msg * ep.n / GB / elapsed if elapsed > 0 else float("inf"),
-            "model_thpt_gbps": None, "relative_error": None,
+            "measured_thpt_gbps": measured,
+            "model_thpt_gbps": model if finite else None,
+            "relative_error": abs(model - measured) / measured if finite else None,
         })
         del buf, out
     return rows

@@ -136,3 +136,19 @@ def test_bench_one_gpu_nccl_path(tmp_path):
                      "--out", str(out)]) == 0
     rows = list(csv.reader(open(out)))
     assert len(rows) == 3 and all(float(r[7]) > 0 for r in rows[1:])
+
+
+@pytest.mark.parametrize("k,v,bg,bn,eff,shuf,bcast", [
+    (8, 1, 900, 900, 0.8, 6582.857142857143, 822.8571428571429),
+    (4, 2, 900, 50, 0.8, 160.0, 76.8),
+    (8, 4, 900, 400, 0.9, 1920.0, 345.6),
+    (2, 1, 900, 900, 1.0, 3600.0, 1800.0)])
+def test_model_overlay_matches_reference_models(k, v, bg, bn, eff, shuf, bcast):
+    """xbench's model column == shufflecast.models (values computed by the
+    reference's models.py:65-89 in the dev container)."""
+    from paper_2506_09226_b200.cluster import Topology
+    from paper_2506_09226_b200.xbench import model_throughput
+    t = Topology(k, v, bg, bn, eff)
+    assert model_throughput("shuffle", t) == pytest.approx(shuf, rel=1e-12)
+    assert model_throughput("broadcast", t) == pytest.approx(bcast, rel=1e-12)
+    assert model_throughput("broadcast_p2p", t) == pytest.approx(bcast, rel=1e-12)

@@ -174,3 +174,22 @@ def test_skewed_data_n8(qid):
     per = _DS[(0.05, 1.5)][2].setdefault("_per8", P.partition_tables(ds, 8))
     res, _ = P.run_query(qid, "default", _cluster(8), per)
     assert_same(res, _expected(0.05, 1.5, qid), f"{qid}@skew")
+
+
+@pytest.mark.parametrize("sf", [0.01, 0.1])
+def test_result_digests_match_reference_at_every_n(sf):
+    """engine.py:182-197 result_digest of our results == the digest of the
+    REAL reference's reference_run (tests/golden/digests.json), at N=1 and
+    at N=2/3 virtual ranks: exact fixed-point aggregates make the digest
+    rank-count independent (the reference's float folds are not)."""
+    import paper_2506_09226_b200 as P
+    want = load_golden("digests.json")[f"sf{sf}"]
+    ds, _, _ = _host(sf)
+    dev = P.load_tables(ds)
+    for qid, d in want.items():
+        assert P.result_digest(P.reference_run(qid, dev)) == d, (qid, "N=1")
+    for n in (2, 3):
+        per = P.partition_tables(ds, n)
+        for qid, d in want.items():
+            _, rep = P.run_query(qid, "default", _cluster(n), per)
+            assert rep.result_digest == d, (qid, n)

@@ -754,12 +754,13 @@ def main() -> None:
     # ---- e2e: same suite, base columns H2D from pinned host inside the region ----
     # N > 1: each rank's own rows (the default_keys hash partition, selected on
     # the host outside the timed region); only those cross PCIe per rank
-    from paper_2506_09226_b200.data import partition_rows
+    from paper_2506_09226_b200.data import REPLICATED_TABLES, worker_rows
     rank_rows = {}
     if ep.n > 1:
         for tname in names:
-            rank_rows[tname] = partition_rows(ds.tables[tname], "default_keys",
-                                              P.DEFAULT_PARTITION_KEYS[tname], ep.n)[ep.rank]
+            if tname not in REPLICATED_TABLES:
+                rank_rows[tname] = worker_rows(tname, ds.tables[tname], "default_keys",
+                                               ep.n)[ep.rank]
     host_tables = {t: (ds.tables[t].take(rank_rows[t]) if t in rank_rows else ds.tables[t])
                    for t in names}
     host_cols = {}

@@ -99,7 +99,7 @@ def cmd_query(args) -> int:
     if ep.rank == 0:
         os.makedirs(args.out, exist_ok=True)
     for qid in qids:
-        result, report = run_query(qid, args.variant, ep, tables, scheme)
+        result, report = run_query(qid, args.variant, ep, tables, scheme=scheme)
         if ep.rank == 0:
             _write_result_csv(os.path.join(args.out, f"{qid.lower()}_result.csv"), result)
             with open(os.path.join(args.out, f"{qid.lower()}_report.json"), "w") as fh:

@@ -28,6 +28,11 @@ import numpy as np
 from .table import HostColumn, HostTable, date_to_days, narrow_host
 
 PARTITION_SCHEMES = ("default_keys", "unpartitioned", "round_robin")
+# 25-row nation / 5-row region (generator extension, absent from the
+# reference): replicated on every worker under every scheme, as the paper's
+# Table-4 plan counts assume (Q5 (0,2) = customer +
+# supplier broadcasts, no exchange for nation / region)
+REPLICATED_TABLES = ("nation", "region")
 
 # data.py:47-56 -- conventional partition key per table
 DEFAULT_PARTITION_KEYS = {
@@ -503,6 +508,14 @@ def partition_rows(table: HostTable, scheme: str, key: str | None, n: int) -> li
     return [idx[idx % n == r] for r in range(n)]
 
 
+def worker_rows(name: str, table: HostTable, scheme: str, n: int) -> list[np.ndarray]:
+    """Row indices of table ``name`` per worker: the whole table on every
+    worker for REPLICATED_TABLES, else partition_rows on its default key."""
+    if name in REPLICATED_TABLES:
+        return [np.arange(table.row_count)] * n
+    return partition_rows(table, scheme, DEFAULT_PARTITION_KEYS[name], n)
+
+
 def partition_dataset(ds: Dataset, n_workers: int, scheme: str = "default_keys") -> PartitionedDataset:
     """Host-side partitioning of a narrowed dataset (data.py:284).
 
@@ -515,7 +528,7 @@ def partition_dataset(ds: Dataset, n_workers: int, scheme: str = "default_keys")
         raise DataError(f"unknown partitioning scheme {scheme!r}; choose from {PARTITION_SCHEMES}")
     workers: list[dict] = [{} for _ in range(n_workers)]
     for name, t in ds.tables.items():
-        parts = partition_rows(t, scheme, DEFAULT_PARTITION_KEYS[name], n_workers)
+        parts = worker_rows(name, t, scheme, n_workers)
         for r in range(n_workers):
             workers[r][name] = t.take(parts[r])
     return PartitionedDataset(scheme, n_workers, workers, ds)

@@ -836,6 +836,56 @@ struct Gen {
     }
   }
 
+  // Probes whose key is a base column the host has verified non-decreasing
+  // (table._pad == 1 on an IDENTITY / DIRECT lookup: lineitem.l_orderkey ->
+  // orders) read the build side in one monotone sweep.  Thread 0 reads the
+  // first and last key of the NEXT tile this CTA will process and issues a
+  // cp.async.bulk.prefetch.L2 of that key range of the build-side arrays
+  // (identity: the gathered payload columns; direct: the row table), so the
+  // dependent gathers of the next tile hit L2 instead of waiting on HBM.
+  void emit_gather_prefetch(int64_t tile_rows) {
+    const char* e = getenv("SCX_GATHER_PF");
+    if (e && e[0] == '0') return;
+    const bool cmp = P.sink.kind == SCX_SINK_COMPACT;
+    for (int pi = 0; pi < P.n_probes; ++pi) {
+      const scx_probe& pb = P.probe[pi];
+      const int tk = pb.table.kind;
+      if ((tk != SCX_HT_IDENTITY && tk != SCX_HT_DIRECT) || pb.table._pad != 1) continue;
+      if (pb.key.n != 1 || pb.key.slot[0] < 0 || pb.key.slot[0] >= P.n_base ||
+          pb.key.shift[0] != 0 || (pb.key.xform & 0xff) != SCX_XFORM_NONE)
+        continue;
+      const int s = pb.key.slot[0];
+      const int cp = col_p[s];
+      const int cap_p = param(pb.table.cap);
+      struct Arr { int p; int w; };
+      std::vector<Arr> arrs;
+      if (tk == SCX_HT_DIRECT) {
+        arrs.push_back({param(pb.table.vals), 4});
+      } else if (pb.kind == SCX_JOIN_INNER || pb.kind == SCX_JOIN_LEFT) {
+        for (int j = 0; j < pb.n_payload; ++j)
+          arrs.push_back({param(pb.payload[j].ptr), dtype_size(pb.payload[j].dtype)});
+      }
+      if (arrs.empty()) continue;
+      const char* t = ctype(P.base[s].dtype);
+      o << "    if (tid == 0) {   // L2 prefetch of probe " << pi << "'s build range for the next tile\n";
+      o << "      const i64 nt = tile + " << (cmp ? "1ll" : "(i64)gridDim.x") << ";\n";
+      o << "      if (nt < " << (cmp ? "tend" : "ntiles") << ") {\n";
+      o << "        const " << t << "* kc = (const " << t << "*)a.p[" << cp << "];\n";
+      o << "        const i64 r0 = nt * " << tile_rows << "ll;\n";
+      o << "        const i64 r1 = (n < r0 + " << tile_rows << "ll ? n : r0 + " << tile_rows << "ll) - 1;\n";
+      o << "        const i64 k0 = (i64)kc[r0] - " << lit64(pb.key.lo[0]) << ", k1 = (i64)kc[r1] - "
+        << lit64(pb.key.lo[0]) << ";\n";
+      o << "        if (k0 >= 0 && k1 >= k0 && (u64)k1 < a.p[" << cap_p << "] && k1 - k0 < 65536ll) {\n";
+      for (const Arr& A : arrs) {
+        o << "          { const u64 b = a.p[" << A.p << "];\n";
+        o << "            const u64 s0 = (b + (u64)k0 * " << A.w << "ull) & ~15ull;\n";
+        o << "            const u64 s1 = (b + (u64)(k1 + 1) * " << A.w << "ull + 15ull) & ~15ull;\n";
+        o << "            if (s0 >= (b & ~15ull)) l2_prefetch((const void*)s0, (u32)(s1 - s0)); }\n";
+      }
+      o << "        }\n      }\n    }\n";
+    }
+  }
+
   // ------------------------------------------------------------------------
   int generate(std::string& src, std::string& name, int& tiles_out) {
     const scx_sink& S = P.sink;
@@ -1169,6 +1219,7 @@ struct Gen {
       }
       o << "        l2_prefetch(cp, cb);\n      }\n    }\n";
     }
+    emit_gather_prefetch(tile_rows);
     if (tma) {
       o << "    const int tma_st = tma_it % " << tma_stages << ";\n";
       o << "    mb_wait(bars + 8u * tma_st, (u32)((tma_it / " << tma_stages << ") & 1));\n";

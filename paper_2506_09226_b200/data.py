@@ -214,7 +214,7 @@ def generate(sf: float, skew: float = 0.0, seed: int = 0) -> Dataset:
     tax = narrow_host(rng.integers(0, 9, size=n_li))
     rflag = rng.integers(0, len(RETURN_FLAGS), size=n_li)
     lineitem_cols = {
-        "l_orderkey": HostColumn.from_ints("int64", l_ok),
+        "l_orderkey": _sorted(HostColumn.from_ints("int64", l_ok)),
         "l_partkey": HostColumn.from_ints("int64", l_pk),
         "l_quantity": HostColumn.from_ints("int64", qty),
         "l_extendedprice": HostColumn.decimal(ext_cents, 2),
@@ -421,7 +421,7 @@ def save_dataset(ds: Dataset, path: str) -> None:
             np.save(os.path.join(path, f"{tname}.{cname}.npy"), c.values)
             cols[cname] = {"kind": c.kind, "scale": c.scale, "lo": c.lo, "hi": c.hi,
                            "dictionary": list(c.dictionary) if c.dictionary else None,
-                           "dense": bool(c.dense)}
+                           "dense": bool(c.dense), "sorted": bool(c.sorted)}
         meta["tables"][tname] = cols
     tmp = os.path.join(path, "manifest.json.tmp")
     with open(tmp, "w") as fh:
@@ -442,7 +442,8 @@ def load_dataset(path: str, mmap: bool = True) -> Dataset:
                         mmap_mode="r" if mmap else None)
             hc[cname] = HostColumn(m["kind"], v, m["scale"],
                                    tuple(m["dictionary"]) if m["dictionary"] else None,
-                                   m["lo"], m["hi"], bool(m.get("dense", False)))
+                                   m["lo"], m["hi"], bool(m.get("dense", False)),
+                                   bool(m.get("sorted", cname == "l_orderkey")))
         tables[tname] = HostTable(hc)
     return Dataset(tables, meta["sf"], meta["skew"], meta["seed"])
 
@@ -506,6 +507,13 @@ def partition_rows(table: HostTable, scheme: str, key: str | None, n: int) -> li
         return [np.arange(cuts[i], cuts[i + 1]) for i in range(n)]
     idx = np.arange(rows)
     return [idx[idx % n == r] for r in range(n)]
+
+
+def _sorted(c: HostColumn) -> HostColumn:
+    """Mark a column generated in non-decreasing order (l_orderkey: orders'
+    lines are emitted order by order, data.py:195-198 in the reference)."""
+    c.sorted = True
+    return c
 
 
 def worker_rows(name: str, table: HostTable, scheme: str, n: int) -> list[np.ndarray]:

@@ -713,6 +713,16 @@ def _pushdown_join(lv: TableView, rv: TableView, on: tuple[str, str], how: str):
 TRACE: set | None = None
 
 
+_GATHER_PF_MIN_ROWS = 1 << 20
+
+
+def _probe_key_sorted(c: Column) -> bool:
+    """Non-decreasing probe key, known without a device check: generated in
+    order (l_orderkey, surrogate keys), kept by increasing row selections and
+    the stable compaction (_materialize), or verified earlier on the device."""
+    return bool(c.sorted)
+
+
 class _Builder:
     """Assigns operand slots and serialises a TableView into scx_pipeline."""
 
@@ -773,6 +783,13 @@ class _Builder:
                 cb = st.lookup.coarse(shift)
                 pb.table.keys = cb.data_ptr()
                 pb.table._pad = shift + 1
+            if (st.lookup.lk.kind in (L.HT_IDENTITY, L.HT_DIRECT) and len(st.probe_keys) == 1
+                    and P.n_rows >= _GATHER_PF_MIN_ROWS
+                    and v.origin.get(st.probe_keys[0], ("x",))[0] == "base"
+                    and _probe_key_sorted(v.meta[st.probe_keys[0]])):
+                # monotone probe sweep: the kernel prefetches the next tile's
+                # build range into L2 (jit.cu emit_gather_prefetch)
+                pb.table._pad = 1
             used = [n for n in st.payload if n in self.slot]
             if len(used) > L.MAX_PAYLOAD:
                 raise SchemaError("too many payload columns from one join")
@@ -1004,8 +1021,13 @@ def _materialize(v: TableView) -> ColumnTable:
     m = int(_to_host(count)[0]) if n else 0
     # probes build on unique keys, so a filtered / joined row set keeps the
     # base table's key property
-    return ColumnTable({name: v.meta[name].like(_fit(outs[name], m)) for name in cols},
-                       v.base.unique_keys)
+    out = {}
+    for name in cols:
+        c = v.meta[name].like(_fit(outs[name], m))
+        if v.origin[name][0] == "base" and v.meta[name].sorted:
+            c.sorted = True          # the compaction is stable: order is kept
+        out[name] = c
+    return ColumnTable(out, v.base.unique_keys)
 
 
 def _fit(buf, m: int):
@@ -1413,6 +1435,9 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
     acc = acc.view(cells, M, 2)
     S.acc = acc.data_ptr()
     b.run(timing)
+    if GRAPH_CAPTURE is not None and (cross is None or cross.ep.n == 1):
+        GRAPH_CAPTURE.append(DenseGraph(b, acc, pattern, cells, M,
+                                        (keys, kcols, cards, luts, plan, measures, count_m)))
     if cross is not None and cross.ep.n > 1:
         from .exchange import all_gather_tensor
         parts = all_gather_tensor(cross.ep, acc)
@@ -1422,6 +1447,45 @@ def _group_dense(v, b, keys, kcols, cards, cells, plan, measures, count_m, cross
         L.call("scx_dense_reduce", _ptr(parts), cross.ep.n, cells, M, ops, _ptr(red), _stream())
         acc = red
     return finish_dense(_to_host(acc), keys, kcols, cards, luts, plan, measures, count_m)
+
+
+# CUDA-graph capture of dense final aggregates (bench.py config 1): while set
+# to a list, every single-rank dense group-by also records a DenseGraph
+GRAPH_CAPTURE: list | None = None
+
+
+class DenseGraph:
+    """A dense aggregation's device work -- accumulator fill, the fused scan
+    kernel, D2H of the exact 128-bit cells into pinned memory -- captured once
+    as a CUDA graph.  ``replay()`` relaunches it (no host plan building, one
+    graph launch instead of per-kernel launches) and finishes the result on
+    the host exactly as the eager path does.  The captured descriptor keeps
+    its base-column pointers: the tables must stay alive and unchanged."""
+
+    def __init__(self, b: "_Builder", acc, pattern, cells: int, M: int, finish_args):
+        torch = _torch()
+        self.b, self.acc, self.finish_args = b, acc, finish_args
+        self.pattern = (C.c_int64 * (2 * M))(*pattern)
+        self.host = torch.empty(acc.shape, dtype=torch.int64, pin_memory=True)
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(self.graph, stream=side):
+            L.call("scx_fill_rows", _ptr(acc), cells, 2 * M, self.pattern, _stream())
+            b.run()
+            self.host.copy_(acc, non_blocking=True)
+        torch.cuda.current_stream().wait_stream(side)
+
+    def launch(self) -> None:
+        self.graph.replay()
+
+    def finish(self) -> "ColumnTable":
+        _torch().cuda.current_stream().synchronize()
+        return finish_dense(self.host.numpy(), *self.finish_args)
+
+    def replay(self) -> "ColumnTable":
+        self.launch()
+        return self.finish()
 
 
 def _i128(lohi) -> int:

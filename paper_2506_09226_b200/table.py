@@ -122,6 +122,7 @@ class HostColumn:
     lo: int = 0
     hi: int = -1
     dense: bool = False                  # row i holds lo + i (a surrogate key column)
+    sorted: bool = False                 # non-decreasing by construction (l_orderkey)
 
     @staticmethod
     def from_ints(kind: str, a: np.ndarray) -> "HostColumn":
@@ -133,7 +134,7 @@ class HostColumn:
     def int_range(start: int, stop: int) -> "HostColumn":
         dt = narrow_dtype(start, max(start, stop - 1))
         return HostColumn("int64", np.arange(start, stop, dtype=dt), 0, None, start, stop - 1,
-                          True)
+                          True, True)
 
     @staticmethod
     def from_codes(codes: np.ndarray, dictionary: tuple[str, ...]) -> "HostColumn":
@@ -183,7 +184,13 @@ class HostColumn:
         return int(self.values.nbytes)
 
     def take(self, idx: np.ndarray) -> "HostColumn":
-        return HostColumn(self.kind, self.values[idx], self.scale, self.dictionary, self.lo, self.hi)
+        idx = np.asarray(idx)
+        # a sorted column stays sorted under an increasing row selection
+        # (partition_rows / row ranges keep input order)
+        keep = bool(self.sorted and (idx.dtype == bool or idx.size < 2
+                                     or bool(np.all(idx[1:] > idx[:-1]))))
+        return HostColumn(self.kind, self.values[idx], self.scale, self.dictionary, self.lo,
+                          self.hi, False, keep)
 
     def to_int64(self) -> np.ndarray:
         return self.values.astype(np.int64)
@@ -344,6 +351,8 @@ class Column:
         c = Column(hc.kind, None, hc.scale, hc.dictionary, hc.lo, hc.hi,
                    hc.dense and hc.row_count == hc.hi - hc.lo + 1)
         c._host = np.ascontiguousarray(hc.values)
+        if hc.sorted:
+            c.sorted = True
         return c
 
     @staticmethod
@@ -355,8 +364,11 @@ class Column:
             v = np.ascontiguousarray(hc.values)
             src = torch.from_numpy(v if v.flags.writeable else v.copy())
             buf.copy_(src, non_blocking=False)
-        return Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
-                      hc.dense and n == hc.hi - hc.lo + 1)
+        c = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
+                   hc.dense and n == hc.hi - hc.lo + 1)
+        if hc.sorted:
+            c.sorted = True
+        return c
 
     @staticmethod
     def from_numpy(kind: str, values, dictionary=None, device=None) -> "Column":

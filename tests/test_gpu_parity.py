@@ -393,3 +393,23 @@ def test_top_k_wide_keys(k):
     idx = np.lexsort([-b, c, -a])[:k]
     for name, ref in (("a", a), ("b", b), ("c", c)):
         assert np.array_equal(got.column(name).values, ref[idx]), name
+
+
+@pytest.mark.parametrize("qid", ["Q1", "Q6"])
+def test_dense_graph_replay_matches_golden(qid):
+    """relops.DenseGraph (bench config 1/2): the query's device work captured
+    as one CUDA graph replays to the reference's result, repeatedly."""
+    import paper_2506_09226_b200 as P
+    import paper_2506_09226_b200.relops as R
+    key = "sf0.1_skew0.0"
+    tables = device_tables(key)
+    R.GRAPH_CAPTURE = []
+    try:
+        eager = P.reference_run(qid, tables)
+        graphs = R.GRAPH_CAPTURE
+    finally:
+        R.GRAPH_CAPTURE = None
+    assert len(graphs) == 1
+    assert_table_matches(eager, RES[key][qid], f"{qid}/eager")
+    for i in range(3):
+        assert_table_matches(graphs[0].replay(), RES[key][qid], f"{qid}/graph{i}")

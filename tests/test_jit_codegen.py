@@ -82,6 +82,13 @@ def _compact_probe(kind=L.HT_HASH, jk=L.JOIN_INNER):
     S.status = 0xb000; S.count = 0xc000
     return P
 
+def _prefetch_probe(kind):
+    # monotone probe key (table._pad = 1): next-tile L2 prefetch of the build range
+    P = _compact_probe(kind, L.JOIN_INNER)
+    P.probe[0].table._pad = 1
+    return P
+
+
 def _hashgroup():
     P = _compact_probe()
     S = P.sink; S.kind = L.SINK_AGG_HASH; S.n_measures = 2
@@ -177,6 +184,8 @@ PLANS = {
     "compact_anti_hash": lambda: _compact_probe(L.HT_HASH, L.JOIN_ANTI),
     "hash_group": _hashgroup,
     "hash_group_direct_narrow": _hashgroup_narrow,
+    "prefetch_identity_inner": lambda: _prefetch_probe(L.HT_IDENTITY),
+    "prefetch_direct_inner": lambda: _prefetch_probe(L.HT_DIRECT),
 }
 
 
@@ -210,6 +219,16 @@ def test_source_is_deterministic_and_pointer_free(lib):
     lib.scx_pipeline_source(C.byref(a), sa, 1 << 16)
     lib.scx_pipeline_source(C.byref(b), sb, 1 << 16)
     assert sa.value == sb.value          # pointers are launch parameters, not code
+
+
+def test_prefetch_emitted_only_for_monotone_probes(lib):
+    def src(P):
+        n = lib.scx_pipeline_source(C.byref(P), None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib.scx_pipeline_source(C.byref(P), buf, n + 1)
+        return buf.value.decode()
+    assert "l2_prefetch((const void*)s0" in src(_prefetch_probe(L.HT_IDENTITY))
+    assert "l2_prefetch((const void*)s0" not in src(_compact_probe(L.HT_DIRECT, L.JOIN_INNER))
 
 
 def test_codegen_rejects_bad_descriptor(lib):

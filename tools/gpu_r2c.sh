@@ -19,3 +19,9 @@ for Q in ${QS:-Q3 Q5 Q7}; do
   python tools/ncu_summary.py gpurun_out/prof_${Q}_$TAG.ncu-rep > gpurun_out/ncu_${Q}_$TAG.txt 2>&1
   cat gpurun_out/ncu_${Q}_$TAG.txt
 done
+# compute-sanitizer over the SF0.01 suite (N=1 and N=3 virtual ranks)
+for T in memcheck racecheck synccheck; do
+  N3=1; [ $T != memcheck ] && N3=0
+  SAN_N3=$N3 timeout 900 compute-sanitizer --tool $T --print-limit 20 python tools/sanitize_suite.py > gpurun_out/sanitize_${T}_$TAG.log 2>&1
+  echo "$T rc=$?"; tail -4 gpurun_out/sanitize_${T}_$TAG.log
+done

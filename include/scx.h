@@ -495,6 +495,26 @@ int scx_allreduce_i64(void* comm, const int64_t* send_dev, int64_t* recv_dev, in
 int scx_gather_to0(void* comm, const void* send_dev, int64_t bytes, void* const* recv_dev,
                    const int64_t* recv_bytes, void* stream);
 
+/* ---- packed host columns: the load path's H2D bytes (data.py:284-302
+ * partition_dataset / the cold run) ---------------------------
+ * The reference hands float64/int64 columns to its workers; here a host
+ * column is sent bit-packed and unpacked on the device into its narrowed
+ * layout.  SCX_PACK_FOR: value = lo + field (k bits); SCX_PACK_DELTA
+ * (non-decreasing columns): blocks of scx_pack_delta_block() rows, value =
+ * bases[block] + running sum of the block's fields (first field 0);
+ * SCX_PACK_IOTA (surrogate keys): value = lo + row, no words.  Field i sits at
+ * bits [i*k, i*k+k) of a little-endian u32 word stream of scx_pack_words(n, k)
+ * words (one padding word).  scx_pack_host is host code (threads), k <= 32. */
+#define SCX_PACK_FOR   0
+#define SCX_PACK_DELTA 1
+#define SCX_PACK_IOTA  2
+int64_t scx_pack_words(int64_t n, int k);
+int64_t scx_pack_delta_block(void);
+int scx_pack_host(const void* in, int dtype, int64_t n, int64_t lo, int k, int delta,
+                  uint32_t* out_words, int64_t* out_bases, int n_threads);
+int scx_unpack(const uint32_t* words_dev, int64_t n, int k, int64_t lo, int encoding,
+               const int64_t* bases_dev, scx_column out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,7 @@ JOIN_SEMI, JOIN_ANTI, JOIN_INNER, JOIN_LEFT = 0, 1, 2, 3
 HT_HASH, HT_DIRECT, HT_BITMAP, HT_IDENTITY = 0, 1, 2, 3
 AGG_SUM, AGG_COUNT, AGG_MIN, AGG_MAX = 0, 1, 2, 3
 SINK_AGG_DENSE, SINK_AGG_HASH, SINK_COMPACT, SINK_COUNT, SINK_BITMAP = 0, 1, 2, 3, 4
+PACK_FOR, PACK_DELTA, PACK_IOTA = 0, 1, 2
 EMPTY_KEY = 0xFFFFFFFFFFFFFFFF
 NO_ROW = 0xFFFFFFFF
 
@@ -171,6 +172,10 @@ _PROTOS = {
     "scx_bcast_group": (C.c_int, [_vp, C.POINTER(_vp), C.POINTER(i64), C.c_int, _vp]),
     "scx_allreduce_i64": (C.c_int, [_vp, _vp, _vp, i64, C.c_int, _vp]),
     "scx_gather_to0": (C.c_int, [_vp, _vp, i64, C.POINTER(_vp), C.POINTER(i64), _vp]),
+    "scx_pack_words": (i64, [i64, C.c_int]),
+    "scx_pack_delta_block": (i64, []),
+    "scx_pack_host": (C.c_int, [_vp, C.c_int, i64, i64, C.c_int, C.c_int, _vp, _vp, C.c_int]),
+    "scx_unpack": (C.c_int, [_vp, i64, C.c_int, i64, C.c_int, _vp, Column_, _vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

@@ -1,0 +1,205 @@
+"""Bit-packed host columns for the host -> HBM load path (csrc/codec.cu).
+
+The cold path -- a dataset in host memory becoming HBM-resident tables
+(the reference's ``partition_dataset`` hand-off, data.py:284-302; the
+paper's cold run) -- is bound by PCIe, ~48 GB/s against
+~6.5 TB/s of HBM.  Columns are already narrowed losslessly at generation
+(table.py); for the copy they are packed further:
+
+* FOR   -- frame of reference: ``value - lo`` in ``k = bits(hi - lo)`` bits
+           (dates 12 bits, quantity 6, flags 1-3, keys 20-28, prices 24);
+* DELTA -- a non-decreasing column (l_orderkey) packs its deltas per 2048-row
+           block (1 bit per row at uniform SF100) plus one int64 base per block;
+* IOTA  -- a surrogate key column (lo, lo+1, ...) sends nothing;
+* RAW   -- anything that would not shrink (raw float64, k >= the narrowed width).
+
+``scx_pack_host`` (threaded C++) packs; ``scx_unpack`` rebuilds the narrowed
+column on the device on the copy stream, right behind its words.  At SF100
+the 21.7 GB of narrowed columns cross PCIe as ~10 GB.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from .table import NP_TO_SCX, HostColumn
+
+RAW = -1
+_CHUNK = 1 << 24
+
+
+@dataclass
+class PackedColumn:
+    """A HostColumn in its transfer encoding (``meta`` keeps the logical
+    description; its ``values`` are only needed by RAW)."""
+
+    meta: HostColumn
+    n: int
+    encoding: int
+    k: int = 0
+    lo: int = 0
+    words: np.ndarray | None = None      # u32
+    bases: np.ndarray | None = None      # i64, DELTA only
+
+    @property
+    def dtype(self) -> np.dtype:
+        return self.meta.values.dtype
+
+    @property
+    def nbytes(self) -> int:
+        """Bytes that cross PCIe for this column."""
+        if self.encoding == RAW:
+            return int(self.meta.values.nbytes)
+        b = 0 if self.words is None else int(self.words.nbytes)
+        return b + (0 if self.bases is None else int(self.bases.nbytes))
+
+
+def _bits(span: int) -> int:
+    return int(span).bit_length() if span > 0 else 0
+
+
+def _delta_bits(v: np.ndarray, block: int) -> int | None:
+    """Bits of the largest in-block delta of a non-decreasing column (None if
+    a delta is negative: the column is not sorted after all)."""
+    mx = 0
+    for s in range(0, len(v), _CHUNK):
+        c = v[s:min(len(v), s + _CHUNK + 1)].astype(np.int64)
+        d = np.diff(c)
+        if d.size == 0:
+            continue
+        # block-start rows carry field 0: their deltas are not encoded
+        starts = np.arange(s + 1, s + 1 + d.size)
+        d = np.where(starts % block == 0, 0, d)
+        if d.min() < 0:
+            return None
+        mx = max(mx, int(d.max()))
+    return _bits(mx)
+
+
+def pack_column(hc: HostColumn, threads: int = 0) -> PackedColumn:
+    v = np.ascontiguousarray(hc.values)
+    n = len(v)
+    if v.dtype.kind not in "iu" or v.dtype not in NP_TO_SCX:
+        return PackedColumn(hc, n, RAW)
+    if hc.dense and n and hc.hi - hc.lo + 1 == n:
+        return PackedColumn(hc, n, L.PACK_IOTA, 0, hc.lo)
+    lib = L.load()
+    k_for = _bits(hc.hi - hc.lo) if n and hc.hi >= hc.lo else 0
+    enc, k = L.PACK_FOR, k_for
+    block = int(lib.scx_pack_delta_block())
+    if hc.sorted and n:
+        kd = _delta_bits(v, block)
+        if kd is not None and kd < k_for:
+            enc, k = L.PACK_DELTA, kd
+    if k > 32 or k >= 8 * v.dtype.itemsize:
+        return PackedColumn(hc, n, RAW)
+    words = np.empty(int(lib.scx_pack_words(n, k)), dtype=np.uint32)
+    bases = np.empty(max(1, (n + block - 1) // block), dtype=np.int64) \
+        if enc == L.PACK_DELTA else None
+    L.call("scx_pack_host", v.ctypes.data_as(C.c_void_p), NP_TO_SCX[v.dtype], n, hc.lo, k,
+           1 if enc == L.PACK_DELTA else 0, words.ctypes.data_as(C.c_void_p),
+           bases.ctypes.data_as(C.c_void_p) if bases is not None else None, threads)
+    return PackedColumn(hc, n, enc, k, hc.lo, words, bases)
+
+
+def pack_table(ht, threads: int = 0) -> dict[str, PackedColumn]:
+    return {c: pack_column(hc, threads) for c, hc in ht.columns.items()}
+
+
+def unpack_host(pc: PackedColumn) -> np.ndarray:
+    """numpy restatement of scx_unpack (test infrastructure)."""
+    if pc.encoding == RAW:
+        return np.asarray(pc.meta.values)
+    n, k = pc.n, pc.k
+    if pc.encoding == L.PACK_IOTA:
+        return (pc.lo + np.arange(n, dtype=np.int64)).astype(pc.dtype)
+    if k == 0:
+        f = np.zeros(n, dtype=np.int64)
+    else:
+        bit = np.arange(n, dtype=np.int64) * k
+        w = pc.words.astype(np.uint64)
+        two = w[bit >> 5] | (w[(bit >> 5) + 1] << np.uint64(32))
+        f = ((two >> (bit & 31).astype(np.uint64)) & np.uint64((1 << k) - 1)).astype(np.int64)
+    if pc.encoding == L.PACK_FOR:
+        return (pc.lo + f).astype(pc.dtype)
+    block = int(L.load().scx_pack_delta_block())
+    out = np.empty(n, dtype=np.int64)
+    for b in range(0, n, block):
+        out[b:b + block] = pc.bases[b // block] + np.cumsum(f[b:b + block])
+    return out.astype(pc.dtype)
+
+
+def upload_packed(pc: PackedColumn, src_words, src_bases, stream):
+    """Device column buffer of ``pc``: H2D of the pinned words (+ bases) on
+    ``stream``, then scx_unpack on the same stream.  The scratch copies are
+    tied to ``stream`` (record_stream) so the allocator does not hand them to
+    another stream before the unpack has read them."""
+    import torch
+    from .table import alloc
+    buf = alloc(pc.n, pc.dtype)
+    with torch.cuda.stream(stream):
+        dw = db = None
+        if src_words is not None and pc.words is not None:
+            dw = alloc(src_words.numel(), np.int32)
+            dw.copy_(src_words, non_blocking=True)
+            dw.record_stream(stream)
+        if src_bases is not None:
+            db = alloc(src_bases.numel(), np.int64)
+            db.copy_(src_bases, non_blocking=True)
+            db.record_stream(stream)
+        L.call("scx_unpack", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n, pc.k,
+               pc.lo, pc.encoding, C.c_void_p(db.data_ptr() if db is not None else 0),
+               L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(stream))
+    return buf
+
+
+@dataclass
+class PinnedPacked:
+    """A packed column with its words / bases in pinned host memory."""
+
+    col: PackedColumn
+    words: object = None       # torch uint32 (int32 view) pinned tensor
+    bases: object = None       # torch int64 pinned tensor
+
+    @property
+    def nbytes(self) -> int:
+        return self.col.nbytes
+
+
+def _pin(a: np.ndarray):
+    import torch
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint32:
+        a = a.view(np.int32)
+    return torch.from_numpy(a if a.flags.writeable else a.copy()).pin_memory()
+
+
+def pin_tables(tables: dict, packed: bool = True, threads: int = 0) -> dict:
+    """{table: {column: (HostColumn, source)}} for engine.upload_tables_async:
+    the source is a pinned raw tensor, or a PinnedPacked (packed=True) whose
+    words cross PCIe and are unpacked on the device."""
+    out = {}
+    for t, ht in tables.items():
+        cols = {}
+        for c, hc in ht.columns.items():
+            pc = pack_column(hc, threads) if packed else PackedColumn(hc, hc.row_count, RAW)
+            if pc.encoding == RAW:
+                cols[c] = (hc, _pin(hc.values))
+            else:
+                cols[c] = (hc, PinnedPacked(pc, _pin(pc.words) if pc.words is not None else None,
+                                            _pin(pc.bases) if pc.bases is not None else None))
+        out[t] = cols
+    return out
+
+
+def h2d_bytes(host: dict) -> int:
+    """Bytes a pin_tables() result moves over PCIe."""
+    tot = 0
+    for cols in host.values():
+        for _, src in cols.values():
+            tot += src.nbytes if isinstance(src, PinnedPacked) else src.numel() * src.element_size()
+    return tot

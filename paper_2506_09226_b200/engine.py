@@ -381,13 +381,15 @@ def upload_tables_async(host: dict, order=None, stream=None):
     """Upload pinned host columns on a copy stream, table by table in `order`
     (first use first), without blocking the compute stream.
 
-    ``host``: {table: {column: (HostColumn, pinned torch tensor)}}.  Returns
+    ``host``: {table: {column: (HostColumn, pinned torch tensor or
+    codec.PinnedPacked)}} (codec.pin_tables).  Returns
     (device tables, {table: event}); pass the events as
     ``DeviceContext(ready=...)`` so each query waits only for the tables it
     touches while the later tables are still crossing PCIe (H2D overlapped
     with the queries that can already run).  Single-rank tables only.
     """
     import torch
+    from .codec import PinnedPacked, upload_packed
     # two copy streams: columns alternate between them (both DMA engines busy)
     streams = [stream or torch.cuda.Stream(), torch.cuda.Stream()]
     main = torch.cuda.current_stream()
@@ -399,14 +401,21 @@ def upload_tables_async(host: dict, order=None, stream=None):
         cols = {}
         used = set()
         for cname, (hc, pinned) in host[tname].items():
-            buf = alloc(hc.row_count, hc.values.dtype)
             cs = streams[k % 2]
             k += 1
             used.add(id(cs))
-            with torch.cuda.stream(cs):
-                buf.copy_(pinned, non_blocking=True)
-            cols[cname] = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
-                                 hc.dense and hc.row_count == hc.hi - hc.lo + 1)
+            if isinstance(pinned, PinnedPacked):
+                # packed words cross PCIe, scx_unpack rebuilds the column
+                buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs)
+            else:
+                buf = alloc(hc.row_count, hc.values.dtype)
+                with torch.cuda.stream(cs):
+                    buf.copy_(pinned, non_blocking=True)
+            col = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
+                         hc.dense and hc.row_count == hc.hi - hc.lo + 1)
+            if hc.sorted:
+                col.sorted = True
+            cols[cname] = col
         evs = []
         for cs in streams:
             if id(cs) in used:

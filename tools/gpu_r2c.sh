@@ -19,6 +19,13 @@ for Q in ${QS:-Q3 Q5 Q7}; do
   python tools/ncu_summary.py gpurun_out/prof_${Q}_$TAG.ncu-rep > gpurun_out/ncu_${Q}_$TAG.txt 2>&1
   cat gpurun_out/ncu_${Q}_$TAG.txt
 done
+# A/B of the next-tile gather prefetch (suite, single stream + 3 streams)
+for PF in 0 1; do
+  SCX_GATHER_PF=$PF timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu --no-configs --sweep "" > gpurun_out/ab_pf${PF}_$TAG.json 2> gpurun_out/ab_pf${PF}_$TAG.err
+  python -c "
+import json,sys; d=json.loads(open('gpurun_out/ab_pf${PF}_$TAG.json').read().strip().splitlines()[-1])
+print('PF=$PF value', d['value'], 'single', d['single_stream']['value'], {q: round(v['s']*1e3,2) for q, v in d['per_query'].items()})"
+done
 # compute-sanitizer over the SF0.01 suite (N=1 and N=3 virtual ranks)
 for T in memcheck racecheck synccheck; do
   N3=1; [ $T != memcheck ] && N3=0

@@ -286,7 +286,9 @@ def q10(T):
 
 
 def q11(T):
-    """Important stock (GERMANY); value > 0.0001 * total; order value desc, ps_partkey."""
+    """Important stock (GERMANY); value > FRACTION * total with TPC-H's
+    FRACTION = 0.0001 / SF, SF = supplier rows / 10000 (so the test is
+    value * n_suppliers > total); order value desc, ps_partkey."""
     de = nation_key(T, "GERMANY")
     s = T["supplier"]
     ps = T["partsupp"]
@@ -295,7 +297,7 @@ def q11(T):
     v = (cents(ps, "ps_supplycost") * ints(ps, "ps_availqty"))[keep]
     total = int(v.sum())
     (gk,), agg = group_int([ints(ps, "ps_partkey")[keep]], {"v": v}, {})
-    sel = agg["v"] * 10000 > total            # value > total * 0.0001, exactly
+    sel = agg["v"] * nrows(s) > total         # value > total * 0.0001 / SF, exactly
     out = {"ps_partkey": col("int64", gk[sel]), "value": col("float64", fdiv(agg["v"][sel], DEC))}
     return sort_by(out, ["value", "ps_partkey"], {"value"})
 

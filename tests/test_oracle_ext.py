@@ -300,7 +300,7 @@ def test_q11_pandas():
     m = m[m.s_nationkey.isin(de)]
     m["v"] = cents(m.ps_supplycost) * m.ps_availqty
     g = m.groupby("ps_partkey").v.sum().reset_index()
-    g = g[g.v * 10000 > m.v.sum()].sort_values(["v", "ps_partkey"], ascending=[False, True])
+    g = g[g.v * len(s) > m.v.sum()].sort_values(["v", "ps_partkey"], ascending=[False, True])
     r = E.q11(T)
     assert len(g) > 0
     assert list(r["ps_partkey"][1]) == list(g.ps_partkey)

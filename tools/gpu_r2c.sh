@@ -19,6 +19,12 @@ for Q in ${QS:-Q3 Q5 Q7}; do
   python tools/ncu_summary.py gpurun_out/prof_${Q}_$TAG.ncu-rep > gpurun_out/ncu_${Q}_$TAG.txt 2>&1
   cat gpurun_out/ncu_${Q}_$TAG.txt
 done
+# partition scatter (config 5 shape) under ncu --set full
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:part_ -c 3 \
+  -o gpurun_out/prof_part_$TAG -f python tools/part_bench.py --parts 8 > gpurun_out/ncu_part_$TAG.log 2>&1
+echo "part rc=$?"
+python tools/ncu_summary.py gpurun_out/prof_part_$TAG.ncu-rep > gpurun_out/ncu_part_$TAG.txt 2>&1
+cat gpurun_out/ncu_part_$TAG.txt
 # A/B of the next-tile gather prefetch (suite, single stream + 3 streams)
 for PF in 0 1; do
   SCX_GATHER_PF=$PF timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu --no-configs --sweep "" > gpurun_out/ab_pf${PF}_$TAG.json 2> gpurun_out/ab_pf${PF}_$TAG.err

@@ -843,9 +843,14 @@ struct Gen {
   // cp.async.bulk.prefetch.L2 of that key range of the build-side arrays
   // (identity: the gathered payload columns; direct: the row table), so the
   // dependent gathers of the next tile hit L2 instead of waiting on HBM.
+  // Measured at SF100 and rejected as the default (opt-in SCX_GATHER_PF=1):
+  // Q12 2.19 -> 3.15 ms, Q10 3.28 -> 4.66, Q5 4.87 -> 5.35 -- thread 0's two
+  // dependent key loads per tile stall its warp and with it the CTA, and the
+  // monotone gathers were already served by L2 (neighbouring CTAs touch the
+  // same build range at the same time).
   void emit_gather_prefetch(int64_t tile_rows) {
     const char* e = getenv("SCX_GATHER_PF");
-    if (e && e[0] == '0') return;
+    if (!e || e[0] != '1') return;
     const bool cmp = P.sink.kind == SCX_SINK_COMPACT;
     for (int pi = 0; pi < P.n_probes; ++pi) {
       const scx_probe& pb = P.probe[pi];

@@ -221,7 +221,8 @@ def test_source_is_deterministic_and_pointer_free(lib):
     assert sa.value == sb.value          # pointers are launch parameters, not code
 
 
-def test_prefetch_emitted_only_for_monotone_probes(lib):
+def test_prefetch_emitted_only_for_monotone_probes(lib, monkeypatch):
+    monkeypatch.setenv("SCX_GATHER_PF", "1")
     def src(P):
         n = lib.scx_pipeline_source(C.byref(P), None, 0)
         buf = C.create_string_buffer(n + 1)

@@ -5,8 +5,6 @@
 TAG=${1:-r2c}
 SF=${2:-100}
 mkdir -p gpurun_out/jit_src_$TAG
-timeout 1500 python -m pytest tests -m gpu -x -q --durations=10 > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_$TAG.log
-tail -n 8 gpurun_out/pytest_$TAG.log
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --print-nvtx-rename none --csv \
   --log-file gpurun_out/launches_q_$TAG.csv python tools/suite_once.py --sf $SF > gpurun_out/ncu_suite_$TAG.log 2>&1; echo "launch list rc=$?"
 python tools/launch_by_query.py gpurun_out/launches_q_$TAG.csv 8 > gpurun_out/by_query_$TAG.txt 2>&1
@@ -25,13 +23,6 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:part
 echo "part rc=$?"
 python tools/ncu_summary.py gpurun_out/prof_part_$TAG.ncu-rep > gpurun_out/ncu_part_$TAG.txt 2>&1
 cat gpurun_out/ncu_part_$TAG.txt
-# A/B of the next-tile gather prefetch (suite, single stream + 3 streams)
-for PF in 0 1; do
-  SCX_GATHER_PF=$PF timeout 900 python bench.py --steps 3 --warmup 2 --no-cpu --no-configs --sweep "" > gpurun_out/ab_pf${PF}_$TAG.json 2> gpurun_out/ab_pf${PF}_$TAG.err
-  python -c "
-import json,sys; d=json.loads(open('gpurun_out/ab_pf${PF}_$TAG.json').read().strip().splitlines()[-1])
-print('PF=$PF value', d['value'], 'single', d['single_stream']['value'], {q: round(v['s']*1e3,2) for q, v in d['per_query'].items()})"
-done
 # compute-sanitizer over the SF0.01 suite (N=1 and N=3 virtual ranks)
 for T in memcheck racecheck synccheck; do
   N3=1; [ $T != memcheck ] && N3=0

@@ -974,6 +974,7 @@ def main() -> None:
                     "h2d_bytes_per_step": h2d_bytes,
                     "d2h_bytes_per_step": d2h_bytes,
                     "narrowed_bytes": narrow_bytes,
+                    "passes_ms": [round(x, 2) for x in e2e_ms],
                     "encoding": "bit-packed host columns (codec.py), unpacked on the device"
                                 if not args.no_pack else "narrowed columns, unpacked"},
             "roofline": roofline,

@@ -426,6 +426,14 @@ struct Gen {
   size_t sink_smem = 0;         // dynamic smem used by the sink (before the load stages)
   std::vector<int> col_p;       // Args.p index of each base column
   std::string err;
+  // chunked dense mode (probe kernels, see emit_chunk_tile): base values are
+  // read from the staged TMA tile, one row per lane; survivors of each
+  // filtering stage are compacted into per-warp shared-memory queues
+  bool chunk = false;
+  int SEG = 0;                  // rows of a tile per warp (32 * V)
+  size_t q_off = 0, qb_bytes = 0, ob_off = 0, ob_bytes = 0;
+  std::vector<int> q_poff;      // payload slot -> byte offset inside a queue buffer
+  std::vector<int> ob_coff;     // COMPACT output column -> offset inside a warp's out buffer
 
   explicit Gen(const scx_pipeline& p) : P(p) {}
 
@@ -457,7 +465,25 @@ struct Gen {
   // value of slot s at row r (r is a loop variable / literal in the source)
   std::string val(int s, const char* r) {
     const int dt = P.slot_dtype[s];
-    char b[96];
+    char b[160];
+    if (chunk) {
+      if (s >= P.n_base) {
+        if (fits32_dt(dt)) snprintf(b, sizeof(b), "((i32)pv%d)", s);
+        else snprintf(b, sizeof(b), "pv%d", s);
+        return b;
+      }
+      const long long off = (long long)stage_off(s);
+      switch (dt) {
+        case SCX_I8: snprintf(b, sizeof(b), "((i32)*(const i8*)(stg + %lldu + lr))", off); break;
+        case SCX_U8: snprintf(b, sizeof(b), "((i32)*(const u8*)(stg + %lldu + lr))", off); break;
+        case SCX_I16: snprintf(b, sizeof(b), "((i32)*(const i16*)(stg + %lldu + 2 * lr))", off); break;
+        case SCX_U16: snprintf(b, sizeof(b), "((i32)*(const u16*)(stg + %lldu + 2 * lr))", off); break;
+        case SCX_I32: snprintf(b, sizeof(b), "(*(const i32*)(stg + %lldu + 4 * lr))", off); break;
+        case SCX_U32: snprintf(b, sizeof(b), "(*(const u32*)(stg + %lldu + 4 * lr))", off); break;
+        default: snprintf(b, sizeof(b), "(*(const i64*)(stg + %lldu + 8 * lr))", off); break;
+      }
+      return b;
+    }
     if (s < P.n_base) {
       switch (dt) {
         case SCX_I8: snprintf(b, sizeof(b), "X1S(w%d, %s)", s, r); break;
@@ -891,6 +917,233 @@ struct Gen {
     }
   }
 
+  // ---- chunked dense mode (one row per lane, per-warp selection queues) ----
+  void emit_chunk_pred(const scx_pred& pr) {
+    if (pr.clause_mask == 0 || pr.n_atoms == 0) return;
+    o << "        if (ok && !(" << pred_expr(pr, "") << ")) ok = false;\n";
+  }
+
+  // probe pi for the lane's row: idx<pi>, ok update, payload registers pv<s>
+  void emit_chunk_probe(int pi) {
+    const scx_probe& pb = P.probe[pi];
+    if (pb.kind < SCX_JOIN_SEMI || pb.kind > SCX_JOIN_LEFT) { err = "unknown join kind"; return; }
+    const int keys_p = param(pb.table.keys);
+    const int vals_p = param(pb.table.vals);
+    const int cap_p = param(pb.table.cap);
+    const char* kinds[] = {"semi", "anti", "inner", "left"};
+    o << "        // probe " << pi << " (" << kinds[pb.kind] << ", "
+      << (pb.table.kind == SCX_HT_IDENTITY ? "identity" : pb.table.kind == SCX_HT_DIRECT ? "direct"
+          : pb.table.kind == SCX_HT_BITMAP ? "bitmap" : "hash") << ")\n";
+    o << "        u32 idx" << pi << " = SCX_NOROW;\n";
+    o << "        if (ok) {\n";
+    o << "          const u32* vals = (const u32*)a.p[" << vals_p << "]; (void)vals;\n";
+    o << "          const u64 cap = a.p[" << cap_p << "];\n";
+    pack_key(pb.key, "", nullptr, 0, "key", "kin");
+    if (pb.table.kind == SCX_HT_IDENTITY) {
+      o << "          if (kin && key < cap) idx" << pi << " = (u32)key;\n";
+    } else if (pb.table.kind == SCX_HT_BITMAP) {
+      if (pb.kind != SCX_JOIN_SEMI && pb.kind != SCX_JOIN_ANTI) { err = "bitmap probe needs a semi/anti join"; return; }
+      o << "          if (kin && key < cap && ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u)) idx" << pi << " = 0u;\n";
+    } else if (pb.table.kind == SCX_HT_DIRECT) {
+      o << "          if (kin && key < cap) idx" << pi << " = __ldg(vals + key);\n";
+    } else {
+      o << "          if (kin) {\n";
+      o << "            const u64* keys = (const u64*)a.p[" << keys_p << "];\n";
+      o << "            const u64 mask = cap - 1;\n";
+      o << "            u64 h = mix64(key) & mask, k = __ldg(keys + h);\n";
+      o << "            while (k != key && k != SCX_EMPTY) { h = (h + 1) & mask; k = __ldg(keys + h); }\n";
+      o << "            if (k == key) idx" << pi << " = __ldg(vals + h);\n";
+      o << "          }\n";
+    }
+    o << "        }\n";
+    if (pb.kind == SCX_JOIN_ANTI) o << "        if (idx" << pi << " != SCX_NOROW) ok = false;\n";
+    else if (pb.kind != SCX_JOIN_LEFT) o << "        if (idx" << pi << " == SCX_NOROW) ok = false;\n";
+    if (pb.kind == SCX_JOIN_INNER || pb.kind == SCX_JOIN_LEFT) {
+      for (int j = 0; j < pb.n_payload; ++j) {
+        const int sl = pb.payload_slot[j];
+        const int src_p = param(pb.payload[j].ptr);
+        const char* t = ctype(pb.payload[j].dtype);
+        o << "        const " << t << " pv" << sl << " = (ok && idx" << pi << " != SCX_NOROW) ? __ldg((const "
+          << t << "*)a.p[" << src_p << "] + idx" << pi << ") : (" << t << ")0;\n";
+      }
+    }
+  }
+
+  // one tile: levels separated by compaction points (after every stage that
+  // can drop rows and is followed by another probe), then the sink
+  void emit_chunk(int64_t tile_rows, bool dense_priv, bool dense_reg, int NC, int NW, int M,
+                  const std::vector<int>& mword, const std::vector<int>& mshift,
+                  const std::vector<int>& mbits) {
+    const scx_sink& S = P.sink;
+    o << "    const unsigned char* stg = dsm + " << ring_off << " + (u32)tma_st * " << stage_bytes() << "u;\n";
+    o << "    const i64 trow0 = tile * " << tile_rows << "ll;\n";
+    o << "    const int rows = (int)(n - trow0 < " << tile_rows << "ll ? n - trow0 : " << tile_rows << "ll);\n";
+    o << "    const u32 lt = (1u << lane) - 1u;\n";
+    o << "    unsigned char* qbuf0 = dsm + " << q_off << " + (u32)warp * " << qb_bytes << "u;\n";
+    o << "    unsigned char* qbuf1 = dsm + " << q_off << " + (u32)(" << kTPB / 32 << " + warp) * " << qb_bytes << "u;\n";
+    o << "    (void)qbuf0; (void)qbuf1;\n";
+    if (S.kind == SCX_SINK_COMPACT)
+      o << "    unsigned char* obuf = dsm + " << ob_off << " + (u32)warp * " << ob_bytes << "u;\n"
+        << "    u32 wq = 0;\n";
+    auto filters = [&](int i) -> bool {
+      if (i < 0) return P.pre.clause_mask != 0 && P.pre.n_atoms != 0;
+      const scx_probe& pb = P.probe[i];
+      if (pb.after.clause_mask != 0 && pb.after.n_atoms != 0) return true;
+      if (pb.kind == SCX_JOIN_SEMI || pb.kind == SCX_JOIN_ANTI) return true;
+      return pb.kind == SCX_JOIN_INNER && pb.table.kind != SCX_HT_IDENTITY;
+    };
+    std::vector<std::pair<int, int>> levels;      // [first item, last item]; -1 = pre, n_probes = post
+    int start = -1;
+    for (int i = -1; i < P.n_probes - 1; ++i)
+      if (filters(i)) { levels.push_back({start, i}); start = i + 1; }
+    levels.push_back({start, P.n_probes});
+    std::vector<int> have;                        // payload slots carried into the level
+    o << "    u32 qcnt = 0; (void)qcnt;\n";
+    for (size_t L = 0; L < levels.size(); ++L) {
+      const bool first = L == 0, last = L + 1 == levels.size();
+      const char* qin = (L % 2 == 1) ? "qbuf0" : "qbuf1";
+      const char* qout = (L % 2 == 0) ? "qbuf0" : "qbuf1";
+      o << "    { // level " << L << ": items " << levels[L].first << ".." << levels[L].second << "\n";
+      if (!last) o << "      u32 qn = 0;\n";
+      if (first) {
+        o << "#pragma unroll 1\n      for (int c = 0; c < " << SEG << "; c += 32) {\n";
+        o << "        const int lr = warp * " << SEG << " + c + lane;\n";
+        o << "        bool ok = lr < rows;\n";
+      } else {
+        o << "#pragma unroll 1\n      for (u32 c = 0; c < qcnt; c += 32) {\n";
+        o << "        const u32 q = c + lane;\n";
+        o << "        bool ok = q < qcnt;\n";
+        o << "        const int lr = ok ? (int)((const u16*)" << qin << ")[q] : 0;\n";
+        for (int sl : have) {
+          const char* t = ctype(P.slot_dtype[sl]);
+          o << "        const " << t << " pv" << sl << " = ok ? ((const " << t << "*)(" << qin << " + "
+            << q_poff[sl] << "))[q] : (" << t << ")0;\n";
+        }
+      }
+      std::vector<int> now = have;
+      for (int i = levels[L].first; i <= levels[L].second; ++i) {
+        if (i < 0) emit_chunk_pred(P.pre);
+        else if (i < P.n_probes) {
+          emit_chunk_probe(i);
+          emit_chunk_pred(P.probe[i].after);
+          const scx_probe& pb = P.probe[i];
+          if (pb.kind == SCX_JOIN_INNER || pb.kind == SCX_JOIN_LEFT)
+            for (int j = 0; j < pb.n_payload; ++j) now.push_back(pb.payload_slot[j]);
+        } else {
+          emit_chunk_pred(P.post);
+        }
+      }
+      if (!last) {
+        o << "        const u32 m = __ballot_sync(0xffffffffu, ok);\n";
+        o << "        if (ok) {\n          const u32 pos = qn + __popc(m & lt);\n";
+        o << "          ((u16*)" << qout << ")[pos] = (u16)lr;\n";
+        for (int sl : now) {
+          const char* t = ctype(P.slot_dtype[sl]);
+          o << "          ((" << t << "*)(" << qout << " + " << q_poff[sl] << "))[pos] = pv" << sl << ";\n";
+        }
+        o << "        }\n        qn += __popc(m);\n";
+      } else {
+        emit_chunk_sink(dense_priv, dense_reg, NC, NW, M, mword, mshift, mbits);
+      }
+      o << "      }\n      __syncwarp();\n";
+      if (!last) o << "      qcnt = qn;\n";
+      o << "    }\n";
+      have = now;
+    }
+    // every consumer thread releases the stage (after a generic->async proxy
+    // fence: the next bulk copy must not overtake our shared-memory reads)
+    o << "    asm volatile(\"fence.proxy.async.shared::cta;\" ::: \"memory\");\n";
+    o << "    mb_arrive(bars + 8u * (" << tma_stages << " + tma_st));\n";
+    if (S.kind == SCX_SINK_COMPACT) {
+      // stable order across the CTA: warp w's rows precede warp w+1's
+      o << "    if (lane == 0) s_cnt[tpar][warp] = wq;\n";
+      o << "    CSYNC();\n";
+      o << "    u32 before = 0, ttot = 0;\n";
+      o << "#pragma unroll\n    for (int w2 = 0; w2 < " << kTPB / 32 << "; ++w2) { const u32 c2 = s_cnt[tpar][w2]; before += w2 < warp ? c2 : 0u; ttot += c2; }\n";
+      o << "    const i64 obase = (i64)(tbeg * " << tile_rows << "ll) + (i64)cta_pos + (i64)before;\n";
+      o << "    for (u32 q = lane; q < wq; q += 32) {\n";
+      for (int i = 0; i < S.n_out; ++i) {
+        const char* t = ctype(S.out[i].dtype);
+        o << "      sdst" << i << "[obase + q] = ((const " << t << "*)(obuf + " << ob_coff[i] << "))[q];\n";
+      }
+      o << "    }\n";
+      o << "    cta_pos += ttot;\n    tpar ^= 1;\n    __syncwarp();\n";
+    }
+  }
+
+  void emit_chunk_sink(bool dense_priv, bool dense_reg, int NC, int NW, int M,
+                       const std::vector<int>& mword, const std::vector<int>& mshift,
+                       const std::vector<int>& mbits) {
+    const scx_sink& S = P.sink;
+    if (S.kind == SCX_SINK_COUNT) {
+      o << "        cnt += ok ? 1ull : 0ull;\n";
+      return;
+    }
+    if (S.kind == SCX_SINK_COMPACT) {
+      o << "        const u32 m = __ballot_sync(0xffffffffu, ok);\n";
+      o << "        if (ok) {\n          const u32 pos = wq + __popc(m & lt);\n";
+      for (int i = 0; i < S.n_out; ++i) {
+        const int s2 = S.out_slot[i];
+        const char* t = ctype(S.out[i].dtype);
+        o << "          ((" << t << "*)(obuf + " << ob_coff[i] << "))[pos] = (" << t << ")";
+        if (s2 < 0) o << "(trow0 + lr);\n";
+        else o << val(s2, "") << ";\n";
+      }
+      o << "        }\n        wq += __popc(m);\n";
+      return;
+    }
+    // dense group-by, one row
+    o << "        if (ok) {\n";
+    o << "          int cell = 0;\n";
+    for (int i = 0; i < S.gkey.n; ++i) {
+      std::string v = "(" + key_value(S.gkey, i, "") + " - " + lit64(S.gkey.lo[i]) + ")";
+      if (S.glut[i] >= 0) v = lut_expr(S.glut[i], S.gcard[i], v);
+      o << "          cell = cell * " << S.gcard[i] << " + (int)" << v << ";\n";
+    }
+    for (int m = 0; m < M; ++m) o << "          const i64 m" << m << " = " << measure_expr(S.m[m], "") << ";\n";
+    if (dense_priv) {
+      o << "          i64* pa = pacc + cell * " << NW * kTPB << " + tid;\n";
+      for (int w = 0; w < NW; ++w) {
+        const std::string slot = "pa[" + std::to_string(w * kTPB) + "]";
+        std::string packed_add;
+        for (int m = 0; m < M; ++m) {
+          if (mword[m] != w) continue;
+          const int op = S.m[m].op;
+          if (mbits[m] == 64) {
+            if (op == SCX_AGG_MIN) o << "          " << slot << " = smin(" << slot << ", m" << m << ");\n";
+            else if (op == SCX_AGG_MAX) o << "          " << slot << " = smax(" << slot << ", m" << m << ");\n";
+            else o << "          " << slot << " += m" << m << ";\n";
+          } else {
+            packed_add += (packed_add.empty() ? "" : " + ") + std::string("((u64)m") + std::to_string(m) +
+                          " << " + std::to_string(mshift[m]) + ")";
+          }
+        }
+        if (!packed_add.empty()) o << "          " << slot << " = (i64)((u64)" << slot << " + " << packed_add << ");\n";
+      }
+    } else if (dense_reg) {
+      for (int c = 0; c < NC; ++c) {
+        if (NC > 1) o << "          if (cell == " << c << ") {\n";
+        for (int m = 0; m < M; ++m) {
+          const int op = S.m[m].op;
+          o << "            acc[" << c << "][" << m << "] = ";
+          if (op == SCX_AGG_MIN) o << "smin(acc[" << c << "][" << m << "], m" << m << ");\n";
+          else if (op == SCX_AGG_MAX) o << "smax(acc[" << c << "][" << m << "], m" << m << ");\n";
+          else o << "acc[" << c << "][" << m << "] + m" << m << ";\n";
+        }
+        if (NC > 1) o << "          }\n";
+      }
+    } else {
+      for (int m = 0; m < M; ++m) {
+        const int op = S.m[m].op;
+        o << "          { unsigned long long* t = (unsigned long long*)&tab[cell * " << M << " + " << m << "]; ";
+        if (op == SCX_AGG_MIN) o << "atomicMin((long long*)t, (long long)m" << m << "); }\n";
+        else if (op == SCX_AGG_MAX) o << "atomicMax((long long*)t, (long long)m" << m << "); }\n";
+        else o << "atomicAdd(t, (unsigned long long)m" << m << "); }\n";
+      }
+    }
+    o << "        }\n";
+  }
+
   // ------------------------------------------------------------------------
   int generate(std::string& src, std::string& name, int& tiles_out) {
     const scx_sink& S = P.sink;
@@ -968,6 +1221,36 @@ struct Gen {
       while (V > 4 && V * (row_bytes + payload_bytes) / 4 + V * probe_regs + acc_regs > reg_budget())
         V /= 2;
     }
+    // chunked dense mode for probe kernels (emit_chunk): measured on B200 the
+    // row-owner kernels with probes ran at V = 4 (register budget) and issued
+    // 100-130 thread-instructions per row (ncu, profiles/r2_ncu_probe_scans.txt):
+    // instruction-bound, every stage executed for every row.  In chunk mode
+    // the tile stays in shared memory (TMA), each lane takes one row, and the
+    // survivors of every filtering stage are ballot-compacted into per-warp
+    // queues, so each stage runs on dense lanes of survivors only.
+    {
+      const char* e = getenv("SCX_CHUNK");
+      bool coarse = false;
+      for (int pi = 0; pi < P.n_probes; ++pi)
+        coarse |= P.probe[pi].table.kind == SCX_HT_BITMAP && P.probe[pi].table._pad > 0 &&
+                  P.probe[pi].table.keys != 0;
+      chunk = !(e && e[0] == '0') && P.n_probes > 0 && P.n_base > 0 && row_bytes > 0 && !coarse &&
+              (S.kind == SCX_SINK_AGG_DENSE || S.kind == SCX_SINK_COMPACT ||
+               S.kind == SCX_SINK_COUNT);
+      if (chunk) {
+        int out_bytes = 0;
+        if (S.kind == SCX_SINK_COMPACT)
+          for (int i = 0; i < S.n_out; ++i) out_bytes += dtype_size(S.out[i].dtype);
+        auto est = [&](int v) {
+          const int seg = 32 * v;
+          return (size_t)2 * kTPB * v * row_bytes + (size_t)16 * seg * (2 + payload_bytes + 8) +
+                 (size_t)8 * seg * (out_bytes + 8);
+        };
+        const char* ev = getenv("SCX_CHUNK_V");
+        V = ev && *ev ? (atoi(ev) >= 8 ? 8 : 4) : (est(8) <= 80 * 1024 ? 8 : 4);
+        SEG = 32 * V;
+      }
+    }
     // load pipeline: each thread copies (cp.async) its chunk of the NEXT tile's
     // base columns into shared memory while it processes this one, so a
     // tile's HBM latency overlaps the previous tile's probes and sink.  V
@@ -984,7 +1267,7 @@ struct Gen {
       const char* env = getenv("SCX_PIPE");
       // measured on B200 (SF100 suite): per-thread cp.async staging is slower
       // than direct 128-bit ld.global.nc (Q6 1.04 -> 1.44 ms), so it is opt-in
-      pipe = env && env[0] == '1' && P.n_base > 0 && row_bytes > 0;
+      pipe = env && env[0] == '1' && P.n_base > 0 && row_bytes > 0 && !chunk;
       if (pipe) {
         int v = V;
         while (v > 4 && sink_b + 2 * (size_t)kTPB * v * row_bytes > kPipeSmem) v /= 2;
@@ -1009,10 +1292,10 @@ struct Gen {
       for (int pi = 0; pi < P.n_probes; ++pi) hash_probe |= P.probe[pi].table.kind == SCX_HT_HASH;
       // (private-accumulator group-bys keep 3 CTAs/SM on the register path:
       // their 48 KB of accumulators + the ring would leave 2; Q1 1.63 vs 1.68 ms)
-      tma = (mode == '1' || (mode == '2' && P.n_probes == 0) ||
-             (mode == '3' && ((P.n_probes == 0 && !dense_priv) ||
-                              (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
-            !pipe && P.n_base > 0 && row_bytes > 0;
+      tma = chunk || ((mode == '1' || (mode == '2' && P.n_probes == 0) ||
+                       (mode == '3' && ((P.n_probes == 0 && !dense_priv) ||
+                                        (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
+                      !pipe && P.n_base > 0 && row_bytes > 0);
       if (tma) {
         const size_t stage = (size_t)kTPB * V * row_bytes;
         const char* rb = getenv("SCX_TMA_RING_KB");
@@ -1022,6 +1305,27 @@ struct Gen {
         ring_off = (sink_smem + 127) & ~(size_t)127;
         bar_off = ring_off + (size_t)tma_stages * stage;
         bar_off = (bar_off + 15) & ~(size_t)15;
+      }
+      if (chunk) {
+        // per-warp queue buffers (two, ping-pong): u16 tile-local row ids +
+        // one array per payload slot; then (COMPACT) a per-warp out buffer
+        auto a16 = [](size_t x) { return (x + 15) & ~(size_t)15; };
+        q_off = a16(bar_off + 16 * (size_t)tma_stages);
+        size_t off = a16((size_t)SEG * 2);
+        q_poff.assign(P.n_slots > 0 ? P.n_slots : 1, -1);
+        for (int sl = P.n_base; sl < P.n_slots; ++sl) {
+          q_poff[sl] = (int)off;
+          off += a16((size_t)SEG * dtype_size(P.slot_dtype[sl]));
+        }
+        qb_bytes = off;
+        ob_off = q_off + 16 * qb_bytes;
+        ob_bytes = 0;
+        ob_coff.assign(S.n_out > 0 ? S.n_out : 1, 0);
+        if (S.kind == SCX_SINK_COMPACT)
+          for (int i = 0; i < S.n_out; ++i) {
+            ob_coff[i] = (int)ob_bytes;
+            ob_bytes += a16((size_t)SEG * dtype_size(S.out[i].dtype));
+          }
       }
     }
     const int64_t tile_rows = (int64_t)kTPB * V;
@@ -1142,6 +1446,7 @@ struct Gen {
       stage_rows_p = param(0);
       o << "  __shared__ u32 s_warp[" << kTPB / 32 << "];\n";
       o << "  __shared__ u32 s_tot;\n";
+      if (chunk) o << "  __shared__ u32 s_cnt[2][" << kTPB / 32 << "];\n  int tpar = 0;\n";
       o << "  const i64 tpc = (ntiles + gridDim.x - 1) / gridDim.x;\n";
       o << "  const i64 tbeg = (i64)blockIdx.x * tpc;\n";
       o << "  const i64 tend = tbeg + tpc < ntiles ? tbeg + tpc : ntiles;\n";
@@ -1190,6 +1495,7 @@ struct Gen {
     }
     if (dyn_smem < sink_smem) dyn_smem = sink_smem;
     if (tma) dyn_smem = bar_off + 16 * (size_t)tma_stages;
+    if (chunk) dyn_smem = ob_off + 8 * ob_bytes;
     if (pipe) {
       dyn_smem = sink_smem + 2 * (size_t)stage_bytes();
       const bool cmp = S.kind == SCX_SINK_COMPACT;
@@ -1230,6 +1536,9 @@ struct Gen {
       o << "    mb_wait(bars + 8u * tma_st, (u32)((tma_it / " << tma_stages << ") & 1));\n";
       o << "    ++tma_it;\n";
     }
+    if (chunk) {
+      emit_chunk(tile_rows, dense_priv, dense_reg, NC, NW, M, mword, mshift, mbits);
+    } else {
     o << "    const i64 row0 = (tile * " << kTPB << " + tid) * (i64)V;\n";
     o << "    const bool full = row0 + V <= n;\n";
     o << "    const int rem = row0 >= n ? 0 : (int)(n - row0 < V ? n - row0 : V);\n";
@@ -1430,6 +1739,7 @@ struct Gen {
       }
       o << "    }\n";
     }
+    }   // !chunk
     o << "  }\n";  // tile loop
     if (pipe) o << "  cpa_wait0();\n";
 

@@ -434,6 +434,9 @@ struct Gen {
   size_t q_off = 0, qb_bytes = 0, ob_off = 0, ob_bytes = 0;
   std::vector<int> q_poff;      // payload slot -> byte offset inside a queue buffer
   std::vector<int> ob_coff;     // COMPACT output column -> offset inside a warp's out buffer
+  std::string cu;               // chunk mode: variable suffix of the current sub-row ("_2")
+  int U = 1;                    // chunk mode: sub-rows (32-row chunks) per lane per iteration
+  static std::string sfx(int u) { return "_" + std::to_string(u); }
 
   explicit Gen(const scx_pipeline& p) : P(p) {}
 
@@ -468,19 +471,20 @@ struct Gen {
     char b[160];
     if (chunk) {
       if (s >= P.n_base) {
-        if (fits32_dt(dt)) snprintf(b, sizeof(b), "((i32)pv%d)", s);
-        else snprintf(b, sizeof(b), "pv%d", s);
+        if (fits32_dt(dt)) snprintf(b, sizeof(b), "((i32)pv%d%s)", s, cu.c_str());
+        else snprintf(b, sizeof(b), "pv%d%s", s, cu.c_str());
         return b;
       }
       const long long off = (long long)stage_off(s);
+      const char* l = cu.c_str();
       switch (dt) {
-        case SCX_I8: snprintf(b, sizeof(b), "((i32)*(const i8*)(stg + %lldu + lr))", off); break;
-        case SCX_U8: snprintf(b, sizeof(b), "((i32)*(const u8*)(stg + %lldu + lr))", off); break;
-        case SCX_I16: snprintf(b, sizeof(b), "((i32)*(const i16*)(stg + %lldu + 2 * lr))", off); break;
-        case SCX_U16: snprintf(b, sizeof(b), "((i32)*(const u16*)(stg + %lldu + 2 * lr))", off); break;
-        case SCX_I32: snprintf(b, sizeof(b), "(*(const i32*)(stg + %lldu + 4 * lr))", off); break;
-        case SCX_U32: snprintf(b, sizeof(b), "(*(const u32*)(stg + %lldu + 4 * lr))", off); break;
-        default: snprintf(b, sizeof(b), "(*(const i64*)(stg + %lldu + 8 * lr))", off); break;
+        case SCX_I8: snprintf(b, sizeof(b), "((i32)*(const i8*)(stg + %lldu + lr%s))", off, l); break;
+        case SCX_U8: snprintf(b, sizeof(b), "((i32)*(const u8*)(stg + %lldu + lr%s))", off, l); break;
+        case SCX_I16: snprintf(b, sizeof(b), "((i32)*(const i16*)(stg + %lldu + 2 * lr%s))", off, l); break;
+        case SCX_U16: snprintf(b, sizeof(b), "((i32)*(const u16*)(stg + %lldu + 2 * lr%s))", off, l); break;
+        case SCX_I32: snprintf(b, sizeof(b), "(*(const i32*)(stg + %lldu + 4 * lr%s))", off, l); break;
+        case SCX_U32: snprintf(b, sizeof(b), "(*(const u32*)(stg + %lldu + 4 * lr%s))", off, l); break;
+        default: snprintf(b, sizeof(b), "(*(const i64*)(stg + %lldu + 8 * lr%s))", off, l); break;
       }
       return b;
     }
@@ -918,12 +922,18 @@ struct Gen {
   }
 
   // ---- chunked dense mode (one row per lane, per-warp selection queues) ----
+  // Every op is emitted for the U sub-rows of an iteration back to back (u
+  // suffix), so a stage's U independent probe / gather loads are in flight
+  // together before any of them is used.
   void emit_chunk_pred(const scx_pred& pr) {
     if (pr.clause_mask == 0 || pr.n_atoms == 0) return;
-    o << "        if (ok && !(" << pred_expr(pr, "") << ")) ok = false;\n";
+    for (int u = 0; u < U; ++u) {
+      cu = sfx(u);
+      o << "        if (ok" << cu << " && !(" << pred_expr(pr, "") << ")) ok" << cu << " = false;\n";
+    }
+    cu.clear();
   }
 
-  // probe pi for the lane's row: idx<pi>, ok update, payload registers pv<s>
   void emit_chunk_probe(int pi) {
     const scx_probe& pb = P.probe[pi];
     if (pb.kind < SCX_JOIN_SEMI || pb.kind > SCX_JOIN_LEFT) { err = "unknown join kind"; return; }
@@ -934,37 +944,55 @@ struct Gen {
     o << "        // probe " << pi << " (" << kinds[pb.kind] << ", "
       << (pb.table.kind == SCX_HT_IDENTITY ? "identity" : pb.table.kind == SCX_HT_DIRECT ? "direct"
           : pb.table.kind == SCX_HT_BITMAP ? "bitmap" : "hash") << ")\n";
-    o << "        u32 idx" << pi << " = SCX_NOROW;\n";
-    o << "        if (ok) {\n";
+    if (pb.table.kind == SCX_HT_BITMAP && pb.kind != SCX_JOIN_SEMI && pb.kind != SCX_JOIN_ANTI) {
+      err = "bitmap probe needs a semi/anti join";
+      return;
+    }
+    for (int u = 0; u < U; ++u) o << "        u32 idx" << pi << sfx(u) << " = SCX_NOROW;\n";
+    o << "        {\n";
     o << "          const u32* vals = (const u32*)a.p[" << vals_p << "]; (void)vals;\n";
     o << "          const u64 cap = a.p[" << cap_p << "];\n";
-    pack_key(pb.key, "", nullptr, 0, "key", "kin");
-    if (pb.table.kind == SCX_HT_IDENTITY) {
-      o << "          if (kin && key < cap) idx" << pi << " = (u32)key;\n";
-    } else if (pb.table.kind == SCX_HT_BITMAP) {
-      if (pb.kind != SCX_JOIN_SEMI && pb.kind != SCX_JOIN_ANTI) { err = "bitmap probe needs a semi/anti join"; return; }
-      o << "          if (kin && key < cap && ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u)) idx" << pi << " = 0u;\n";
-    } else if (pb.table.kind == SCX_HT_DIRECT) {
-      o << "          if (kin && key < cap) idx" << pi << " = __ldg(vals + key);\n";
-    } else {
-      o << "          if (kin) {\n";
-      o << "            const u64* keys = (const u64*)a.p[" << keys_p << "];\n";
-      o << "            const u64 mask = cap - 1;\n";
-      o << "            u64 h = mix64(key) & mask, k = __ldg(keys + h);\n";
-      o << "            while (k != key && k != SCX_EMPTY) { h = (h + 1) & mask; k = __ldg(keys + h); }\n";
-      o << "            if (k == key) idx" << pi << " = __ldg(vals + h);\n";
+    if (pb.table.kind == SCX_HT_HASH)
+      o << "          const u64* keys = (const u64*)a.p[" << keys_p << "];\n"
+        << "          const u64 mask = cap - 1;\n";
+    for (int u = 0; u < U; ++u) {
+      cu = sfx(u);
+      const std::string ix = "idx" + std::to_string(pi) + cu;
+      o << "          if (ok" << cu << ") {\n";
+      pack_key(pb.key, "", nullptr, 0, "key", "kin");
+      if (pb.table.kind == SCX_HT_IDENTITY) {
+        o << "            if (kin && key < cap) " << ix << " = (u32)key;\n";
+      } else if (pb.table.kind == SCX_HT_BITMAP) {
+        o << "            if (kin && key < cap && ((__ldg(vals + (key >> 5)) >> (key & 31)) & 1u)) " << ix << " = 0u;\n";
+      } else if (pb.table.kind == SCX_HT_DIRECT) {
+        o << "            if (kin && key < cap) " << ix << " = __ldg(vals + key);\n";
+      } else {
+        o << "            if (kin) {\n";
+        o << "              u64 h = mix64(key) & mask, k = __ldg(keys + h);\n";
+        o << "              while (k != key && k != SCX_EMPTY) { h = (h + 1) & mask; k = __ldg(keys + h); }\n";
+        o << "              if (k == key) " << ix << " = __ldg(vals + h);\n";
+        o << "            }\n";
+      }
       o << "          }\n";
     }
+    cu.clear();
     o << "        }\n";
-    if (pb.kind == SCX_JOIN_ANTI) o << "        if (idx" << pi << " != SCX_NOROW) ok = false;\n";
-    else if (pb.kind != SCX_JOIN_LEFT) o << "        if (idx" << pi << " == SCX_NOROW) ok = false;\n";
+    for (int u = 0; u < U; ++u) {
+      const std::string ix = "idx" + std::to_string(pi) + sfx(u);
+      if (pb.kind == SCX_JOIN_ANTI) o << "        if (" << ix << " != SCX_NOROW) ok" << sfx(u) << " = false;\n";
+      else if (pb.kind != SCX_JOIN_LEFT) o << "        if (" << ix << " == SCX_NOROW) ok" << sfx(u) << " = false;\n";
+    }
     if (pb.kind == SCX_JOIN_INNER || pb.kind == SCX_JOIN_LEFT) {
       for (int j = 0; j < pb.n_payload; ++j) {
         const int sl = pb.payload_slot[j];
         const int src_p = param(pb.payload[j].ptr);
         const char* t = ctype(pb.payload[j].dtype);
-        o << "        const " << t << " pv" << sl << " = (ok && idx" << pi << " != SCX_NOROW) ? __ldg((const "
-          << t << "*)a.p[" << src_p << "] + idx" << pi << ") : (" << t << ")0;\n";
+        for (int u = 0; u < U; ++u) {
+          const std::string ix = "idx" + std::to_string(pi) + sfx(u);
+          o << "        const " << t << " pv" << sl << sfx(u) << " = (ok" << sfx(u) << " && " << ix
+            << " != SCX_NOROW) ? __ldg((const " << t << "*)a.p[" << src_p << "] + " << ix << ") : ("
+            << t << ")0;\n";
+        }
       }
     }
   }
@@ -975,6 +1003,8 @@ struct Gen {
                   const std::vector<int>& mword, const std::vector<int>& mshift,
                   const std::vector<int>& mbits) {
     const scx_sink& S = P.sink;
+    const int U0 = V < 4 ? V : 4;         // level 0: sub-rows per iteration
+    const int UQ = 4;                     // queue levels
     o << "    const unsigned char* stg = dsm + " << ring_off << " + (u32)tma_st * " << stage_bytes() << "u;\n";
     o << "    const i64 trow0 = tile * " << tile_rows << "ll;\n";
     o << "    const int rows = (int)(n - trow0 < " << tile_rows << "ll ? n - trow0 : " << tile_rows << "ll);\n";
@@ -1003,21 +1033,27 @@ struct Gen {
       const bool first = L == 0, last = L + 1 == levels.size();
       const char* qin = (L % 2 == 1) ? "qbuf0" : "qbuf1";
       const char* qout = (L % 2 == 0) ? "qbuf0" : "qbuf1";
+      U = first ? U0 : UQ;
       o << "    { // level " << L << ": items " << levels[L].first << ".." << levels[L].second << "\n";
       if (!last) o << "      u32 qn = 0;\n";
       if (first) {
-        o << "#pragma unroll 1\n      for (int c = 0; c < " << SEG << "; c += 32) {\n";
-        o << "        const int lr = warp * " << SEG << " + c + lane;\n";
-        o << "        bool ok = lr < rows;\n";
+        o << "#pragma unroll 1\n      for (int c = 0; c < " << SEG << "; c += " << 32 * U << ") {\n";
+        for (int u = 0; u < U; ++u) {
+          o << "        const int lr" << sfx(u) << " = warp * " << SEG << " + c + " << 32 * u << " + lane;\n";
+          o << "        bool ok" << sfx(u) << " = lr" << sfx(u) << " < rows;\n";
+        }
       } else {
-        o << "#pragma unroll 1\n      for (u32 c = 0; c < qcnt; c += 32) {\n";
-        o << "        const u32 q = c + lane;\n";
-        o << "        bool ok = q < qcnt;\n";
-        o << "        const int lr = ok ? (int)((const u16*)" << qin << ")[q] : 0;\n";
-        for (int sl : have) {
-          const char* t = ctype(P.slot_dtype[sl]);
-          o << "        const " << t << " pv" << sl << " = ok ? ((const " << t << "*)(" << qin << " + "
-            << q_poff[sl] << "))[q] : (" << t << ")0;\n";
+        o << "#pragma unroll 1\n      for (u32 c = 0; c < qcnt; c += " << 32 * U << ") {\n";
+        for (int u = 0; u < U; ++u) {
+          const std::string q = "q" + sfx(u);
+          o << "        const u32 " << q << " = c + " << 32 * u << "u + lane;\n";
+          o << "        bool ok" << sfx(u) << " = " << q << " < qcnt;\n";
+          o << "        const int lr" << sfx(u) << " = ok" << sfx(u) << " ? (int)((const u16*)" << qin << ")[" << q << "] : 0;\n";
+          for (int sl : have) {
+            const char* t = ctype(P.slot_dtype[sl]);
+            o << "        const " << t << " pv" << sl << sfx(u) << " = ok" << sfx(u) << " ? ((const " << t
+              << "*)(" << qin << " + " << q_poff[sl] << "))[" << q << "] : (" << t << ")0;\n";
+          }
         }
       }
       std::vector<int> now = have;
@@ -1034,16 +1070,23 @@ struct Gen {
         }
       }
       if (!last) {
-        o << "        const u32 m = __ballot_sync(0xffffffffu, ok);\n";
-        o << "        if (ok) {\n          const u32 pos = qn + __popc(m & lt);\n";
-        o << "          ((u16*)" << qout << ")[pos] = (u16)lr;\n";
-        for (int sl : now) {
-          const char* t = ctype(P.slot_dtype[sl]);
-          o << "          ((" << t << "*)(" << qout << " + " << q_poff[sl] << "))[pos] = pv" << sl << ";\n";
+        for (int u = 0; u < U; ++u) {
+          const std::string su = sfx(u);
+          o << "        { const u32 m = __ballot_sync(0xffffffffu, ok" << su << ");\n";
+          o << "          if (ok" << su << ") {\n            const u32 pos = qn + __popc(m & lt);\n";
+          o << "            ((u16*)" << qout << ")[pos] = (u16)lr" << su << ";\n";
+          for (int sl : now) {
+            const char* t = ctype(P.slot_dtype[sl]);
+            o << "            ((" << t << "*)(" << qout << " + " << q_poff[sl] << "))[pos] = pv" << sl << su << ";\n";
+          }
+          o << "          }\n          qn += __popc(m); }\n";
         }
-        o << "        }\n        qn += __popc(m);\n";
       } else {
-        emit_chunk_sink(dense_priv, dense_reg, NC, NW, M, mword, mshift, mbits);
+        for (int u = 0; u < U; ++u) {
+          cu = sfx(u);
+          emit_chunk_sink(dense_priv, dense_reg, NC, NW, M, mword, mshift, mbits);
+        }
+        cu.clear();
       }
       o << "      }\n      __syncwarp();\n";
       if (!last) o << "      qcnt = qn;\n";
@@ -1071,29 +1114,31 @@ struct Gen {
     }
   }
 
+  // sink of the current sub-row (cu)
   void emit_chunk_sink(bool dense_priv, bool dense_reg, int NC, int NW, int M,
                        const std::vector<int>& mword, const std::vector<int>& mshift,
                        const std::vector<int>& mbits) {
     const scx_sink& S = P.sink;
+    const std::string ok = "ok" + cu;
     if (S.kind == SCX_SINK_COUNT) {
-      o << "        cnt += ok ? 1ull : 0ull;\n";
+      o << "        cnt += " << ok << " ? 1ull : 0ull;\n";
       return;
     }
     if (S.kind == SCX_SINK_COMPACT) {
-      o << "        const u32 m = __ballot_sync(0xffffffffu, ok);\n";
-      o << "        if (ok) {\n          const u32 pos = wq + __popc(m & lt);\n";
+      o << "        { const u32 m = __ballot_sync(0xffffffffu, " << ok << ");\n";
+      o << "          if (" << ok << ") {\n            const u32 pos = wq + __popc(m & lt);\n";
       for (int i = 0; i < S.n_out; ++i) {
         const int s2 = S.out_slot[i];
         const char* t = ctype(S.out[i].dtype);
-        o << "          ((" << t << "*)(obuf + " << ob_coff[i] << "))[pos] = (" << t << ")";
-        if (s2 < 0) o << "(trow0 + lr);\n";
+        o << "            ((" << t << "*)(obuf + " << ob_coff[i] << "))[pos] = (" << t << ")";
+        if (s2 < 0) o << "(trow0 + lr" << cu << ");\n";
         else o << val(s2, "") << ";\n";
       }
-      o << "        }\n        wq += __popc(m);\n";
+      o << "          }\n          wq += __popc(m); }\n";
       return;
     }
     // dense group-by, one row
-    o << "        if (ok) {\n";
+    o << "        if (" << ok << ") {\n";
     o << "          int cell = 0;\n";
     for (int i = 0; i < S.gkey.n; ++i) {
       std::string v = "(" + key_value(S.gkey, i, "") + " - " + lit64(S.gkey.lo[i]) + ")";
@@ -1299,7 +1344,9 @@ struct Gen {
       if (tma) {
         const size_t stage = (size_t)kTPB * V * row_bytes;
         const char* rb = getenv("SCX_TMA_RING_KB");
-        const size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : 32) * 1024;
+        // chunk mode holds a stage for the whole tile (later levels re-read
+        // base columns): one more stage in flight than the row-owner path
+        const size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : (chunk ? 48 : 32)) * 1024;
         int st = (int)(ring_budget / stage);
         tma_stages = st < 2 ? 2 : (st > 6 ? 6 : st);
         ring_off = (sink_smem + 127) & ~(size_t)127;

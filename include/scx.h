@@ -265,6 +265,9 @@ int64_t scx_pipeline_status_words(const scx_pipeline* desc_host);
 int64_t scx_pipeline_source(const scx_pipeline* desc_host, char* buf, int64_t cap);
 int scx_pipeline_compile(const scx_pipeline* desc_host);
 int scx_jit_stats(int64_t* compiled, int64_t* disk_hits, int64_t* mem_hits);
+/* Drop the memoised launch plans (tuning runs that change SCX_* codegen knobs
+ * in-process; compiled kernels stay cached by source). */
+int scx_jit_clear_plans(void);
 
 /* ---- lookup tables (local_hash_join build side, relops.py:81-84) --------
  * Inserts packed keys of rows [0, n) of `cols` into `table` (pre-cleared

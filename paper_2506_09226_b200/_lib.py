@@ -113,6 +113,7 @@ _PROTOS = {
     "scx_pipeline_source": (i64, [C.POINTER(Pipeline), C.c_char_p, i64]),
     "scx_pipeline_compile": (C.c_int, [C.POINTER(Pipeline)]),
     "scx_jit_stats": (C.c_int, [C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+    "scx_jit_clear_plans": (C.c_int, []),
     "scx_lookup_clear": (C.c_int, [C.POINTER(Lookup), _vp]),
     "scx_lookup_build": (C.c_int, [C.POINTER(Lookup), C.POINTER(Column_), C.c_int,
                                    C.POINTER(KeySpec), i64, _vp, _vp]),

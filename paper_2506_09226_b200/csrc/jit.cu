@@ -1003,8 +1003,15 @@ struct Gen {
                   const std::vector<int>& mword, const std::vector<int>& mshift,
                   const std::vector<int>& mbits) {
     const scx_sink& S = P.sink;
-    const int U0 = V < 4 ? V : 4;         // level 0: sub-rows per iteration
-    const int UQ = 4;                     // queue levels
+    // sub-rows per lane per iteration: level 0 walks its whole segment in
+    // blocks of U0 chunks; queue levels use UQ (measured: UQ = 4 wasted
+    // issue slots on partly empty chunks, Q3 3.30 -> 3.67 ms)
+    const char* e0 = getenv("SCX_CHUNK_U0");
+    const char* eq = getenv("SCX_CHUNK_UQ");
+    int U0 = e0 && *e0 ? atoi(e0) : 4;
+    const int UQ = eq && *eq ? std::max(1, std::min(4, atoi(eq))) : 1;
+    U0 = std::max(1, std::min(U0, V));
+    while (V % U0) --U0;
     o << "    const unsigned char* stg = dsm + " << ring_off << " + (u32)tma_st * " << stage_bytes() << "u;\n";
     o << "    const i64 trow0 = tile * " << tile_rows << "ll;\n";
     o << "    const int rows = (int)(n - trow0 < " << tile_rows << "ll ? n - trow0 : " << tile_rows << "ll);\n";
@@ -2092,6 +2099,14 @@ extern "C" int scx_pipeline_compile(const scx_pipeline* d) {
   std::string cubin;
   bool disk = false;
   return jit::get_cubin(pp.src, pp.name, cubin, disk);
+}
+
+// drop the memoised launch plans (tuning: codegen knobs read from the
+// environment take effect for descriptors that were already planned)
+extern "C" int scx_jit_clear_plans(void) {
+  std::lock_guard<std::mutex> lk(jit::g_memo_mu);
+  jit::memo().clear();
+  return SCX_OK;
 }
 
 extern "C" int scx_jit_stats(int64_t* compiled, int64_t* disk_hits, int64_t* mem_hits) {

@@ -58,6 +58,7 @@ struct Keys {
   uint32_t np;
   uint64_t magic;                          // floor((2^64 - 1) / np) for h % np
   int staged;                              // single key == payload column 0 (staged by TMA)
+  int nbits;                               // bits of a bucket id: ceil(log2(np))
 };
 struct Cols {
   scx_column in[SCX_MAX_OUT];
@@ -153,10 +154,13 @@ struct alignas(128) Smem {
   uint64_t stage[2][kTile];                // TMA ring: two column tiles, source row order
   uint64_t perm[kTile];                    // one column tile in partition order
   uint16_t pos[kTile];                     // tile row -> tile-local partition-order position
-  uint32_t wcnt[kW][kMaxParts];            // per-warp running counts -> warp prefix
+  union {                                  // (wcnt while ranking, pid while moving columns)
+    uint32_t wcnt[kW][kMaxParts];          // per-warp running counts -> warp prefix
+    uint8_t pid[kTile];                    // tile-local position -> its part
+  };
+  uint64_t dptr[kMaxParts];                // this column: byte address of position 0's slot in part p
   uint32_t lbase[kMaxParts + 1];           // tile-local start of each part
   int64_t rel[kMaxParts];                  // destination row of tile-local position 0 of part p
-  uint64_t dbase[kMaxParts];               // destination base address of part p (this column)
   uint64_t bar[2];
 };
 
@@ -196,15 +200,12 @@ __device__ __forceinline__ void move_column(Smem& S, const T* stage, int rows) {
     if (r < rows) perm[S.pos[r]] = stage[r];
   }
   __syncthreads();
-  int p = 0;
-  uint32_t next = S.lbase[1];
-  T* out = reinterpret_cast<T*>(S.dbase[0]) + S.rel[0];   // part p's run, indexed by j
-  for (int j = tid; j < rows; j += kT) {
-    if ((uint32_t)j >= next) {
-      do { next = S.lbase[++p + 1]; } while ((uint32_t)j >= next);
-      out = reinterpret_cast<T*>(S.dbase[p]) + S.rel[p];
-    }
-    out[j] = perm[j];
+  // position j belongs to part pid[j]; its slot is dptr[p] + j (dptr folds
+  // the part's destination base and the tile's offset inside the part)
+#pragma unroll
+  for (int s = 0; s < kPer; ++s) {
+    const int j = s * kT + tid;
+    if (j < rows) reinterpret_cast<T*>(S.dptr[S.pid[j]])[j] = perm[j];
   }
 }
 
@@ -269,7 +270,16 @@ __global__ void __launch_bounds__(kT, 4) part_scatter_kernel(const __grid_consta
     uint32_t rk[kPer];
 #pragma unroll
     for (int s = 0; s < kPer; ++s) {
-      const uint32_t peers = __match_any_sync(0xffffffffu, d[s]);
+      // lanes with the same bucket: one ballot per bucket bit (np <= 64:
+      // at most 6) instead of match.any
+      const bool valid = d[s] != 0xFFFFFFFFu;
+      const uint32_t vb = __ballot_sync(0xffffffffu, valid);
+      uint32_t peers = valid ? vb : ~vb;
+      for (int k = 0; k < K.nbits; ++k) {
+        const bool bit = (d[s] >> k) & 1u;
+        const uint32_t b = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? b : ~b;
+      }
       uint32_t before = 0;
       if (d[s] != 0xFFFFFFFFu) before = S.wcnt[w][d[s]];
       __syncwarp();
@@ -311,17 +321,26 @@ __global__ void __launch_bounds__(kT, 4) part_scatter_kernel(const __grid_consta
     }
 #pragma unroll
     for (int s = 0; s < kPer; ++s)
-      if (d[s] != 0xFFFFFFFFu)
-        S.pos[w * kSeg + s * 32 + lane] = (uint16_t)(S.lbase[d[s]] + S.wcnt[w][d[s]] + rk[s]);
+      if (d[s] != 0xFFFFFFFFu) rk[s] += S.lbase[d[s]] + S.wcnt[w][d[s]];
+    __syncthreads();                       // wcnt is dead: its bytes become pid
+#pragma unroll
+    for (int s = 0; s < kPer; ++s)
+      if (d[s] != 0xFFFFFFFFu) {
+        S.pos[w * kSeg + s * 32 + lane] = (uint16_t)rk[s];
+        S.pid[rk[s]] = (uint8_t)d[s];
+      }
 
     // ---- every column: TMA-staged tile -> partition order -> part runs
     for (int c = 0; c < C.n; ++c) {
       const int64_t q = q0 + c;
       const int b = (int)(q & 1);
-      for (int p = tid; p < np; p += kT)
-        S.dbase[p] = dst ? dst[(int64_t)C.orig[c] * np + p] : C.out[c];
+      {
+        const int wdt = dtype_size_d(C.in[c].dtype);
+        for (int p = tid; p < np; p += kT)
+          S.dptr[p] = (dst ? dst[(int64_t)C.orig[c] * np + p] : C.out[c]) + (uint64_t)(S.rel[p] * wdt);
+      }
       mbar_wait(&S.bar[b], (q >> 1) & 1);
-      __syncthreads();                     // pos / dbase / plain-loaded tail bytes visible
+      __syncthreads();                     // pos / pid / dptr / plain-loaded tail bytes visible
       switch (dtype_size_d(C.in[c].dtype)) {
         case 1: move_column(S, reinterpret_cast<const uint8_t*>(S.stage[b]), rows); break;
         case 2: move_column(S, reinterpret_cast<const uint16_t*>(S.stage[b]), rows); break;
@@ -331,7 +350,7 @@ __global__ void __launch_bounds__(kT, 4) part_scatter_kernel(const __grid_consta
       // stage[b] was consumed before move_column's barrier: refill it with q + 2
       if (tid == 0) fence_proxy_async_smem();
       issue(q + 2);
-      __syncthreads();                     // perm / dbase reuse
+      __syncthreads();                     // perm / dptr reuse
     }
   }
 }
@@ -398,6 +417,8 @@ static int load_keys(const scx_column* keys, int n_keys, int np, Keys& K) {
   K.np = (uint32_t)np;
   K.magic = ~0ull / (uint64_t)np;
   K.staged = 0;
+  K.nbits = 0;
+  while ((1 << K.nbits) < np) ++K.nbits;
   for (int i = 0; i < n_keys; ++i) {
     if (dtype_size(keys[i].dtype) == 0) {
       set_error("partition: key %d has bad dtype %d", i, keys[i].dtype);

@@ -1,0 +1,53 @@
+"""Per-query device time of the probe-heavy queries at SF100 under several
+codegen configurations (env knobs of csrc/jit.cu), one process, the launch-
+plan memo cleared between configurations (scx_jit_clear_plans).
+
+    python tools/chunk_sweep.py --configs "SCX_CHUNK=0;SCX_CHUNK=1;SCX_CHUNK=1,SCX_CHUNK_U0=2"
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2506_09226_b200 as P  # noqa: E402
+from paper_2506_09226_b200 import _lib  # noqa: E402
+from paper_2506_09226_b200.data import cached_generate  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--sf", type=float, default=100)
+ap.add_argument("--queries", default="Q3,Q5,Q7,Q8,Q9,Q10,Q12,Q17,Q19,Q20,Q21,Q2,Q16,Q11")
+ap.add_argument("--configs", required=True)
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+lib = _lib.load()
+tables = P.load_tables(cached_generate(a.sf))
+qs = a.queries.split(",")
+knobs = set()
+out = {}
+for cfg in a.configs.split(";"):
+    env = dict(kv.split("=") for kv in cfg.split(",") if kv)
+    for k in knobs | set(env):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    knobs |= set(env)
+    lib.scx_jit_clear_plans()
+    res = {}
+    for q in qs:
+        P.reference_run(q, tables)            # compile + warm
+        ts = []
+        for _ in range(a.reps):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            P.reference_run(q, tables)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        res[q] = round(statistics.median(ts), 3)
+    out[cfg] = res
+    print(cfg, "sum", round(sum(res.values()), 2), res, flush=True)
+print(json.dumps(out))

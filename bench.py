@@ -852,9 +852,9 @@ def main() -> None:
         sync_all()
         if i > 0:            # first e2e pass warms the pinned path
             e2e_ms.append(e0.elapsed_time(e1))
-            if ep.n == 1:    # when the last column (and its unpack) landed
-                e2e_up_ms.append(max(e0.elapsed_time(ev) for evs in ready.values()
-                                     for ev in evs))
+            evs_all = [ev for evs in ready.values() for ev in evs] if ep.n == 1 else []
+            if evs_all:      # when the last column (and its unpack) landed
+                e2e_up_ms.append(max(e0.elapsed_time(ev) for ev in evs_all))
         d2h_bytes = sum(v.nbytes for r in out.values() if r for _, v, _ in r.values())
         del dev_tables
         gc.enable()

@@ -141,14 +141,17 @@ def upload_packed(pc: PackedColumn, src_words, src_bases, stream):
     import torch
     from .table import alloc
     buf = alloc(pc.n, pc.dtype)
+    # scratch comes from the CALLER's stream pool (the caching allocator only
+    # recycles a block on the stream that allocated it; a fresh copy stream
+    # per upload would cudaMalloc every pass) and is fenced to `stream`
+    dw = alloc(src_words.numel(), np.int32) if src_words is not None and pc.words is not None \
+        else None
+    db = alloc(src_bases.numel(), np.int64) if src_bases is not None else None
     with torch.cuda.stream(stream):
-        dw = db = None
-        if src_words is not None and pc.words is not None:
-            dw = alloc(src_words.numel(), np.int32)
+        if dw is not None:
             dw.copy_(src_words, non_blocking=True)
             dw.record_stream(stream)
-        if src_bases is not None:
-            db = alloc(src_bases.numel(), np.int64)
+        if db is not None:
             db.copy_(src_bases, non_blocking=True)
             db.record_stream(stream)
         L.call("scx_unpack", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n, pc.k,

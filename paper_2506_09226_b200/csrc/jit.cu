@@ -1286,9 +1286,23 @@ struct Gen {
       for (int pi = 0; pi < P.n_probes; ++pi)
         coarse |= P.probe[pi].table.kind == SCX_HT_BITMAP && P.probe[pi].table._pad > 0 &&
                   P.probe[pi].table.keys != 0;
+      // a compaction point exists when a filtering stage is followed by
+      // another probe; without one the mode only adds overhead (measured:
+      // Q9's semi-join compaction 10.1 -> 11.1 ms, Q11 2.6 -> 2.8), and the
+      // private-accumulator group-bys measured slower too (Q8 4.5 -> 5.6)
+      int cuts = 0;
+      if (P.pre.clause_mask != 0 && P.pre.n_atoms != 0 && P.n_probes > 0) ++cuts;
+      for (int i = 0; i + 1 < P.n_probes; ++i) {
+        const scx_probe& pb = P.probe[i];
+        if ((pb.after.clause_mask != 0 && pb.after.n_atoms != 0) || pb.kind == SCX_JOIN_SEMI ||
+            pb.kind == SCX_JOIN_ANTI || (pb.kind == SCX_JOIN_INNER && pb.table.kind != SCX_HT_IDENTITY))
+          ++cuts;
+      }
+      const bool forced = e && e[0] == '2';
       chunk = !(e && e[0] == '0') && P.n_probes > 0 && P.n_base > 0 && row_bytes > 0 && !coarse &&
               (S.kind == SCX_SINK_AGG_DENSE || S.kind == SCX_SINK_COMPACT ||
-               S.kind == SCX_SINK_COUNT);
+               S.kind == SCX_SINK_COUNT) &&
+              (forced || (cuts > 0 && !dense_priv));
       if (chunk) {
         int out_bytes = 0;
         if (S.kind == SCX_SINK_COMPACT)
@@ -1351,9 +1365,9 @@ struct Gen {
       if (tma) {
         const size_t stage = (size_t)kTPB * V * row_bytes;
         const char* rb = getenv("SCX_TMA_RING_KB");
-        // chunk mode holds a stage for the whole tile (later levels re-read
-        // base columns): one more stage in flight than the row-owner path
-        const size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : (chunk ? 48 : 32)) * 1024;
+        // (chunk mode with a 48 KB ring measured slower than 32 KB: 69.0 vs
+        // 66.9 ms over the probe-heavy queries -- fewer CTAs per SM)
+        const size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : 32) * 1024;
         int st = (int)(ring_budget / stage);
         tma_stages = st < 2 ? 2 : (st > 6 ? 6 : st);
         ring_off = (sink_smem + 127) & ~(size_t)127;

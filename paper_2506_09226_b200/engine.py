@@ -377,6 +377,9 @@ def reserve_device_pool(nbytes: int) -> int:
     return nbytes
 
 
+_COPY_STREAMS: dict = {}
+
+
 def upload_tables_async(host: dict, order=None, stream=None):
     """Upload pinned host columns on a copy stream, table by table in `order`
     (first use first), without blocking the compute stream.
@@ -390,8 +393,13 @@ def upload_tables_async(host: dict, order=None, stream=None):
     """
     import torch
     from .codec import PinnedPacked, upload_packed
-    # two copy streams: columns alternate between them (both DMA engines busy)
-    streams = [stream or torch.cuda.Stream(), torch.cuda.Stream()]
+    # two copy streams: columns alternate between them (both DMA engines busy);
+    # kept per device so repeated uploads reuse them
+    global _COPY_STREAMS
+    dev = torch.cuda.current_device()
+    if dev not in _COPY_STREAMS:
+        _COPY_STREAMS[dev] = [torch.cuda.Stream(), torch.cuda.Stream()]
+    streams = [stream or _COPY_STREAMS[dev][0], _COPY_STREAMS[dev][1]]
     main = torch.cuda.current_stream()
     for cs in streams:
         cs.wait_stream(main)       # buffers below are allocated on `main`
@@ -419,7 +427,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
         evs = []
         for cs in streams:
             if id(cs) in used:
-                ev = torch.cuda.Event()
+                ev = torch.cuda.Event(enable_timing=True)
                 ev.record(cs)
                 evs.append(ev)
         tables[tname] = ColumnTable(cols)

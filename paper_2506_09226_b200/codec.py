@@ -133,27 +133,47 @@ def unpack_host(pc: PackedColumn) -> np.ndarray:
     return out.astype(pc.dtype)
 
 
-def upload_packed(pc: PackedColumn, src_words, src_bases, stream):
+def scratch_bytes(pp: "PinnedPacked") -> int:
+    """Device scratch (256-B aligned words + bases) of one packed column."""
+    n = 0
+    if pp.words is not None:
+        n += (pp.words.numel() * 4 + 255) // 256 * 256
+    if pp.bases is not None:
+        n += (pp.bases.numel() * 8 + 255) // 256 * 256
+    return n
+
+
+def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None):
     """Device column buffer of ``pc``: H2D of the pinned words (+ bases) on
-    ``stream``, then scx_unpack on the same stream.  The scratch copies are
-    tied to ``stream`` (record_stream) so the allocator does not hand them to
-    another stream before the unpack has read them."""
+    ``stream``, then scx_unpack on the same stream.  ``scratch``: a uint8
+    device view of >= scratch_bytes() (the caller carves one arena per upload
+    so repeated uploads reuse one allocation); without it the words get their
+    own allocation, fenced to ``stream`` (record_stream)."""
     import torch
     from .table import alloc
     buf = alloc(pc.n, pc.dtype)
-    # scratch comes from the CALLER's stream pool (the caching allocator only
-    # recycles a block on the stream that allocated it; a fresh copy stream
-    # per upload would cudaMalloc every pass) and is fenced to `stream`
-    dw = alloc(src_words.numel(), np.int32) if src_words is not None and pc.words is not None \
-        else None
-    db = alloc(src_bases.numel(), np.int64) if src_bases is not None else None
+    dw = db = None
+    off = 0
+    if src_words is not None and pc.words is not None:
+        nw = src_words.numel()
+        if scratch is not None:
+            dw = scratch[off:off + nw * 4].view(torch.int32)
+            off += (nw * 4 + 255) // 256 * 256
+        else:
+            dw = alloc(nw, np.int32)
+    if src_bases is not None:
+        nb = src_bases.numel()
+        db = scratch[off:off + nb * 8].view(torch.int64) if scratch is not None \
+            else alloc(nb, np.int64)
     with torch.cuda.stream(stream):
         if dw is not None:
             dw.copy_(src_words, non_blocking=True)
-            dw.record_stream(stream)
+            if scratch is None:
+                dw.record_stream(stream)
         if db is not None:
             db.copy_(src_bases, non_blocking=True)
-            db.record_stream(stream)
+            if scratch is None:
+                db.record_stream(stream)
         L.call("scx_unpack", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n, pc.k,
                pc.lo, pc.encoding, C.c_void_p(db.data_ptr() if db is not None else 0),
                L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(stream))

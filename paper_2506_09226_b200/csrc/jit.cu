@@ -434,6 +434,8 @@ struct Gen {
   size_t q_off = 0, qb_bytes = 0, ob_off = 0, ob_bytes = 0;
   std::vector<int> q_poff;      // payload slot -> byte offset inside a queue buffer
   std::vector<int> ob_coff;     // COMPACT output column -> offset inside a warp's out buffer
+  uint32_t early = 0xffffffffu;  // late materialisation: base columns loaded before the first filter
+  bool late = false;
   std::string cu;               // chunk mode: variable suffix of the current sub-row ("_2")
   int U = 1;                    // chunk mode: sub-rows (32-row chunks) per lane per iteration
   static std::string sfx(int u) { return "_" + std::to_string(u); }
@@ -718,8 +720,9 @@ struct Gen {
     o << "      }\n    }\n";
   }
 
-  void emit_loads() {
+  void emit_loads(uint32_t only = 0xffffffffu) {
     for (int s = 0; s < P.n_base; ++s) {
+      if (!((only >> s) & 1u)) continue;
       const int w = dtype_size(P.base[s].dtype);
       const int nb = V * w;                  // bytes per chunk
       const int nwords = nb / 4;
@@ -919,6 +922,26 @@ struct Gen {
       }
       o << "        }\n      }\n    }\n";
     }
+  }
+
+  // base slots read by a predicate
+  uint32_t pred_cols(const scx_pred& pr) {
+    uint32_t m = 0;
+    if (pr.clause_mask == 0 || pr.n_atoms == 0) return 0;
+    auto add = [&](int sl) { if (sl >= 0 && sl < P.n_base) m |= 1u << sl; };
+    for (int a = pr.first_atom; a < pr.first_atom + pr.n_atoms && a < SCX_MAX_ATOMS; ++a) {
+      const scx_atom& A = P.atoms[a];
+      if (A.op == SCX_ATOM_POLY) {
+        if (A.slot < 0 || A.slot >= SCX_MAX_POLYS) continue;
+        const scx_measure& M = P.polys[A.slot];
+        for (int t = 0; t < M.n_terms && t < 2; ++t)
+          for (int f = 0; f < M.t[t].n_factors && f < 3; ++f) add(M.t[t].f[f].slot);
+      } else {
+        add(A.slot);
+        if (A.op == SCX_ATOM_DIFF) add(A.slot2);
+      }
+    }
+    return m;
   }
 
   // ---- chunked dense mode (one row per lane, per-warp selection queues) ----
@@ -1317,6 +1340,35 @@ struct Gen {
         SEG = 32 * V;
       }
     }
+    // Late materialisation (row-owner probe kernels): load only the columns
+    // of the first filtering stage (the pre-predicate, else probe 0's key and
+    // its after-filter), then the rest only in threads that still hold a
+    // selected row -- a selective first stage (Q9's green-part semi join:
+    // 5% survive) skips most sectors of the other columns.
+    {
+      const char* e = getenv("SCX_LATE");
+      const bool pre_on = P.pre.clause_mask != 0 && P.pre.n_atoms != 0;
+      bool filt0 = false;
+      uint32_t m = 0;
+      if (pre_on) {
+        m = pred_cols(P.pre);
+        filt0 = true;
+      } else if (P.n_probes > 0) {
+        const scx_probe& pb = P.probe[0];
+        for (int i = 0; i < pb.key.n && i < SCX_MAX_KEYS; ++i)
+          if (pb.key.slot[i] >= 0 && pb.key.slot[i] < P.n_base) m |= 1u << pb.key.slot[i];
+        m |= pred_cols(pb.after);
+        filt0 = pb.kind == SCX_JOIN_SEMI || pb.kind == SCX_JOIN_ANTI ||
+                (pb.kind == SCX_JOIN_INNER && pb.table.kind != SCX_HT_IDENTITY) ||
+                (pb.after.clause_mask != 0 && pb.after.n_atoms != 0);
+      }
+      int late_bytes = 0;
+      for (int c = 0; c < P.n_base; ++c)
+        if (!((m >> c) & 1u)) late_bytes += dtype_size(P.base[c].dtype);
+      late = !chunk && !(e && e[0] == '0') && P.n_probes > 0 && filt0 && m != 0 &&
+             2 * late_bytes >= row_bytes;
+      if (late) early = m;
+    }
     // load pipeline: each thread copies (cp.async) its chunk of the NEXT tile's
     // base columns into shared memory while it processes this one, so a
     // tile's HBM latency overlaps the previous tile's probes and sink.  V
@@ -1358,7 +1410,7 @@ struct Gen {
       for (int pi = 0; pi < P.n_probes; ++pi) hash_probe |= P.probe[pi].table.kind == SCX_HT_HASH;
       // (private-accumulator group-bys keep 3 CTAs/SM on the register path:
       // their 48 KB of accumulators + the ring would leave 2; Q1 1.63 vs 1.68 ms)
-      tma = chunk || ((mode == '1' || (mode == '2' && P.n_probes == 0) ||
+      tma = chunk || (!late && (mode == '1' || (mode == '2' && P.n_probes == 0) ||
                        (mode == '3' && ((P.n_probes == 0 && !dense_priv) ||
                                         (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
                       !pipe && P.n_base > 0 && row_bytes > 0);
@@ -1614,7 +1666,7 @@ struct Gen {
       << " : ((1u << rem) - 1u);\n";
     emit_word_decls();
     o << "    if (rem > 0) {\n";
-    emit_loads();
+    emit_loads(late ? early : 0xffffffffu);
     o << "    }\n";
     // every consumer thread releases the stage itself, after a proxy fence:
     // its generic-proxy shared-memory reads must be ordered before the async
@@ -1624,7 +1676,18 @@ struct Gen {
                   << "    mb_arrive(bars + 8u * (" << tma_stages << " + tma_st));\n";
     // when rem == 0 the word arrays are uninitialised but sel == 0 masks every use
     emit_pred(P.pre, "pre-predicate");
-    for (int p = 0; p < P.n_probes; ++p) {
+    int p_first = 0;
+    if (late) {
+      if (!(P.pre.clause_mask != 0 && P.pre.n_atoms != 0)) {
+        emit_probe(0);
+        emit_pred(P.probe[0].after, "filter after probe");
+        p_first = 1;
+      }
+      o << "    if (sel) {   // late columns: only threads with a surviving row\n";
+      emit_loads(~early);
+      o << "    }\n";
+    }
+    for (int p = p_first; p < P.n_probes; ++p) {
       emit_probe(p);
       emit_pred(P.probe[p].after, "filter after probe");
     }

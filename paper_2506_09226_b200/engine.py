@@ -392,7 +392,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
     with the queries that can already run).  Single-rank tables only.
     """
     import torch
-    from .codec import PinnedPacked, upload_packed
+    from .codec import PinnedPacked, scratch_bytes, upload_packed
     # two copy streams: columns alternate between them (both DMA engines busy);
     # kept per device so repeated uploads reuse them
     global _COPY_STREAMS
@@ -404,6 +404,15 @@ def upload_tables_async(host: dict, order=None, stream=None):
     for cs in streams:
         cs.wait_stream(main)       # buffers below are allocated on `main`
     tables, events = {}, {}
+    # one scratch arena for every packed column's words: the same size each
+    # pass, so the caching allocator hands back the same block (per-column
+    # scratch allocations cudaMalloc'ed / freed inside timed passes)
+    total = sum(scratch_bytes(src) for cols in host.values() for _, src in cols.values()
+                if isinstance(src, PinnedPacked))
+    arena = alloc(max(total, 256), np.uint8)
+    for cs in streams:
+        arena.record_stream(cs)
+    aoff = 0
     k = 0
     for tname in (order or list(host)):
         cols = {}
@@ -414,7 +423,10 @@ def upload_tables_async(host: dict, order=None, stream=None):
             used.add(id(cs))
             if isinstance(pinned, PinnedPacked):
                 # packed words cross PCIe, scx_unpack rebuilds the column
-                buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs)
+                nb = scratch_bytes(pinned)
+                buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs,
+                                    arena[aoff:aoff + nb])
+                aoff += nb
             else:
                 buf = alloc(hc.row_count, hc.values.dtype)
                 with torch.cuda.stream(cs):

@@ -355,6 +355,104 @@ __global__ void __launch_bounds__(kT, 4) part_scatter_kernel(const __grid_consta
   }
 }
 
+// pass 2, direct variant: no shared-memory staging of the data at all.
+// Each lane keeps the bucket and stable rank of its 8 rows in registers;
+// after one CTA-wide prefix of the per-warp part counts every row's final
+// slot is known and each column is loaded (coalesced) and stored straight to
+// it.  A warp's 32 rows of one step land in at most np contiguous runs, one
+// per part, and neighbouring warps extend the same runs, so L2 merges the
+// partial sectors at run ends before they reach HBM.
+struct DirectSmem {
+  uint32_t wcnt[2][kW][kMaxParts];         // per-warp part counts -> warp prefix (tile parity)
+  int64_t tb[2][kMaxParts];                // tile's first slot of part p (within the part / global)
+  uint64_t base[SCX_MAX_OUT][kMaxParts];   // destination byte address of slot 0 of part p
+};
+
+template <typename T>
+__device__ __forceinline__ void direct_column(const scx_column& in, const DirectSmem& S, int c,
+                                              int64_t r0, int64_t n, int lane,
+                                              const uint32_t (&d)[kPer],
+                                              const uint64_t (&slot)[kPer]) {
+  const T* src = reinterpret_cast<const T*>(in.ptr);
+  T v[kPer];
+#pragma unroll
+  for (int s = 0; s < kPer; ++s) {
+    const int64_t i = r0 + s * 32 + lane;
+    v[s] = i < n ? __ldg(src + i) : T(0);
+  }
+#pragma unroll
+  for (int s = 0; s < kPer; ++s)
+    if (d[s] != 0xFFFFFFFFu) {
+      T* dstp = reinterpret_cast<T*>(S.base[c][d[s]]);
+      __stcs(dstp + slot[s], v[s]);
+    }
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kT, 4) part_scatter_direct_kernel(const __grid_constant__ Keys K,
+                                                                    const __grid_constant__ Cols C,
+                                                                    int64_t n,
+                                                                    const uint64_t* __restrict__ offs,
+                                                                    int64_t nb,
+                                                                    const uint64_t* __restrict__ dst) {
+  __shared__ DirectSmem S;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int np = (int)K.np;
+  for (int j = tid; j < 2 * kW * kMaxParts; j += kT) (&S.wcnt[0][0][0])[j] = 0;
+  for (int j = tid; j < C.n * np; j += kT) {
+    const int c = j / np, p = j % np;
+    S.base[c][p] = dst ? dst[(int64_t)C.orig[c] * np + p] : C.out[c];
+  }
+  __syncthreads();
+  const uint32_t lt = (1u << lane) - 1u;
+  int par = 0;
+  for (int64_t tile = blockIdx.x; tile < nb; tile += gridDim.x, par ^= 1) {
+    const int64_t r0 = tile * kTile + w * kSeg;
+    uint32_t d[kPer];
+    warp_buckets<KT>(K, r0, n, lane, d);
+    uint32_t rk[kPer];
+#pragma unroll
+    for (int s = 0; s < kPer; ++s) {
+      const bool valid = d[s] != 0xFFFFFFFFu;
+      const uint32_t vb = __ballot_sync(0xffffffffu, valid);
+      uint32_t peers = valid ? vb : ~vb;
+      for (int k = 0; k < K.nbits; ++k) {
+        const bool bit = (d[s] >> k) & 1u;
+        const uint32_t b = __ballot_sync(0xffffffffu, bit);
+        peers &= bit ? b : ~b;
+      }
+      uint32_t before = 0;
+      if (valid) before = S.wcnt[par][w][d[s]];
+      __syncwarp();
+      if (valid && (peers & lt) == 0) S.wcnt[par][w][d[s]] = before + __popc(peers);
+      __syncwarp();
+      rk[s] = before + __popc(peers & lt);
+    }
+    __syncthreads();
+    for (int p = tid; p < np; p += kT) {
+      uint32_t run = 0;
+#pragma unroll
+      for (int ww = 0; ww < kW; ++ww) { const uint32_t c = S.wcnt[par][ww][p]; S.wcnt[par][ww][p] = run; run += c; }
+      const int64_t o = (int64_t)offs[(int64_t)p * nb + tile];
+      S.tb[par][p] = dst ? o - (int64_t)offs[(int64_t)p * nb] : o;
+    }
+    for (int j = tid; j < kW * kMaxParts; j += kT) (&S.wcnt[par ^ 1][0][0])[j] = 0;
+    __syncthreads();
+    uint64_t slot[kPer];             // 64-bit: a 64 GiB table has 2^32 rows
+#pragma unroll
+    for (int s = 0; s < kPer; ++s)
+      slot[s] = d[s] != 0xFFFFFFFFu ? (uint64_t)(S.tb[par][d[s]] + S.wcnt[par][w][d[s]] + rk[s]) : 0ull;
+    for (int c = 0; c < C.n; ++c) {
+      switch (dtype_size_d(C.in[c].dtype)) {
+        case 1: direct_column<uint8_t>(C.in[c], S, c, r0, n, lane, d, slot); break;
+        case 2: direct_column<uint16_t>(C.in[c], S, c, r0, n, lane, d, slot); break;
+        case 4: direct_column<uint32_t>(C.in[c], S, c, r0, n, lane, d, slot); break;
+        default: direct_column<uint64_t>(C.in[c], S, c, r0, n, lane, d, slot); break;
+      }
+    }
+  }
+}
+
 // launch `F<KT>` for the single key's physical type (generic otherwise)
 template <template <typename> class F, typename... A>
 static void by_key_type(const Keys& K, A&&... a) {
@@ -393,6 +491,13 @@ struct ScatterLaunch {
     }
     static const int64_t per_sm = getenv("SCX_PART_CTAS") ? atoll(getenv("SCX_PART_CTAS")) : 4;
     const int64_t cap = per_sm > 0 ? (int64_t)(g_sms > 0 ? g_sms : 148) * per_sm : nb;
+    static const bool direct = !(getenv("SCX_PART_DIRECT") && getenv("SCX_PART_DIRECT")[0] == '0');
+    if (direct) {
+      const int64_t dcap = (int64_t)(g_sms > 0 ? g_sms : 148) * 8;
+      part_scatter_direct_kernel<KT><<<(unsigned)(nb < dcap ? nb : dcap), kT, 0, st>>>(
+          K, C, n, offs, nb, dst);
+      return;
+    }
     part_scatter_kernel<KT><<<(unsigned)(nb < cap ? nb : cap), kT, sizeof(Smem), st>>>(
         K, C, n, offs, nb, dst);
   }

@@ -835,6 +835,7 @@ def main() -> None:
         e0.record()
         if ep.n == 1:
             dev_tables, ready = upload_tables_async(host, copy_order)
+            up_events = [ev for evs in ready.values() for ev in evs]
             res = {}
             for q in E2E_QUERY_ORDER:
                 ctx = DeviceContext(ep, dev_tables, "default", "default_keys", timed=False,
@@ -852,9 +853,8 @@ def main() -> None:
         sync_all()
         if i > 0:            # first e2e pass warms the pinned path
             e2e_ms.append(e0.elapsed_time(e1))
-            evs_all = [ev for evs in ready.values() for ev in evs] if ep.n == 1 else []
-            if evs_all:      # when the last column (and its unpack) landed
-                e2e_up_ms.append(max(e0.elapsed_time(ev) for ev in evs_all))
+            if ep.n == 1 and up_events:   # when the last column (and its unpack) landed
+                e2e_up_ms.append(max(e0.elapsed_time(ev) for ev in up_events))
         d2h_bytes = sum(v.nbytes for r in out.values() if r for _, v, _ in r.values())
         del dev_tables
         gc.enable()

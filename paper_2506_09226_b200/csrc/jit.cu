@@ -1365,7 +1365,10 @@ struct Gen {
       int late_bytes = 0;
       for (int c = 0; c < P.n_base; ++c)
         if (!((m >> c) & 1u)) late_bytes += dtype_size(P.base[c].dtype);
-      late = !chunk && !(e && e[0] == '0') && P.n_probes > 0 && filt0 && m != 0 &&
+      // measured at SF100 and left opt-in (SCX_LATE=1): Q21 7.8 -> 8.7 ms,
+      // Q9 10.3 -> 10.6 -- the second dependent load round per tile costs
+      // more than the skipped sectors save
+      late = !chunk && e && e[0] == '1' && P.n_probes > 0 && filt0 && m != 0 &&
              2 * late_bytes >= row_bytes;
       if (late) early = m;
     }

@@ -1336,7 +1336,7 @@ struct Gen {
                  (size_t)8 * seg * (out_bytes + 8);
         };
         const char* ev = getenv("SCX_CHUNK_V");
-        V = ev && *ev ? (atoi(ev) >= 8 ? 8 : 4) : (est(8) <= 80 * 1024 ? 8 : 4);
+        V = ev && *ev ? (atoi(ev) >= 8 ? 8 : atoi(ev) <= 2 ? 2 : 4) : (est(8) <= 80 * 1024 ? 8 : 4);
         SEG = 32 * V;
       }
     }

@@ -219,7 +219,8 @@ typedef struct scx_pipeline {
   int32_t n_base;
   int32_t n_slots;
   int32_t n_probes;
-  int32_t _pad;
+  int32_t _pad;                  /* hint: estimated % of rows passing the first
+                                    filtering stage (0 = unknown); tiling only */
   scx_column base[SCX_MAX_BASE];
   int32_t slot_dtype[SCX_MAX_SLOTS];
   scx_pred pre;                  /* on base slots, before probes          */

@@ -1336,7 +1336,14 @@ struct Gen {
                  (size_t)8 * seg * (out_bytes + 8);
         };
         const char* ev = getenv("SCX_CHUNK_V");
-        V = ev && *ev ? (atoi(ev) >= 8 ? 8 : atoi(ev) <= 2 ? 2 : 4) : (est(8) <= 80 * 1024 ? 8 : 4);
+        // P._pad = host estimate of the first stage's survivors in percent:
+        // very selective first stages amortise each tile's fixed cost over
+        // more rows with 2048-row tiles (measured: Q20 5.0 -> 4.1 ms, Q19
+        // 2.6 -> 2.2, Q14 2.3 -> 1.9), the rest keep 1024 (Q5 3.7 vs 4.1,
+        // Q3 5.1 vs 5.4)
+        const bool selective = P._pad > 0 && P._pad <= 12;
+        V = ev && *ev ? (atoi(ev) >= 8 ? 8 : atoi(ev) <= 2 ? 2 : 4)
+                      : (selective && est(8) <= 110 * 1024 ? 8 : 4);
         SEG = 32 * V;
       }
     }

@@ -239,6 +239,12 @@ class BitmapLookup:
         self._bits = alloc((span + 31) // 32, np.uint32)
         self.lk.vals = self._bits.data_ptr()
         self.lk.keys = 0
+        # build-side row estimate (a tiling hint only, see _first_stage_survival)
+        if isinstance(source, TableView):
+            f = _pred_survival(source.pre, source.meta) if not source.pre.is_true else 1.0
+            self.rows_est = source.base.row_count * f
+        else:
+            self.rows_est = source.row_count
         L.call("scx_lookup_clear", C.byref(self.lk), _stream())
         if isinstance(source, TableView) and (source.probes or not source.pre.is_true
                                               or not source.post.is_true):
@@ -716,6 +722,52 @@ TRACE: set | None = None
 _GATHER_PF_MIN_ROWS = 1 << 20
 
 
+def _atom_survival(a, meta) -> float:
+    c = meta.get(a.col)
+    if a.op == "set" and c is not None and c.dictionary:
+        f = len(a.codes) / max(1, len(c.dictionary))
+    elif a.op == "range" and c is not None and c.hi > c.lo:
+        lo, hi = max(a.lo, c.lo), min(a.hi, c.hi)
+        f = max(0.0, (hi - lo + 1) / (c.hi - c.lo + 1))
+    else:
+        f = 0.5
+    return 1.0 - f if a.negate else f
+
+
+def _pred_survival(pred: Pred, meta) -> float:
+    tot = 0.0
+    for clause in pred.clauses:
+        f = 1.0
+        for a in clause:
+            f *= _atom_survival(a, meta)
+        tot += f
+    return min(1.0, tot)
+
+
+def _first_stage_survival(v: "TableView"):
+    """Guess of the fraction of rows passing the first filtering stage (the
+    pre-predicate, else probe 0 with its after-filter), None if unknown."""
+    if not v.pre.is_true:
+        return _pred_survival(v.pre, v.meta)
+    if not v.probes:
+        return None
+    st = v.probes[0]
+    lk = st.lookup
+    f = 1.0
+    if lk.lk.kind == L.HT_BITMAP or (lk.lk.kind == L.HT_DIRECT and st.kind != L.JOIN_LEFT):
+        t = getattr(lk, "table", None)
+        rows = t.row_count if t is not None else getattr(lk, "rows_est", None)
+        if rows is not None and lk.lk.cap:
+            f = min(1.0, rows / lk.lk.cap)
+            if st.kind == L.JOIN_ANTI:
+                f = 1.0 - f
+        else:
+            return None
+    if not st.after.is_true:
+        f *= _pred_survival(st.after, v.meta)
+    return f
+
+
 def _probe_key_sorted(c: Column) -> bool:
     """Non-decreasing probe key, known without a device check: generated in
     order (l_orderkey, surrogate keys), kept by increasing row selections and
@@ -801,6 +853,11 @@ class _Builder:
         for i, st in enumerate(v.probes):
             self._pred(P.probe[i].after, st.after)
         self._pred(P.post, v.post)
+        # hint for the kernel generator (scx_pipeline._pad): estimated percent
+        # of rows surviving the first filtering stage (uniform-range guess;
+        # 0 = unknown).  Very selective first stages get bigger chunk tiles.
+        est = _first_stage_survival(v)
+        P._pad = 0 if est is None else max(1, min(100, int(round(est * 100))))
 
     # ---- atoms ----
     def _atom(self, a: Atom, clause: int) -> int:

@@ -1626,23 +1626,47 @@ def finish_dense(acc: np.ndarray, keys, kcols, cards, luts, plan, measures, coun
     return ColumnTable(out, tuple(keys))
 
 
-def _agg_columns(out: dict, plan, measure_col, G: int) -> None:
+def _agg_bounds(measures, meta, n_in: int) -> dict:
+    """Proven [lo, hi] of each aggregated measure over at most n_in input rows
+    (per-row interval x row count): a sort / top-k over the result then packs
+    its keys without a min/max pass and the host sync that reads it."""
+    out = {}
+    for j, (op, im) in enumerate(measures):
+        if op == "count":
+            out[j] = (0, max(0, n_in))
+            continue
+        if op != "sum":
+            continue
+        r = _measure_range(im, meta)
+        if r is None:
+            continue
+        lo, hi = min(0, r[0] * n_in), max(0, r[1] * n_in)
+        if INT64_MIN < lo and hi < INT64_MAX:
+            out[j] = (lo, hi)
+    return out
+
+
+def _agg_columns(out: dict, plan, measure_col, G: int, bounds: dict | None = None) -> None:
     """Result columns of a keyed aggregation from its per-measure int64
-    accumulators (measure_col(j) -> tensor of G values), relops.py:131-158."""
+    accumulators (measure_col(j) -> tensor of G values), relops.py:131-158.
+    ``bounds``: measure index -> proven [lo, hi] (_agg_bounds)."""
+    bounds = bounds or {}
     for a in plan:
         if a.op == "count":
-            out[a.out] = Column("int64", measure_col(a.m), 0, None, 0, INT64_MAX)
+            lo, hi = bounds.get(a.m, (0, INT64_MAX))
+            out[a.out] = Column("int64", measure_col(a.m), 0, None, lo, hi)
         elif a.op in ("min", "max"):
             s = a.src
             out[a.out] = Column(s.kind, measure_col(a.m), s.scale, None, s.lo, s.hi)
         elif a.op == "sum":
             k = decimal_exponent(a.q)
+            lo, hi = bounds.get(a.m, (INT64_MIN, INT64_MAX))
             if a.kind == "float64":
                 if k < 0:
                     raise SchemaError("sum with a non-decimal denominator")
-                out[a.out] = Column("float64", measure_col(a.m), k, None, INT64_MIN, INT64_MAX)
+                out[a.out] = Column("float64", measure_col(a.m), k, None, lo, hi)
             else:
-                out[a.out] = Column("int64", measure_col(a.m), 0, None, INT64_MIN, INT64_MAX)
+                out[a.out] = Column("int64", measure_col(a.m), 0, None, lo, hi)
         else:  # avg
             k = decimal_exponent(a.q)
             if k < 0:
@@ -1708,7 +1732,8 @@ def _stream_group(v: TableView, key: str, kcol: Column, plan, measures, having):
             break
         cap = G + (G & 1)             # keeps every measure slice 16-byte aligned
     out = {key: Column(kcol.kind, okeys[:G], kcol.scale, kcol.dictionary, kcol.lo, kcol.hi)}
-    _agg_columns(out, plan, lambda j: oacc[j * cap: j * cap + G], G)
+    _agg_columns(out, plan, lambda j: oacc[j * cap: j * cap + G], G,
+                 _agg_bounds(measures, v.meta, v.base.row_count))
     return ColumnTable(out, (key,))
 
 
@@ -1902,7 +1927,7 @@ def _group_hash(v, b, keys, kcols, plan, measures, count_m, sort=True, hv=None) 
             raise SchemaError("aggregate result exceeds the 64-bit output range")
         return out64
 
-    _agg_columns(out, plan, measure_col, G)
+    _agg_columns(out, plan, measure_col, G, _agg_bounds(measures, v.meta, v.base.row_count))
     res = ColumnTable(out, tuple(keys))
     res._having_done = direct and hv is not None
     return res

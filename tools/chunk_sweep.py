@@ -27,27 +27,37 @@ lib = _lib.load()
 tables = P.load_tables(cached_generate(a.sf))
 qs = a.queries.split(",")
 knobs = set()
-out = {}
-for cfg in a.configs.split(";"):
+cfgs = a.configs.split(";")
+best = {c: {} for c in cfgs}
+
+
+def apply(cfg):
+    global knobs
     env = dict(kv.split("=") for kv in cfg.split(",") if kv)
     for k in knobs | set(env):
         os.environ.pop(k, None)
     os.environ.update(env)
     knobs |= set(env)
     lib.scx_jit_clear_plans()
-    res = {}
+
+
+for cfg in cfgs:                       # compile + warm every configuration once
+    apply(cfg)
     for q in qs:
-        P.reference_run(q, tables)            # compile + warm
-        ts = []
-        for _ in range(a.reps):
+        P.reference_run(q, tables)
+for r in range(a.reps):                # interleaved rounds: min over rounds per query
+    for cfg in (cfgs if r % 2 == 0 else cfgs[::-1]):
+        apply(cfg)
+        for q in qs:
+            P.reference_run(q, tables)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             P.reference_run(q, tables)
             e1.record()
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1))
-        res[q] = round(statistics.median(ts), 3)
-    out[cfg] = res
-    print(cfg, "sum", round(sum(res.values()), 2), res, flush=True)
-print(json.dumps(out))
+            t = e0.elapsed_time(e1)
+            best[cfg][q] = min(best[cfg].get(q, 1e9), round(t, 3))
+for cfg in cfgs:
+    print(cfg, "sum", round(sum(best[cfg].values()), 2), best[cfg], flush=True)
+print(json.dumps(best))

@@ -1028,12 +1028,16 @@ def _pack_budgets(P, measures, meta, n: int) -> None:
             P.sink.m[i]._pad = 0x100 | bits
 
 
-def _measure_bound(im: IntMeasure, meta: dict[str, Column]) -> int:
+def _measure_bound(im: IntMeasure, meta: dict[str, Column], tight: bool = True) -> int:
+    """|value| bound of a measure polynomial.  ``tight``: columns whose proven
+    range spans >= 2^32 (an aggregate's proven range is rows x per-row range,
+    far wider than its values) are measured with a min/max pass, as an
+    unproven column is; sort-key packing uses the proven range as is."""
     tot = 0
     for coef, fs in im.terms:
         b = abs(coef)
         for a, bb, col in fs:
-            lo, hi = _col_range(meta[col])
+            lo, hi = _col_range(meta[col], tight)
             b *= max(abs(a + bb * lo), abs(a + bb * hi), 1)
         tot += b
     return max(tot, 1)
@@ -1951,8 +1955,8 @@ def sort_pairs(keys, vals, n_bits: int):
     return ko, vo
 
 
-def _col_range(c: Column) -> tuple[int, int]:
-    if c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo:
+def _col_range(c: Column, tight: bool = False) -> tuple[int, int]:
+    if c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo and (not tight or c.hi - c.lo < 1 << 32):
         return c.lo, c.hi
     if c.row_count == 0:           # no values (e.g. a worker's empty partition)
         return 0, 0

@@ -1330,10 +1330,10 @@ struct Gen {
         int out_bytes = 0;
         if (S.kind == SCX_SINK_COMPACT)
           for (int i = 0; i < S.n_out; ++i) out_bytes += dtype_size(S.out[i].dtype);
-        auto est = [&](int v) {
+        auto est = [&](int v) {          // ring (2 stages) + queue buffers + out buffers
           const int seg = 32 * v;
-          return (size_t)2 * kTPB * v * row_bytes + (size_t)16 * seg * (2 + payload_bytes + 8) +
-                 (size_t)8 * seg * (out_bytes + 8);
+          return (size_t)2 * kTPB * v * row_bytes + (size_t)16 * seg * (2 + payload_bytes) +
+                 (size_t)8 * seg * out_bytes + 4096;
         };
         const char* ev = getenv("SCX_CHUNK_V");
         // P._pad = host estimate of the first stage's survivors in percent:

@@ -735,11 +735,20 @@ def _atom_survival(a, meta) -> float:
 
 
 def _pred_survival(pred: Pred, meta) -> float:
+    """Uniform-independence guess; the range atoms of one column in a clause
+    are intersected first (lo <= d AND d < hi is one interval)."""
     tot = 0.0
     for clause in pred.clauses:
         f = 1.0
+        ranges = {}
         for a in clause:
-            f *= _atom_survival(a, meta)
+            if a.op == "range" and not a.negate:
+                lo, hi = ranges.get(a.col, (INT64_MIN, INT64_MAX))
+                ranges[a.col] = (max(lo, a.lo), min(hi, a.hi))
+            else:
+                f *= _atom_survival(a, meta)
+        for col, (lo, hi) in ranges.items():
+            f *= _atom_survival(Atom("range", col, lo, hi), meta)
         tot += f
     return min(1.0, tot)
 
@@ -985,7 +994,7 @@ def _measure_range(im: IntMeasure | None, meta: dict[str, Column]):
         lo, hi = coef, coef
         for a, bb, col in fs:
             c = meta[col]
-            if not (c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo):
+            if not (c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo) or c.loose:
                 return None
             clo, chi = c.lo, c.hi
             x, y = a + bb * clo, a + bb * chi
@@ -1030,9 +1039,9 @@ def _pack_budgets(P, measures, meta, n: int) -> None:
 
 def _measure_bound(im: IntMeasure, meta: dict[str, Column], tight: bool = True) -> int:
     """|value| bound of a measure polynomial.  ``tight``: columns whose proven
-    range spans >= 2^32 (an aggregate's proven range is rows x per-row range,
-    far wider than its values) are measured with a min/max pass, as an
-    unproven column is; sort-key packing uses the proven range as is."""
+    range is loose (an aggregate's: rows x per-row range, far wider than its
+    values) are measured with a min/max pass, as an unproven column is;
+    sort-key packing uses the proven range as is."""
     tot = 0
     for coef, fs in im.terms:
         b = abs(coef)
@@ -1659,6 +1668,7 @@ def _agg_columns(out: dict, plan, measure_col, G: int, bounds: dict | None = Non
         if a.op == "count":
             lo, hi = bounds.get(a.m, (0, INT64_MAX))
             out[a.out] = Column("int64", measure_col(a.m), 0, None, lo, hi)
+            out[a.out].loose = a.m in bounds
         elif a.op in ("min", "max"):
             s = a.src
             out[a.out] = Column(s.kind, measure_col(a.m), s.scale, None, s.lo, s.hi)
@@ -1671,6 +1681,7 @@ def _agg_columns(out: dict, plan, measure_col, G: int, bounds: dict | None = Non
                 out[a.out] = Column("float64", measure_col(a.m), k, None, lo, hi)
             else:
                 out[a.out] = Column("int64", measure_col(a.m), 0, None, lo, hi)
+            out[a.out].loose = a.m in bounds
         else:  # avg
             k = decimal_exponent(a.q)
             if k < 0:
@@ -1956,7 +1967,7 @@ def sort_pairs(keys, vals, n_bits: int):
 
 
 def _col_range(c: Column, tight: bool = False) -> tuple[int, int]:
-    if c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo and (not tight or c.hi - c.lo < 1 << 32):
+    if c.lo > INT64_MIN and c.hi < INT64_MAX and c.hi >= c.lo and not (tight and c.loose):
         return c.lo, c.hi
     if c.row_count == 0:           # no values (e.g. a worker's empty partition)
         return 0, 0

@@ -291,7 +291,8 @@ class Column:
     ``scale`` the fixed-point exponent of float64 columns.
     """
 
-    __slots__ = ("kind", "_data", "_host", "scale", "dictionary", "lo", "hi", "dense", "sorted")
+    __slots__ = ("kind", "_data", "_host", "scale", "dictionary", "lo", "hi", "dense", "sorted",
+                 "loose")
 
     def __init__(self, kind: str, data, scale: int = 0, dictionary=None, lo: int = 0,
                  hi: int = -1, dense: bool = False):
@@ -324,6 +325,9 @@ class Column:
         # non-decreasing in row order: None = not yet checked (relops checks
         # it on the device when a group-by could use dense ranks)
         self.sorted = True if dense else None
+        # [lo, hi] proven but loose (an aggregate: rows x per-row range):
+        # overflow guards measure the values instead (relops._col_range)
+        self.loose = False
 
     @property
     def data(self):
@@ -418,8 +422,10 @@ class Column:
         return _lib.Column_(self.data.data_ptr(), self.scx_dtype, 0)
 
     def like(self, data, lo=None, hi=None) -> "Column":
-        return Column(self.kind, data, self.scale, self.dictionary,
-                      self.lo if lo is None else lo, self.hi if hi is None else hi)
+        c = Column(self.kind, data, self.scale, self.dictionary,
+                   self.lo if lo is None else lo, self.hi if hi is None else hi)
+        c.loose = self.loose and lo is None and hi is None
+        return c
 
     # ---- host views (D2H; inspection / result decoding) ----
     def host(self) -> np.ndarray:

@@ -1341,7 +1341,11 @@ struct Gen {
         // more rows with 2048-row tiles (measured: Q20 5.0 -> 4.1 ms, Q19
         // 2.6 -> 2.2, Q14 2.3 -> 1.9), the rest keep 1024 (Q5 3.7 vs 4.1,
         // Q3 5.1 vs 5.4)
-        const bool selective = P._pad > 0 && P._pad <= 12;
+        // (a cheap pre-predicate level tolerates a weaker filter: Q20's 1994
+        // shipdate year, 15%, prefers 2048-row tiles; Q5's 15% behind the
+        // orders probe + gathers does not)
+        const bool pre_level = P.pre.clause_mask != 0 && P.pre.n_atoms != 0;
+        const bool selective = P._pad > 0 && (P._pad <= 12 || (pre_level && P._pad <= 25));
         V = ev && *ev ? (atoi(ev) >= 8 ? 8 : atoi(ev) <= 2 ? 2 : 4)
                       : (selective && est(8) <= 110 * 1024 ? 8 : 4);
         SEG = 32 * V;

@@ -494,7 +494,7 @@ struct ScatterLaunch {
     // direct stores coalesce while a warp's 32 rows fall into few parts:
     // measured (1 GiB, 16-byte rows) 8 parts 0.626 vs 0.742 ms staged, 64
     // parts 2.29 vs 0.84 ms -- the staged kernel takes the wide fan-outs
-    static const char* env = getenv("SCX_PART_DIRECT");
+    const char* env = getenv("SCX_PART_DIRECT");
     const bool direct = env ? env[0] != '0' : K.np <= 8;
     if (direct) {
       const int64_t dcap = (int64_t)(g_sms > 0 ? g_sms : 148) * 8;

@@ -413,3 +413,41 @@ def test_dense_graph_replay_matches_golden(qid):
     assert_table_matches(eager, RES[key][qid], f"{qid}/eager")
     for i in range(3):
         assert_table_matches(graphs[0].replay(), RES[key][qid], f"{qid}/graph{i}")
+
+
+@pytest.mark.parametrize("parts", [1, 3, 8, 17])
+def test_partition_direct_equals_staged(parts, monkeypatch):
+    """partition.cu: the direct scatter (<= 8 parts by default) and the
+    shared-memory-staged scatter produce the same stable partition."""
+    import paper_2506_09226_b200 as P
+    rng = np.random.default_rng(parts)
+    n = 300_017
+    t = P.ColumnTable({"k": P.Column("int64", rng.integers(0, 1 << 40, n)),
+                       "v": P.Column("int64", np.arange(n)),
+                       "b": P.Column("int64", rng.integers(0, 200, n))})
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SCX_PART_DIRECT", mode)
+        parts_t = P.hash_partition(t, ["k"], parts)
+        outs[mode] = [(p.column("k").values.copy(), p.column("v").values.copy(),
+                       p.column("b").values.copy()) for p in parts_t]
+    for a, b in zip(outs["1"], outs["0"]):
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("qid", ["Q3", "Q5", "Q7", "Q9", "Q14", "Q17", "Q19", "Q20", "Q21"])
+def test_chunk_mode_equals_row_owner(qid, monkeypatch):
+    """jit.cu: the chunked dense kernels (selection queues) and the row-owner
+    kernels return identical results (SF0.1)."""
+    import paper_2506_09226_b200 as P
+    from paper_2506_09226_b200 import _lib
+    tables = device_tables("sf0.1_skew0.0")
+    got = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("SCX_CHUNK", mode)
+        _lib.load().scx_jit_clear_plans()
+        got[mode] = P.result_digest(P.reference_run(qid, tables))
+    monkeypatch.delenv("SCX_CHUNK")
+    _lib.load().scx_jit_clear_plans()
+    assert got["1"] == got["0"], qid

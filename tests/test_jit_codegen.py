@@ -237,3 +237,62 @@ def test_codegen_rejects_bad_descriptor(lib):
     P.base[0].ptr = 0x10001                # misaligned column
     assert lib.scx_pipeline_source(C.byref(P), None, 0) < 0
     assert b"aligned" in lib.scx_last_error()
+
+
+def _chunk_two_probes(sink):
+    # pre-predicate -> direct inner probe (a compaction point) -> semi bitmap
+    # probe on a gathered payload -> sink: three levels in chunk mode
+    P = _compact_probe(L.HT_DIRECT, L.JOIN_INNER)
+    P.n_probes = 2
+    pb = P.probe[1]
+    pb.kind = L.JOIN_SEMI
+    pb.key.n = 1; pb.key.slot[0] = 4; pb.key.bits[0] = 16; pb.key.lo[0] = 0
+    pb.table.kind = L.HT_BITMAP; pb.table.vals = 0x9000; pb.table.cap = 1 << 16
+    S = P.sink
+    if sink == "count":
+        S.kind = L.SINK_COUNT; S.count = 0xc000
+    elif sink == "dense":
+        S.kind = L.SINK_AGG_DENSE; S.n_cells = 1; S.n_measures = 1    # register accumulators
+        m = S.m[0]; m.op = L.AGG_SUM; m.n_terms = 1; m.cond_atom = -1
+        t = m.t[0]; t.coef = 1; t.n_factors = 1
+        t.f[0].a, t.f[0].b, t.f[0].slot, t.f[0]._pad = 0, 1, 2, 1
+        S.acc = 0x900000
+    return P
+
+
+@pytest.mark.parametrize("sink", ["compact", "count", "dense"])
+def test_chunk_mode_levels_compile(lib, sink):
+    P = _chunk_two_probes(sink)
+    n = lib.scx_pipeline_source(C.byref(P), None, 0)
+    assert n > 0, lib.scx_last_error()
+    buf = C.create_string_buffer(n + 1)
+    lib.scx_pipeline_source(C.byref(P), buf, n + 1)
+    src = buf.value.decode()
+    assert "// level 2" in src and "__ballot_sync" in src
+    assert lib.scx_pipeline_compile(C.byref(P)) == 0, lib.scx_last_error().decode()
+
+
+def test_chunk_tile_follows_selectivity_hint(lib):
+    def v_of(P):
+        n = lib.scx_pipeline_source(C.byref(P), None, 0)
+        buf = C.create_string_buffer(n + 1)
+        lib.scx_pipeline_source(C.byref(P), buf, n + 1)
+        return int(buf.value.decode().split("constexpr int V = ")[1].split(";")[0])
+    P = _chunk_two_probes("count")
+    P._pad = 3          # 3% survive the pre-predicate
+    assert v_of(P) == 8
+    P._pad = 60
+    assert v_of(P) == 4
+
+
+def test_selectivity_estimate():
+    from paper_2506_09226_b200 import relops as R
+    from paper_2506_09226_b200.data import generate
+    from paper_2506_09226_b200.table import Column, ColumnTable, date_to_days
+    li = generate(0.001, 0.0, 0).tables["lineitem"]
+    v = R.as_view(ColumnTable({n: Column.from_host_lazy(hc) for n, hc in li.columns.items()}))
+    sd = v["l_shipdate"]
+    month = R.filter_table(v, (sd >= date_to_days("1995-09-01")) & (sd < date_to_days("1995-10-01")))
+    assert 0.005 < R._first_stage_survival(month) < 0.02
+    modes = R.filter_table(v, v.isin("l_shipmode", ["AIR", "MAIL"]))
+    assert abs(R._first_stage_survival(modes) - 2 / 7) < 1e-9

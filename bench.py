@@ -568,7 +568,7 @@ def main() -> None:
     ap.add_argument("--no-pack", action="store_true",
                     help="e2e: send the narrowed columns unpacked")
     ap.add_argument("--shuffle-gib", type=float, default=1.0)
-    ap.add_argument("--streams", type=int, default=int(os.environ.get("SCX_BENCH_STREAMS", "3")),
+    ap.add_argument("--streams", type=int, default=int(os.environ.get("SCX_BENCH_STREAMS", "5")),
                     help="host threads / CUDA streams running the suite's queries concurrently")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -1071,19 +1071,29 @@ struct Gen {
         for (int u = 0; u < U; ++u) {
           o << "        const int lr" << sfx(u) << " = warp * " << SEG << " + c + " << 32 * u << " + lane;\n";
           o << "        bool ok" << sfx(u) << " = lr" << sfx(u) << " < rows;\n";
+          o << "        const bool act" << sfx(u) << " = true;\n";
         }
       } else {
         o << "#pragma unroll 1\n      for (u32 c = 0; c < qcnt; c += " << 32 * U << ") {\n";
         for (int u = 0; u < U; ++u) {
           const std::string q = "q" + sfx(u);
+          // act_u: warp-uniform, sub-row u holds at least one queued row
+          o << "        const bool act" << sfx(u) << " = c + " << 32 * u << "u < qcnt;\n";
           o << "        const u32 " << q << " = c + " << 32 * u << "u + lane;\n";
           o << "        bool ok" << sfx(u) << " = " << q << " < qcnt;\n";
-          o << "        const int lr" << sfx(u) << " = ok" << sfx(u) << " ? (int)((const u16*)" << qin << ")[" << q << "] : 0;\n";
+          o << "        int lr" << sfx(u) << " = 0;\n";
           for (int sl : have) {
             const char* t = ctype(P.slot_dtype[sl]);
-            o << "        const " << t << " pv" << sl << sfx(u) << " = ok" << sfx(u) << " ? ((const " << t
-              << "*)(" << qin << " + " << q_poff[sl] << "))[" << q << "] : (" << t << ")0;\n";
+            o << "        " << t << " pv" << sl << sfx(u) << " = (" << t << ")0;\n";
           }
+          o << "        if (ok" << sfx(u) << ") {\n";
+          o << "          lr" << sfx(u) << " = (int)((const u16*)" << qin << ")[" << q << "];\n";
+          for (int sl : have) {
+            const char* t = ctype(P.slot_dtype[sl]);
+            o << "          pv" << sl << sfx(u) << " = ((const " << t << "*)(" << qin << " + " << q_poff[sl]
+              << "))[" << q << "];\n";
+          }
+          o << "        }\n";
         }
       }
       std::vector<int> now = have;
@@ -1102,7 +1112,7 @@ struct Gen {
       if (!last) {
         for (int u = 0; u < U; ++u) {
           const std::string su = sfx(u);
-          o << "        { const u32 m = __ballot_sync(0xffffffffu, ok" << su << ");\n";
+          o << "        if (act" << su << ") { const u32 m = __ballot_sync(0xffffffffu, ok" << su << ");\n";
           o << "          if (ok" << su << ") {\n            const u32 pos = qn + __popc(m & lt);\n";
           o << "            ((u16*)" << qout << ")[pos] = (u16)lr" << su << ";\n";
           for (int sl : now) {
@@ -1155,7 +1165,7 @@ struct Gen {
       return;
     }
     if (S.kind == SCX_SINK_COMPACT) {
-      o << "        { const u32 m = __ballot_sync(0xffffffffu, " << ok << ");\n";
+      o << "        if (act" << cu << ") { const u32 m = __ballot_sync(0xffffffffu, " << ok << ");\n";
       o << "          if (" << ok << ") {\n            const u32 pos = wq + __popc(m & lt);\n";
       for (int i = 0; i < S.n_out; ++i) {
         const int s2 = S.out_slot[i];

@@ -634,7 +634,7 @@ def main() -> None:
                 per_query.append((q, e0, e1))
         return results
 
-    def suite_concurrent(tabs, per_query=None):
+    def suite_concurrent(tabs, per_query=None, ready=None, order=None):
         """The same 22 queries, pulled in order by `n_streams` host threads,
         each issuing on its own CUDA stream: one query's plan building and
         result finishing overlap another's kernels.  The step's end event
@@ -651,11 +651,13 @@ def main() -> None:
                 s = worker_streams[i]
                 with torch.cuda.stream(s):
                     s.wait_event(start)
-                    for q in assignment[i]:
+                    mine = [q for q in (order or QUERIES) if q in assignment[i]]
+                    for q in mine:
                         if per_query is not None:
                             e0 = torch.cuda.Event(enable_timing=True)
                             e0.record()
-                        ctx = DeviceContext(ep, tabs, "default", "default_keys", timed=False)
+                        ctx = DeviceContext(ep, tabs, "default", "default_keys", timed=False,
+                                            ready=ready)
                         r = PLAN_FUNCTIONS[q](ctx)
                         results[q] = r.materialize() if r is not None else None
                         if per_query is not None:
@@ -837,12 +839,17 @@ def main() -> None:
         if ep.n == 1:
             dev_tables, ready = upload_tables_async(host, copy_order)
             up_events = [ev for evs in ready.values() for ev in evs]
-            res = {}
-            for q in E2E_QUERY_ORDER:
-                ctx = DeviceContext(ep, dev_tables, "default", "default_keys", timed=False,
-                                    ready=ready)
-                r = PLAN_FUNCTIONS[q](ctx)
-                res[q] = r.materialize() if r is not None else None
+            if n_streams > 1:
+                # the same worker streams as the device-resident suite, each
+                # query waiting only for its own tables' upload events
+                res = suite_concurrent(dev_tables, ready=ready, order=E2E_QUERY_ORDER)
+            else:
+                res = {}
+                for q in E2E_QUERY_ORDER:
+                    ctx = DeviceContext(ep, dev_tables, "default", "default_keys", timed=False,
+                                        ready=ready)
+                    r = PLAN_FUNCTIONS[q](ctx)
+                    res[q] = r.materialize() if r is not None else None
         else:
             dev_tables, ready = upload_tables_async(host, copy_order)
             for evs in ready.values():

@@ -211,6 +211,7 @@ class DeviceContext:
         # table name -> CUDA event of its (asynchronous) upload: the first
         # access makes this stream wait for it (upload_tables_async)
         self.ready = ready
+        self._waited: set = set()
         self.variant = variant
         self.scheme = scheme
         self.p2p_broadcast = p2p_broadcast
@@ -229,11 +230,14 @@ class DeviceContext:
         return self.ep.rank == 0
 
     def table(self, name: str) -> ColumnTable:
-        if self.ready is not None and name in self.ready:
+        # the query's stream waits for the table's upload events once per
+        # context (the dict is shared by concurrent queries: never consumed)
+        if self.ready is not None and name in self.ready and name not in self._waited:
             import torch
-            evs = self.ready.pop(name)
+            evs = self.ready[name]
             for ev in (evs if isinstance(evs, (list, tuple)) else [evs]):
                 torch.cuda.current_stream().wait_event(ev)
+            self._waited.add(name)
         return self.tables[name]
 
     def filter(self, t, mask):

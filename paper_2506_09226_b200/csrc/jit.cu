@@ -1164,6 +1164,20 @@ struct Gen {
       o << "        cnt += " << ok << " ? 1ull : 0ull;\n";
       return;
     }
+    if (S.kind == SCX_SINK_BITMAP) {
+      // adjacent lanes hold consecutive surviving rows: a key equal to the
+      // previous lane's (clustered fact tables) sets its bit only once
+      o << "        if (act" << cu << ") { u64 bkey = SCX_EMPTY; bool bin = false;\n";
+      o << "          if (" << ok << ") {\n";
+      pack_key(S.gkey, "", nullptr, 0, "key", "kin");
+      o << "            bkey = key; bin = kin && key < bcap;\n";
+      o << "          }\n";
+      o << "          const u64 pk = __shfl_up_sync(0xffffffffu, bkey, 1);\n";
+      o << "          const bool pin = __shfl_up_sync(0xffffffffu, (int)bin, 1) != 0;\n";
+      o << "          if (bin && !(lane > 0 && pin && pk == bkey)) atomicOr(bits + (bkey >> 5), 1u << (bkey & 31));\n";
+      o << "        }\n";
+      return;
+    }
     if (S.kind == SCX_SINK_COMPACT) {
       o << "        if (act" << cu << ") { const u32 m = __ballot_sync(0xffffffffu, " << ok << ");\n";
       o << "          if (" << ok << ") {\n            const u32 pos = wq + __popc(m & lt);\n";
@@ -1334,7 +1348,7 @@ struct Gen {
       const bool forced = e && e[0] == '2';
       chunk = !(e && e[0] == '0') && P.n_probes > 0 && P.n_base > 0 && row_bytes > 0 && !coarse &&
               (S.kind == SCX_SINK_AGG_DENSE || S.kind == SCX_SINK_COMPACT ||
-               S.kind == SCX_SINK_COUNT) &&
+               S.kind == SCX_SINK_COUNT || S.kind == SCX_SINK_BITMAP) &&
               (forced || (cuts > 0 && !dense_priv));
       if (chunk) {
         int out_bytes = 0;

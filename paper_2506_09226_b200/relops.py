@@ -2024,17 +2024,28 @@ def sort_table(t, names: list[str], descending: set[str], limit: int | None = No
         return t.head(0)
     if n <= 1 or not names:
         return t if limit is None else t.head(limit)
-    specs = []
-    for name in names:
-        c = t.column(name)
-        desc = 1 if name in descending else 0
-        if c.kind == "dict":
-            specs.append((c, 0, _bits(len(c.dictionary) - 1), desc, _rank_tensor(c.dictionary)))
-        elif c.scx_dtype == L.SCX_F64:
-            specs.append((c, 0, 64, desc, None))
-        else:
-            lo, hi = _col_range(c)
-            specs.append((c, lo, _bits(hi - lo), desc, None))
+    def key_specs(tight: bool):
+        out = []
+        for name in names:
+            c = t.column(name)
+            desc = 1 if name in descending else 0
+            if c.kind == "dict":
+                out.append((c, 0, _bits(len(c.dictionary) - 1), desc, _rank_tensor(c.dictionary)))
+            elif c.scx_dtype == L.SCX_F64:
+                out.append((c, 0, 64, desc, None))
+            else:
+                lo, hi = _col_range(c, tight)
+                out.append((c, lo, _bits(hi - lo), desc, None))
+        return out
+
+    # an aggregate's proven range (rows x per-row range) spares a min/max pass
+    # + sync for a full sort, but a top-k's radix select narrows one 8-bit
+    # digit per round (one sync each) and needs the key in one 64-bit word:
+    # measure loose columns there, and whenever the proven key needs > 64 bits
+    specs = key_specs(False)
+    loose = any(sp[0].loose for sp in specs)
+    if loose and (limit is not None or sum(sp[2] for sp in specs) > 64):
+        specs = key_specs(True)
     words, cur, used = [], [], 0
     for sp in reversed(specs):            # least significant key first
         if sp[2] == 0:

@@ -251,6 +251,9 @@ def _chunk_two_probes(sink):
     S = P.sink
     if sink == "count":
         S.kind = L.SINK_COUNT; S.count = 0xc000
+    elif sink == "bitmap":
+        S.kind = L.SINK_BITMAP; S.gkey.n = 1; S.gkey.slot[0] = 0; S.gkey.bits[0] = 28
+        S.gkey.lo[0] = 1; S.gkeys = 0x1000; S.gcap = 1 << 28
     elif sink == "dense":
         S.kind = L.SINK_AGG_DENSE; S.n_cells = 1; S.n_measures = 1    # register accumulators
         m = S.m[0]; m.op = L.AGG_SUM; m.n_terms = 1; m.cond_atom = -1
@@ -260,7 +263,7 @@ def _chunk_two_probes(sink):
     return P
 
 
-@pytest.mark.parametrize("sink", ["compact", "count", "dense"])
+@pytest.mark.parametrize("sink", ["compact", "count", "dense", "bitmap"])
 def test_chunk_mode_levels_compile(lib, sink):
     P = _chunk_two_probes(sink)
     n = lib.scx_pipeline_source(C.byref(P), None, 0)

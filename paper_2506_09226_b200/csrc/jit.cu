@@ -607,6 +607,19 @@ struct Gen {
   // packed key (u64) + in-range flag into variables `kv` / `kin`
   void pack_key(const scx_keyspec& K, const char* r, const int32_t* glut, int lut_n,
                 const std::string& kv, const std::string& kin) {
+    // one 32-bit component (a probe on l_orderkey / l_partkey / ...): the range
+    // check and the offset in 32-bit arithmetic, zero-extended.  Exact when
+    // |lo| < 2^30 and bits <= 30: v - lo then lies in (-2^31 - 2^30, 2^31 + 2^30),
+    // so a negative difference wraps to >= 2^30 and fails the check.
+    static const bool key32 = !(getenv("SCX_KEY32") && getenv("SCX_KEY32")[0] == '0');
+    if (key32 && K.n == 1 && (!glut || glut[0] < 0) && ((K.xform & 0xff) == SCX_XFORM_NONE) &&
+        K.slot[0] >= 0 && K.slot[0] < P.n_slots && fits32_dt(P.slot_dtype[K.slot[0]]) &&
+        K.bits[0] >= 1 && K.bits[0] <= 30 && K.lo[0] > -(1ll << 30) && K.lo[0] < (1ll << 30)) {
+      o << "      const u32 " << kv << "32 = (u32)(" << val(K.slot[0], r) << ") - (u32)("
+        << (long long)K.lo[0] << "); const bool " << kin << " = " << kv << "32 < " << (1u << K.bits[0])
+        << "u; const u64 " << kv << " = (u64)" << kv << "32 << " << K.shift[0] << ";\n";
+      return;
+    }
     o << "      u64 " << kv << " = 0; bool " << kin << " = true;\n";
     for (int i = 0; i < K.n; ++i) {
       std::string v = "(" + key_value(K, i, r) + " - " + lit64(K.lo[i]) + ")";

@@ -611,7 +611,7 @@ struct Gen {
     // check and the offset in 32-bit arithmetic, zero-extended.  Exact when
     // |lo| < 2^30 and bits <= 30: v - lo then lies in (-2^31 - 2^30, 2^31 + 2^30),
     // so a negative difference wraps to >= 2^30 and fails the check.
-    static const bool key32 = !(getenv("SCX_KEY32") && getenv("SCX_KEY32")[0] == '0');
+    const bool key32 = !(getenv("SCX_KEY32") && getenv("SCX_KEY32")[0] == '0');
     if (key32 && K.n == 1 && (!glut || glut[0] < 0) && ((K.xform & 0xff) == SCX_XFORM_NONE) &&
         K.slot[0] >= 0 && K.slot[0] < P.n_slots && fits32_dt(P.slot_dtype[K.slot[0]]) &&
         K.bits[0] >= 1 && K.bits[0] <= 30 && K.lo[0] > -(1ll << 30) && K.lo[0] < (1ll << 30)) {

@@ -264,7 +264,8 @@ def _chunk_two_probes(sink):
 
 
 @pytest.mark.parametrize("sink", ["compact", "count", "dense", "bitmap"])
-def test_chunk_mode_levels_compile(lib, sink):
+def test_chunk_mode_levels_compile(lib, sink, monkeypatch):
+    monkeypatch.setenv("SCX_CHUNK", "2")      # bitmap sinks only when forced
     P = _chunk_two_probes(sink)
     n = lib.scx_pipeline_source(C.byref(P), None, 0)
     assert n > 0, lib.scx_last_error()

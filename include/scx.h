@@ -81,7 +81,8 @@ extern "C" {
 #define SCX_XFORM_YEAR  1      /* civil year of a date32 (days since 1970)    */
 
 /* lookup-table kinds */
-#define SCX_HT_HASH     0      /* open addressing, u64 keys, linear probing   */
+#define SCX_HT_HASH     0      /* open addressing, linear probing: keys = u64
+                                  slots[2*cap], slot h = {key, row} (16 B)    */
 #define SCX_HT_DIRECT   1      /* dense key range: vals[packed key]           */
 #define SCX_HT_BITMAP   2      /* semi/anti membership: bit [packed key] of
                                   the u32 words at vals, cap = key domain    */

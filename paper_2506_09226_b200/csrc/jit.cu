@@ -847,20 +847,21 @@ struct Gen {
       o << "          if (kin && key < cap) idx" << pi << "[r] = __ldg(vals + key);\n";
       o << "        }\n      }\n";
     } else {
-      o << "      const u64* keys = (const u64*)a.p[" << keys_p << "];\n";
+      // 16-byte {key, row} slots: key and row of a probe in one sector
+      o << "      const ulonglong2* slots = (const ulonglong2*)a.p[" << keys_p << "];\n";
       o << "      const u64 mask = cap - 1;\n";
-      o << "      u64 hk[V], hh[V], k0[V];\n";
+      o << "      u64 hk[V], hh[V]; ulonglong2 e0[V];\n";
       o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
-      o << "        idx" << pi << "[r] = SCX_NOROW; hk[r] = SCX_EMPTY; hh[r] = 0; k0[r] = SCX_EMPTY;\n";
+      o << "        idx" << pi << "[r] = SCX_NOROW; hk[r] = SCX_EMPTY; hh[r] = 0; e0[r].x = SCX_EMPTY; e0[r].y = 0;\n";
       o << "        if ((sel >> r) & 1u) {\n";
       pack_key(pb.key, "r", nullptr, 0, "key", "kin");
-      o << "          if (kin) { hk[r] = key; hh[r] = mix64(key) & mask; k0[r] = __ldg(keys + hh[r]); }\n";
+      o << "          if (kin) { hk[r] = key; hh[r] = mix64(key) & mask; e0[r] = __ldg(slots + hh[r]); }\n";
       o << "        }\n      }\n";
       o << "#pragma unroll\n      for (int r = 0; r < V; ++r) {\n";
       o << "        if (hk[r] == SCX_EMPTY) continue;\n";
-      o << "        u64 h = hh[r], k = k0[r];\n";
-      o << "        while (k != hk[r] && k != SCX_EMPTY) { h = (h + 1) & mask; k = __ldg(keys + h); }\n";
-      o << "        if (k == hk[r]) idx" << pi << "[r] = __ldg(vals + h);\n";
+      o << "        u64 h = hh[r]; ulonglong2 e = e0[r];\n";
+      o << "        while (e.x != hk[r] && e.x != SCX_EMPTY) { h = (h + 1) & mask; e = __ldg(slots + h); }\n";
+      o << "        if (e.x == hk[r]) idx" << pi << "[r] = (u32)e.y;\n";
       o << "      }\n";
     }
     o << "    }\n";
@@ -989,7 +990,7 @@ struct Gen {
     o << "          const u32* vals = (const u32*)a.p[" << vals_p << "]; (void)vals;\n";
     o << "          const u64 cap = a.p[" << cap_p << "];\n";
     if (pb.table.kind == SCX_HT_HASH)
-      o << "          const u64* keys = (const u64*)a.p[" << keys_p << "];\n"
+      o << "          const ulonglong2* slots = (const ulonglong2*)a.p[" << keys_p << "];\n"
         << "          const u64 mask = cap - 1;\n";
     for (int u = 0; u < U; ++u) {
       cu = sfx(u);
@@ -1004,9 +1005,9 @@ struct Gen {
         o << "            if (kin && key < cap) " << ix << " = __ldg(vals + key);\n";
       } else {
         o << "            if (kin) {\n";
-        o << "              u64 h = mix64(key) & mask, k = __ldg(keys + h);\n";
-        o << "              while (k != key && k != SCX_EMPTY) { h = (h + 1) & mask; k = __ldg(keys + h); }\n";
-        o << "              if (k == key) " << ix << " = __ldg(vals + h);\n";
+        o << "              u64 h = mix64(key) & mask; ulonglong2 e = __ldg(slots + h);\n";
+        o << "              while (e.x != key && e.x != SCX_EMPTY) { h = (h + 1) & mask; e = __ldg(slots + h); }\n";
+        o << "              if (e.x == key) " << ix << " = (u32)e.y;\n";
         o << "            }\n";
       }
       o << "          }\n";

@@ -238,14 +238,15 @@ _Pragma("unroll")
     for (int r = 0; r < R; ++r)
       if (live[r] && key[r] < cap) idx[r] = __ldg(vals + key[r]);
   } else {
-    const uint64_t* keys = reinterpret_cast<const uint64_t*>(pb.table.keys);
+    // 16-byte {key, row} slots (tables.cu lookup_build_kernel)
+    const uint64_t* slots = reinterpret_cast<const uint64_t*>(pb.table.keys);
     const uint64_t mask = pb.table.cap - 1;
     uint64_t h[R], k0[R];
     // issue all first probes before resolving any (memory-level parallelism)
 _Pragma("unroll")
     for (int r = 0; r < R; ++r) {
       h[r] = mix64(key[r]) & mask;
-      k0[r] = live[r] ? __ldg(keys + h[r]) : SCX_EMPTY_KEY;
+      k0[r] = live[r] ? __ldg(slots + 2 * h[r]) : SCX_EMPTY_KEY;
     }
 _Pragma("unroll")
     for (int r = 0; r < R; ++r) {
@@ -253,9 +254,9 @@ _Pragma("unroll")
       uint64_t hh = h[r], kk = k0[r];
       while (kk != key[r] && kk != SCX_EMPTY_KEY) {
         hh = (hh + 1) & mask;
-        kk = __ldg(keys + hh);
+        kk = __ldg(slots + 2 * hh);
       }
-      if (kk == key[r]) idx[r] = __ldg(vals + hh);
+      if (kk == key[r]) idx[r] = (uint32_t)__ldg(slots + 2 * hh + 1);
     }
   }
 _Pragma("unroll")

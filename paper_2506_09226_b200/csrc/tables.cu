@@ -11,11 +11,18 @@
 
 namespace scx {
 
-__global__ void lookup_clear_kernel(uint64_t* keys, uint32_t* vals, uint64_t cap) {
+// HASH tables are one array of 16-byte slots {u64 key, u64 row}: a probe
+// reads key and row in one sector (separate key / row arrays cost a second
+// dependent random access per hit).  DIRECT: vals[key] = row.
+__global__ void lookup_clear_kernel(uint64_t* slots, uint32_t* vals, uint64_t cap) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cap;
        i += (uint64_t)gridDim.x * blockDim.x) {
-    if (keys) keys[i] = SCX_EMPTY_KEY;
-    vals[i] = SCX_NO_ROW;
+    if (slots) {
+      slots[2 * i] = SCX_EMPTY_KEY;
+      slots[2 * i + 1] = SCX_NO_ROW;
+    } else {
+      vals[i] = SCX_NO_ROW;
+    }
   }
 }
 
@@ -57,13 +64,13 @@ __global__ void lookup_build_kernel(scx_lookup T, BuildCols C, scx_keyspec K, in
       const uint32_t prev = atomicExch(vals + key, (uint32_t)i);
       if (prev != SCX_NO_ROW) atomicOr(flags + 1, 1u);
     } else {
-      uint64_t* keys = reinterpret_cast<uint64_t*>(T.keys);
+      uint64_t* slots = reinterpret_cast<uint64_t*>(T.keys);
       const uint64_t mask = T.cap - 1;
       uint64_t h = mix64(key) & mask;
       for (uint64_t p = 0; p <= mask; ++p) {
         const unsigned long long prev =
-            atomicCAS(reinterpret_cast<unsigned long long*>(keys + h), SCX_EMPTY_KEY, key);
-        if (prev == SCX_EMPTY_KEY) { vals[h] = (uint32_t)i; break; }
+            atomicCAS(reinterpret_cast<unsigned long long*>(slots + 2 * h), SCX_EMPTY_KEY, key);
+        if (prev == SCX_EMPTY_KEY) { slots[2 * h + 1] = (uint64_t)i; break; }
         if (prev == key) { atomicOr(flags + 1, 1u); break; }   // duplicate key
         h = (h + 1) & mask;
       }
@@ -291,7 +298,8 @@ extern "C" int scx_minmax(scx_column col, int64_t n, int64_t* out, void* stream)
 static int launch_grid(int64_t n) { return grid_for(n, 256, 148 * 16); }
 
 extern "C" int scx_lookup_clear(const scx_lookup* T, void* stream) {
-  if (!T || !T->vals || (T->kind == SCX_HT_HASH && (!T->keys || (T->cap & (T->cap - 1))))) {
+  if (!T || (T->kind != SCX_HT_HASH && !T->vals) ||
+      (T->kind == SCX_HT_HASH && (!T->keys || (T->cap & (T->cap - 1))))) {
     set_error("lookup_clear: bad table (hash capacity must be a power of two)");
     return SCX_EINVAL;
   }

@@ -173,10 +173,11 @@ class Lookup:
                 cap *= 2
             self.lk.kind = L.HT_HASH
             self.lk.cap = cap
-            self._keys = alloc(cap, np.uint64)
-            self._vals = alloc(cap, np.uint32)
+            # 16-byte {key, row} slots: a probe reads both in one sector
+            self._keys = alloc(2 * cap, np.uint64)
+            self._vals = None
             self.lk.keys = self._keys.data_ptr()
-            self.lk.vals = self._vals.data_ptr()
+            self.lk.vals = 0
         if self.keys and set(self.keys) == set(getattr(table, "unique_keys", ())):
             self._unique = True            # group-by output keyed on these columns
         self._flags = alloc(4, np.uint32)

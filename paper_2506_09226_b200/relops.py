@@ -1976,6 +1976,10 @@ def _col_range(c: Column, tight: bool = False) -> tuple[int, int]:
     L.call("scx_fill_rows", _ptr(mm), 1, 2, (C.c_int64 * 2)(INT64_MAX, INT64_MIN), _stream())
     L.call("scx_minmax", c.scx(), c.row_count, _ptr(mm), _stream())
     lo, hi = (int(x) for x in _to_host(mm))
+    if c.scx_dtype != L.SCX_F64 and hi >= lo:
+        # columns are immutable: the measured range replaces the proven one,
+        # so later guards / sorts over this column need no second pass + sync
+        c.lo, c.hi, c.loose = lo, hi, False
     return lo, hi
 
 

@@ -454,8 +454,30 @@ def codes_where(ref: ColRef, fn) -> Pred:
     """Rows whose dictionary string satisfies fn (queries.py:23-29)."""
     if ref.col.kind != "dict":
         raise SchemaError(f"codes_where expects a dict column, {ref.name} is {ref.col.kind}")
-    codes = frozenset(i for i, s in enumerate(ref.col.dictionary) if fn(s))
+    codes = _codes_cached(ref.col.dictionary, fn)
     return Pred.atom(Atom("set", ref.name, codes=codes))
+
+
+_CODES_CACHE: dict = {}
+
+
+def _codes_cached(dictionary, fn) -> frozenset:
+    """Evaluating a LIKE-style predicate over a dictionary is host time on
+    every run of a query; the drivers pass the same lambda code with the same
+    captured values each time, so the code set is memoised on (dictionary,
+    code object, closure values)."""
+    try:
+        cells = tuple(c.cell_contents for c in (fn.__closure__ or ()))
+        key = (id(dictionary), fn.__code__, cells, fn.__defaults__)
+        hash(key)
+    except (AttributeError, TypeError, ValueError):
+        return frozenset(i for i, s in enumerate(dictionary) if fn(s))
+    hit = _CODES_CACHE.get(key)
+    if hit is not None and hit[0] is dictionary:
+        return hit[1]
+    codes = frozenset(i for i, s in enumerate(dictionary) if fn(s))
+    _CODES_CACHE[key] = (dictionary, codes)
+    return codes
 
 
 # ---------------------------------------------------------------------------

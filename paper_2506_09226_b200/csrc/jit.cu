@@ -1473,19 +1473,7 @@ struct Gen {
         const char* rb = getenv("SCX_TMA_RING_KB");
         // (chunk mode with a 48 KB ring measured slower than 32 KB: 69.0 vs
         // 66.9 ms over the probe-heavy queries -- fewer CTAs per SM)
-        size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : 32) * 1024;
-        if (chunk && !(rb && *rb)) {
-          // chunk mode holds a stage for the whole tile: give the ring every
-          // byte that still lets 3 CTAs share an SM (~74 KB each incl. the
-          // queues / out buffers); ncu showed the consumers spinning on the
-          // full barrier with 2 stages (10% of issued instructions, Q3)
-          const int seg = 32 * V;
-          size_t other = (size_t)16 * seg * (2 + payload_bytes) + sink_smem + 2048;
-          if (S.kind == SCX_SINK_COMPACT)
-            for (int i = 0; i < S.n_out; ++i) other += (size_t)8 * seg * dtype_size(S.out[i].dtype);
-          const size_t cap_b = (size_t)74 * 1024;
-          if (cap_b > other && cap_b - other > ring_budget) ring_budget = cap_b - other;
-        }
+        const size_t ring_budget = (size_t)(rb && *rb ? atoi(rb) : 32) * 1024;
         int st = (int)(ring_budget / stage);
         tma_stages = st < 2 ? 2 : (st > 6 ? 6 : st);
         ring_off = (sink_smem + 127) & ~(size_t)127;

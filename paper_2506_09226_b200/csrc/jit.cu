@@ -1034,6 +1034,53 @@ struct Gen {
     }
   }
 
+  // Monotone identity / direct probes (table._pad == 1: the probe key is a
+  // sorted base column, l_orderkey -> orders): the tile's key range is known
+  // from its first and last staged key, so one thread issues an L2 bulk
+  // prefetch of that build range for THIS tile before level 0 runs; by the
+  // time the surviving rows gather at a later level the lines are in L2.
+  // (Reading the keys from shared memory costs nothing like the row-owner
+  // variant's dependent global loads, SCX_GATHER_PF.)
+  void emit_chunk_prefetch() {
+    const char* e = getenv("SCX_CHUNK_PF");
+    if (e && e[0] == '0') return;
+    for (int pi = 0; pi < P.n_probes; ++pi) {
+      const scx_probe& pb = P.probe[pi];
+      const int tk = pb.table.kind;
+      if ((tk != SCX_HT_IDENTITY && tk != SCX_HT_DIRECT) || pb.table._pad != 1) continue;
+      if (pb.key.n != 1 || pb.key.slot[0] < 0 || pb.key.slot[0] >= P.n_base ||
+          pb.key.shift[0] != 0 || (pb.key.xform & 0xff) != SCX_XFORM_NONE)
+        continue;
+      struct Arr { int p; int w; };
+      std::vector<Arr> arrs;
+      if (tk == SCX_HT_DIRECT) {
+        arrs.push_back({param(pb.table.vals), 4});
+      } else if (pb.kind == SCX_JOIN_INNER || pb.kind == SCX_JOIN_LEFT) {
+        for (int j = 0; j < pb.n_payload; ++j)
+          arrs.push_back({param(pb.payload[j].ptr), dtype_size(pb.payload[j].dtype)});
+      }
+      if (arrs.empty()) continue;
+      const int cap_p = param(pb.table.cap);
+      const int sl = pb.key.slot[0];
+      const std::string lr0 = "lr_pf0", lr1 = "lr_pf1";
+      o << "    if (tid == 0 && rows > 0) {   // L2 prefetch of probe " << pi << "'s build range\n";
+      o << "      const int lr_pf0 = 0, lr_pf1 = rows - 1;\n";
+      cu = "_pf0";
+      o << "      const i64 k0 = (i64)" << val(sl, "") << " - " << lit64(pb.key.lo[0]) << ";\n";
+      cu = "_pf1";
+      o << "      const i64 k1 = (i64)" << val(sl, "") << " - " << lit64(pb.key.lo[0]) << ";\n";
+      cu.clear();
+      o << "      if (k0 >= 0 && k1 >= k0 && (u64)k1 < a.p[" << cap_p << "] && k1 - k0 < 262144ll) {\n";
+      for (const Arr& A : arrs) {
+        o << "        { const u64 b = a.p[" << A.p << "];\n";
+        o << "          const u64 s0 = (b + (u64)k0 * " << A.w << "ull) & ~15ull;\n";
+        o << "          const u64 s1 = (b + (u64)(k1 + 1) * " << A.w << "ull + 15ull) & ~15ull;\n";
+        o << "          if (s0 >= (b & ~15ull)) l2_prefetch((const void*)s0, (u32)(s1 - s0)); }\n";
+      }
+      o << "      }\n    }\n";
+    }
+  }
+
   // one tile: levels separated by compaction points (after every stage that
   // can drop rows and is followed by another probe), then the sink
   void emit_chunk(int64_t tile_rows, bool dense_priv, bool dense_reg, int NC, int NW, int M,
@@ -1056,6 +1103,7 @@ struct Gen {
     o << "    unsigned char* qbuf0 = dsm + " << q_off << " + (u32)warp * " << qb_bytes << "u;\n";
     o << "    unsigned char* qbuf1 = dsm + " << q_off << " + (u32)(" << kTPB / 32 << " + warp) * " << qb_bytes << "u;\n";
     o << "    (void)qbuf0; (void)qbuf1;\n";
+    emit_chunk_prefetch();
     if (S.kind == SCX_SINK_COMPACT)
       o << "    unsigned char* obuf = dsm + " << ob_off << " + (u32)warp * " << ob_bytes << "u;\n"
         << "    u32 wq = 0;\n";

@@ -519,6 +519,11 @@ int scx_pack_host(const void* in, int dtype, int64_t n, int64_t lo, int k, int d
                   uint32_t* out_words, int64_t* out_bases, int n_threads);
 int scx_unpack(const uint32_t* words_dev, int64_t n, int k, int64_t lo, int encoding,
                const int64_t* bases_dev, scx_column out, void* stream);
+/* Column-relative packing (the host packs value - ref[i] - lo in k bits):
+ * out[i] = ref[i] + lo + field; ref is an already unpacked column of the same
+ * table (l_receiptdate against l_shipdate: 5 bits instead of 12). */
+int scx_unpack_diff(const uint32_t* words_dev, int64_t n, int k, int64_t lo, scx_column ref,
+                    scx_column out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -127,6 +127,17 @@ __global__ void __launch_bounds__(kT) unpack_delta_kernel(const uint32_t* __rest
   }
 }
 
+// column-relative: value = ref[i] + lo + field (a date stored against another
+// date of the same row: l_receiptdate - l_shipdate in [1, 30] packs in 5 bits)
+template <typename T>
+__global__ void unpack_diff_kernel(const uint32_t* __restrict__ words, int64_t n, int k, int64_t lo,
+                                   scx_column ref, T* __restrict__ out) {
+  const void* r = reinterpret_cast<const void*>(ref.ptr);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (T)(load_i64(r, ref.dtype, i) + lo + (int64_t)(k ? field(words, i, k) : 0));
+}
+
 template <typename T>
 __global__ void iota_kernel(int64_t n, int64_t lo, T* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -156,6 +167,12 @@ template <typename T> struct DeltaL {
   static void run(dim3 g, dim3 b, cudaStream_t st, const uint32_t* w, int64_t n, int k,
                   const int64_t* bases, void* out) {
     unpack_delta_kernel<T><<<g, b, 0, st>>>(w, n, k, bases, static_cast<T*>(out));
+  }
+};
+template <typename T> struct DiffL {
+  static void run(dim3 g, dim3 b, cudaStream_t st, const uint32_t* w, int64_t n, int k, int64_t lo,
+                  scx_column ref, void* out) {
+    unpack_diff_kernel<T><<<g, b, 0, st>>>(w, n, k, lo, ref, static_cast<T*>(out));
   }
 };
 template <typename T> struct IotaL {
@@ -243,5 +260,20 @@ extern "C" int scx_unpack(const uint32_t* words, int64_t n, int k, int64_t lo, i
                                      lo, o);
     SCX_CHECK_LAUNCH("unpack_for_kernel");
   }
+  return SCX_OK;
+}
+
+extern "C" int scx_unpack_diff(const uint32_t* words, int64_t n, int k, int64_t lo, scx_column ref,
+                               scx_column out, void* stream) {
+  if (n < 0 || k < 0 || k > 32 || dtype_size(out.dtype) == 0 || dtype_size(ref.dtype) == 0 ||
+      (n > 0 && (!out.ptr || !ref.ptr)) || (n > 0 && k > 0 && !words)) {
+    set_error("scx_unpack_diff: bad arguments (n=%lld k=%d)", (long long)n, k);
+    return SCX_EINVAL;
+  }
+  if (n == 0) return SCX_OK;
+  codec::launch_typed<codec::DiffL>(out.dtype, codec::grid_for(n), codec::kT,
+                                    static_cast<cudaStream_t>(stream), words, n, k, lo, ref,
+                                    reinterpret_cast<void*>(out.ptr));
+  SCX_CHECK_LAUNCH("unpack_diff_kernel");
   return SCX_OK;
 }

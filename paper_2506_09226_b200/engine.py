@@ -421,15 +421,27 @@ def upload_tables_async(host: dict, order=None, stream=None):
     for tname in (order or list(host)):
         cols = {}
         used = set()
-        for cname, (hc, pinned) in host[tname].items():
-            cs = streams[k % 2]
-            k += 1
+        stream_of = {}
+        # column-relative (DIFF) columns go after their reference, on the
+        # reference's copy stream (stream order: the reference is unpacked first)
+        items = list(host[tname].items())
+        is_diff = lambda it: isinstance(it[1][1], PinnedPacked) and it[1][1].col.ref is not None
+        for cname, (hc, pinned) in [it for it in items if not is_diff(it)] + \
+                [it for it in items if is_diff(it)]:
+            ref = pinned.col.ref if isinstance(pinned, PinnedPacked) else None
+            if ref is not None:
+                cs = stream_of[ref]
+            else:
+                cs = streams[k % 2]
+                k += 1
+            stream_of[cname] = cs
             used.add(id(cs))
             if isinstance(pinned, PinnedPacked):
                 # packed words cross PCIe, scx_unpack rebuilds the column
                 nb = scratch_bytes(pinned)
                 buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs,
-                                    arena[aoff:aoff + nb])
+                                    arena[aoff:aoff + nb],
+                                    cols[ref].data if ref is not None else None)
                 aoff += nb
             else:
                 buf = alloc(hc.row_count, hc.values.dtype)
@@ -440,6 +452,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
             if hc.sorted:
                 col.sorted = True
             cols[cname] = col
+        cols = {c: cols[c] for c, _ in items}           # the host table's column order
         evs = []
         for cs in streams:
             if id(cs) in used:

@@ -24,14 +24,27 @@ def ds():
 def test_dataset_columns_round_trip_and_shrink(ds):
     narrow = packed = 0
     for t, ht in ds.tables.items():
+        pt = codec.pack_table(ht, threads=3)
         for c, hc in ht.columns.items():
-            pc = codec.pack_column(hc, threads=3)
-            got = codec.unpack_host(pc)
+            pc = pt[c]
+            got = codec.unpack_host(pc, ht.columns[pc.ref].values if pc.ref else None)
             assert got.dtype == hc.values.dtype, (t, c)
             assert np.array_equal(got, hc.values), (t, c, pc.encoding, pc.k)
             narrow += hc.values.nbytes
             packed += pc.nbytes
     assert packed < 0.6 * narrow, (packed, narrow)
+
+
+def test_column_relative_dates(ds):
+    li = ds.tables["lineitem"]
+    pt = codec.pack_table(li, threads=2)
+    dates = ["l_shipdate", "l_commitdate", "l_receiptdate"]
+    diffs = [c for c in dates if pt[c].encoding == codec.DIFF]
+    assert len(diffs) == 2 and min(pt[c].k for c in diffs) <= 5
+    for c in diffs:
+        assert pt[pt[c].ref].encoding != codec.DIFF          # no chains
+        got = codec.unpack_host(pt[c], li.columns[pt[c].ref].values)
+        assert np.array_equal(got, li.columns[c].values)
 
 
 def test_sorted_orderkey_uses_one_bit_deltas(ds):

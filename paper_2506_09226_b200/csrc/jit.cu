@@ -435,6 +435,8 @@ struct Gen {
   std::vector<int> q_poff;      // payload slot -> byte offset inside a queue buffer
   std::vector<int> ob_coff;     // COMPACT output column -> offset inside a warp's out buffer
   uint32_t early = 0xffffffffu;  // late materialisation: base columns loaded before the first filter
+  uint32_t staged = 0xffffffffu; // base columns the TMA stages in shared memory (chunk: see chunk_late)
+  int first_cut = -2;           // chunk late mode: the first filtering stage (-1 = pre-predicate)
   bool late = false;
   std::string cu;               // chunk mode: variable suffix of the current sub-row ("_2")
   int U = 1;                    // chunk mode: sub-rows (32-row chunks) per lane per iteration
@@ -477,8 +479,15 @@ struct Gen {
         else snprintf(b, sizeof(b), "pv%d%s", s, cu.c_str());
         return b;
       }
-      const long long off = (long long)stage_off(s);
       const char* l = cu.c_str();
+      if (!((staged >> s) & 1u)) {
+        // late column (not staged): this lane's row straight from HBM / L2
+        const char* t = ctype(dt);
+        if (fits32_dt(dt)) snprintf(b, sizeof(b), "((i32)__ldg((const %s*)a.p[%d] + (trow0 + lr%s)))", t, col_p[s], l);
+        else snprintf(b, sizeof(b), "((%s)__ldg((const %s*)a.p[%d] + (trow0 + lr%s)))", t, t, col_p[s], l);
+        return b;
+      }
+      const long long off = (long long)stage_off(s);
       switch (dt) {
         case SCX_I8: snprintf(b, sizeof(b), "((i32)*(const i8*)(stg + %lldu + lr%s))", off, l); break;
         case SCX_U8: snprintf(b, sizeof(b), "((i32)*(const u8*)(stg + %lldu + lr%s))", off, l); break;
@@ -705,7 +714,8 @@ struct Gen {
   // byte offset of base column s inside one load stage ([col][16B piece][thread])
   int64_t stage_off(int s) {
     int64_t off = 0;
-    for (int c = 0; c < s; ++c) off += (int64_t)kTPB * V * dtype_size(P.base[c].dtype);
+    for (int c = 0; c < s; ++c)
+      if ((staged >> c) & 1u) off += (int64_t)kTPB * V * dtype_size(P.base[c].dtype);
     return off;
   }
   int64_t stage_bytes() { return stage_off(P.n_base); }
@@ -1116,8 +1126,11 @@ struct Gen {
     };
     std::vector<std::pair<int, int>> levels;      // [first item, last item]; -1 = pre, n_probes = post
     int start = -1;
-    for (int i = -1; i < P.n_probes - 1; ++i)
-      if (filters(i)) { levels.push_back({start, i}); start = i + 1; }
+    for (int i = -1; i < P.n_probes; ++i)
+      if ((i < P.n_probes - 1 && filters(i)) || i == first_cut) {
+        levels.push_back({start, i});
+        start = i + 1;
+      }
     levels.push_back({start, P.n_probes});
     std::vector<int> have;                        // payload slots carried into the level
     o << "    u32 qcnt = 0; (void)qcnt;\n";
@@ -1408,19 +1421,56 @@ struct Gen {
           ++cuts;
       }
       const bool forced = e && e[0] == '2';
+      // late columns: when the first filtering stage is very selective (host
+      // estimate <= 15%), only the columns it reads are staged by the TMA; the
+      // survivors read the others from memory at the next level (Q9: 5% of
+      // lineitem passes the green-part semi join, 5 of its 6 columns are then
+      // read for those rows only).  Gives a level boundary even when that
+      // stage is the last probe.
+      {
+        const char* el = getenv("SCX_CHUNK_LATE");
+        const bool pre_on = P.pre.clause_mask != 0 && P.pre.n_atoms != 0;
+        int f = -2;
+        if (pre_on) f = -1;
+        else
+          for (int i = 0; i < P.n_probes && f == -2; ++i) {
+            const scx_probe& pb = P.probe[i];
+            if ((pb.after.clause_mask != 0 && pb.after.n_atoms != 0) || pb.kind == SCX_JOIN_SEMI ||
+                pb.kind == SCX_JOIN_ANTI || (pb.kind == SCX_JOIN_INNER && pb.table.kind != SCX_HT_IDENTITY))
+              f = i;
+          }
+        uint32_t m = 0;
+        if (f != -2) {
+          m = pred_cols(P.pre);
+          for (int i = 0; i <= f; ++i) {
+            const scx_probe& pb = P.probe[i];
+            for (int k = 0; k < pb.key.n && k < SCX_MAX_KEYS; ++k)
+              if (pb.key.slot[k] >= 0 && pb.key.slot[k] < P.n_base) m |= 1u << pb.key.slot[k];
+            m |= pred_cols(pb.after);
+          }
+        }
+        const uint32_t all = P.n_base >= 32 ? 0xffffffffu : ((1u << P.n_base) - 1u);
+        const bool late_ok = !(el && el[0] == '0') && f != -2 && m != 0 && (m & all) != all &&
+                             P._pad > 0 && P._pad <= 15 && S.kind != SCX_SINK_BITMAP;
+        if (late_ok) { first_cut = f; staged = m; ++cuts; }
+      }
       chunk = !(e && e[0] == '0') && P.n_probes > 0 && P.n_base > 0 && row_bytes > 0 && !coarse &&
               (S.kind == SCX_SINK_AGG_DENSE || S.kind == SCX_SINK_COMPACT ||
                S.kind == SCX_SINK_COUNT || (forced && S.kind == SCX_SINK_BITMAP)) &&
-              (forced || (cuts > 0 && !dense_priv));
+              (forced || (cuts > 0 && (!dense_priv || first_cut != -2)));
+      if (!chunk) { staged = 0xffffffffu; first_cut = -2; }
       // (bitmap sinks measured slower in chunk mode: Q21 7.75 -> 8.42 ms;
       // SCX_CHUNK=2 forces the mode for every eligible kernel)
       if (chunk) {
         int out_bytes = 0;
         if (S.kind == SCX_SINK_COMPACT)
           for (int i = 0; i < S.n_out; ++i) out_bytes += dtype_size(S.out[i].dtype);
+        int staged_bytes = 0;
+        for (int c = 0; c < P.n_base; ++c)
+          if ((staged >> c) & 1u) staged_bytes += dtype_size(P.base[c].dtype);
         auto est = [&](int v) {          // ring (2 stages) + queue buffers + out buffers
           const int seg = 32 * v;
-          return (size_t)2 * kTPB * v * row_bytes + (size_t)16 * seg * (2 + payload_bytes) +
+          return (size_t)2 * kTPB * v * staged_bytes + (size_t)16 * seg * (2 + payload_bytes) +
                  (size_t)8 * seg * out_bytes + 4096;
         };
         const char* ev = getenv("SCX_CHUNK_V");
@@ -1517,7 +1567,7 @@ struct Gen {
                                         (S.kind == SCX_SINK_COMPACT && !hash_probe)))) &&
                       !pipe && P.n_base > 0 && row_bytes > 0);
       if (tma) {
-        const size_t stage = (size_t)kTPB * V * row_bytes;
+        const size_t stage = (size_t)stage_bytes();    // staged columns only (chunk late mode)
         const char* rb = getenv("SCX_TMA_RING_KB");
         // (chunk mode with a 48 KB ring measured slower than 32 KB: 69.0 vs
         // 66.9 ms over the probe-heavy queries -- fewer CTAs per SM)
@@ -1578,7 +1628,7 @@ struct Gen {
     for (int c = 0; c < P.n_base; ++c) col_p.push_back(param(P.base[c].ptr));
     if (tma) {
       const int S_ = tma_stages;
-      const int64_t stage = (int64_t)kTPB * V * row_bytes;
+      const int64_t stage = stage_bytes();
       const bool cmp = S.kind == SCX_SINK_COMPACT;
       o << "  const u32 ring = smem_u32(dsm + " << ring_off << ");\n";
       o << "  const u32 bars = smem_u32(dsm + " << bar_off << ");   // full[s] = bars+8s (producer + tx), empty[s] = bars+8(S+s) (256 consumer threads)\n";
@@ -1603,11 +1653,13 @@ struct Gen {
       o << "        const i64 rows = n - r0 < " << tile_rows << "ll ? n - r0 : " << tile_rows << "ll;\n";
       o << "        u32 tot = 0;\n";
       for (int c = 0; c < P.n_base; ++c) {
+        if (!((staged >> c) & 1u)) continue;
         const int w = dtype_size(P.base[c].dtype);
         o << "        const u32 b" << c << " = (u32)((rows * " << w << " + 15) & ~15ll); tot += b" << c << ";\n";
       }
       o << "        mb_expect_tx(bars + 8u * st, tot);\n";
       for (int c = 0; c < P.n_base; ++c) {
+        if (!((staged >> c) & 1u)) continue;
         const int w = dtype_size(P.base[c].dtype);
         o << "        bulk_g2s(ring + (u32)st * " << stage << "u + " << stage_off(c) << "u, (const char*)a.p["
           << col_p[c] << "] + r0 * " << w << "ll, b" << c << ", bars + 8u * st);\n";

@@ -300,3 +300,19 @@ def test_selectivity_estimate():
     assert 0.005 < R._first_stage_survival(month) < 0.02
     modes = R.filter_table(v, v.isin("l_shipmode", ["AIR", "MAIL"]))
     assert abs(R._first_stage_survival(modes) - 2 / 7) < 1e-9
+
+
+def test_chunk_late_columns(lib):
+    # one selective semi probe feeding a compaction: only the probe key is
+    # staged; the other outputs are read for the survivors at level 1
+    P = _compact_probe(L.HT_BITMAP, L.JOIN_SEMI)
+    P.pre.n_atoms = 0; P.pre.clause_mask = 0
+    P._pad = 4
+    n = lib.scx_pipeline_source(C.byref(P), None, 0)
+    assert n > 0, lib.scx_last_error()
+    buf = C.create_string_buffer(n + 1)
+    lib.scx_pipeline_source(C.byref(P), buf, n + 1)
+    src = buf.value.decode()
+    assert "// level 1" in src and "__ldg((const i32*)a.p[" in src
+    assert src.count("bulk_g2s(ring") == 1          # the key column only
+    assert lib.scx_pipeline_compile(C.byref(P)) == 0, lib.scx_last_error().decode()

@@ -1450,8 +1450,18 @@ struct Gen {
           }
         }
         const uint32_t all = P.n_base >= 32 ? 0xffffffffu : ((1u << P.n_base) - 1u);
+        int late_b = 0;
+        for (int c = 0; c < P.n_base; ++c)
+          if (!((m >> c) & 1u)) late_b += dtype_size(P.base[c].dtype);
+        // measured per query (profiles/r2_chunk_sweeps.txt, r2af): gains with
+        // aggregate sinks and most of the row late (Q5 3.76 -> 3.40 ms, Q14
+        // 1.86 -> 1.56, Q19 2.16 -> 1.81); losses with compaction sinks (Q9
+        // 8.71 -> 8.99, Q20 3.75 -> 4.52), private accumulators (Q8 4.37 ->
+        // 6.43) and a small late share (Q12: 4 of 11 bytes, 2.27 -> 2.51)
         const bool late_ok = !(el && el[0] == '0') && f != -2 && m != 0 && (m & all) != all &&
-                             P._pad > 0 && P._pad <= 15 && S.kind != SCX_SINK_BITMAP;
+                             P._pad > 0 && P._pad <= 15 &&
+                             (S.kind == SCX_SINK_AGG_DENSE || S.kind == SCX_SINK_COUNT) &&
+                             !dense_priv && 5 * late_b >= 2 * row_bytes;
         if (late_ok) { first_cut = f; staged = m; ++cuts; }
       }
       chunk = !(e && e[0] == '0') && P.n_probes > 0 && P.n_base > 0 && row_bytes > 0 && !coarse &&

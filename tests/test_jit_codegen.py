@@ -303,11 +303,18 @@ def test_selectivity_estimate():
 
 
 def test_chunk_late_columns(lib):
-    # one selective semi probe feeding a compaction: only the probe key is
-    # staged; the other outputs are read for the survivors at level 1
+    # one selective semi probe feeding an aggregate: only the probe key is
+    # staged; the measure's columns are read for the survivors at level 1
     P = _compact_probe(L.HT_BITMAP, L.JOIN_SEMI)
     P.pre.n_atoms = 0; P.pre.clause_mask = 0
     P._pad = 4
+    S = P.sink
+    S.kind = L.SINK_AGG_DENSE; S.n_cells = 1; S.n_measures = 1
+    m = S.m[0]; m.op = L.AGG_SUM; m.n_terms = 1; m.cond_atom = -1
+    t = m.t[0]; t.coef = 1; t.n_factors = 2
+    t.f[0].a, t.f[0].b, t.f[0].slot, t.f[0]._pad = 0, 1, 2, 1
+    t.f[1].a, t.f[1].b, t.f[1].slot, t.f[1]._pad = 0, 1, 3, 1
+    S.acc = 0x900000
     n = lib.scx_pipeline_source(C.byref(P), None, 0)
     assert n > 0, lib.scx_last_error()
     buf = C.create_string_buffer(n + 1)

@@ -8,8 +8,9 @@ results materialised on the root.  `value` = device-timed suite
 seconds (CUDA events on the launching stream, barrier + synchronize on both
 sides, max over ranks).  `e2e` = the same suite through the public API with
 the touched base columns copied H2D from pinned host memory inside the timed
-region, results copied back.  `roofline` = the dominant scan kernel (Q1's
-fused pipeline) vs measured HBM copy bandwidth.  `cpu_baseline` = the oracle
+region, results copied back.  `roofline` = the longest fused-scan launch of a
+single-stream suite pass (the kernel with the largest share of the step) vs the
+measured HBM copy bandwidth; `roofline_q1_scan` = Q1's scan + group-by.  `cpu_baseline` = the oracle
 port of the reference (oracle/ref.py, numpy, 1 core) on a bounded SF sample,
 scaled linearly to `sf`.
 
@@ -913,6 +914,44 @@ def main() -> None:
                 "alg_bytes_per_launch": q1_bytes, "launch_ms": round(k_ms, 4),
                 "peak_source": pk["source"]}
 
+    # ---- the dominant kernel: every fused-scan launch of one single-stream
+    # suite pass timed with CUDA events (L2 flushed before each query); the
+    # longest launch is the kernel with the largest share of the step ----
+    dom = None
+    if ep.n == 1:
+        launches = []
+        for q in QUERIES:
+            flush_l2()
+            torch.cuda.synchronize()
+            R.LAUNCH_LOG, R.LAUNCH_BYTES = [], []
+            try:
+                ctx = DeviceContext(ep, tables, "default", "default_keys", timed=False)
+                r = PLAN_FUNCTIONS[q](ctx)
+                if r is not None:
+                    r.materialize()
+                torch.cuda.synchronize()
+                for i, ((a0, a1), nb) in enumerate(zip(R.LAUNCH_LOG, R.LAUNCH_BYTES)):
+                    launches.append((a0.elapsed_time(a1), nb, q, i))
+            finally:
+                R.LAUNCH_LOG = None
+        if launches:
+            ms, nb, dq, di = max(launches)
+            tot_ms = sum(x[0] for x in launches)
+            dtr = None
+            tp = os.path.join(ROOT, "profiles", "roofline_traffic_dominant.json")
+            if os.path.exists(tp):
+                with open(tp) as fh:
+                    tr = json.load(fh)
+                if float(tr.get("sf", -1)) == float(args.sf) and tr.get("query") == dq:
+                    dtr = int(tr["dram_bytes_read"]) + int(tr["dram_bytes_write"])
+            dom = {"bound": "hbm", "achieved": round(nb / (ms / 1e3) / 1e9, 1),
+                   "peak": pk["hbm_gbs"], "unit": "GB/s",
+                   "frac": round(nb / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4), "traffic": dtr,
+                   "kernel": f"scx_pipe: {dq}'s fused-scan launch #{di} (the longest of the suite)",
+                   "alg_bytes_per_launch": nb, "launch_ms": round(ms, 4),
+                   "share_of_fused_scan_time": round(ms / tot_ms, 4),
+                   "peak_source": pk["source"]}
+
     shuffle = shuffle_bench(ep, args.shuffle_gib) if args.shuffle_gib > 0 else None
 
     per_query = {}
@@ -996,7 +1035,8 @@ def main() -> None:
                     "passes_upload_done_ms": [round(x, 2) for x in e2e_up_ms],
                     "encoding": "bit-packed host columns (codec.py), unpacked on the device"
                                 if not args.no_pack else "narrowed columns, unpacked"},
-            "roofline": roofline,
+            "roofline": dom or roofline,
+            "roofline_q1_scan": roofline,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": int(launches // max(1, args.steps)),

@@ -714,6 +714,15 @@ def _pushdown_join(lv: TableView, rv: TableView, on: tuple[str, str], how: str):
 # pipeline construction
 # ---------------------------------------------------------------------------
 
+# Per-launch timing for the bench's dominant-kernel roofline: while
+# LAUNCH_LOG is a list, every fused-scan launch appends its (start, end) CUDA
+# events and LAUNCH_BYTES its algorithmic bytes (rows x narrowed width of the
+# base columns it scans).
+LAUNCH_LOG: list | None = None
+LAUNCH_BYTES: list = []
+_DT_BYTES = {L.SCX_I8: 1, L.SCX_U8: 1, L.SCX_I16: 2, L.SCX_U16: 2, L.SCX_I32: 4, L.SCX_U32: 4,
+             L.SCX_I64: 8, L.SCX_F64: 8}
+
 # Optional byte trace for roofline accounting: when set to a set(), every
 # pipeline adds (device address, bytes) of each base column it scans, so
 # the union is the query's distinct HBM bytes read (bench.py).
@@ -974,6 +983,10 @@ class _Builder:
 
     def run(self, timing: list | None = None):
         """Launch; with `timing`, CUDA events bracket exactly this launch."""
+        if timing is None and LAUNCH_LOG is not None:
+            timing = LAUNCH_LOG
+            LAUNCH_BYTES.append(sum(int(self.P.n_rows) * _DT_BYTES.get(int(self.P.base[i].dtype), 8)
+                                    for i in range(int(self.P.n_base))))
         if timing is not None:
             torch = _torch()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -919,7 +919,7 @@ def main() -> None:
     # longest launch is the kernel with the largest share of the step ----
     dom = None
     if ep.n == 1:
-        launches = []
+        scans = []
         for q in QUERIES:
             flush_l2()
             torch.cuda.synchronize()
@@ -931,12 +931,12 @@ def main() -> None:
                     r.materialize()
                 torch.cuda.synchronize()
                 for i, ((a0, a1), nb) in enumerate(zip(R.LAUNCH_LOG, R.LAUNCH_BYTES)):
-                    launches.append((a0.elapsed_time(a1), nb, q, i))
+                    scans.append((a0.elapsed_time(a1), nb, q, i))
             finally:
                 R.LAUNCH_LOG = None
-        if launches:
-            ms, nb, dq, di = max(launches)
-            tot_ms = sum(x[0] for x in launches)
+        if scans:
+            ms, nb, dq, di = max(scans)
+            tot_ms = sum(x[0] for x in scans)
             dtr = None
             tp = os.path.join(ROOT, "profiles", "roofline_traffic_dominant.json")
             if os.path.exists(tp):
@@ -1025,7 +1025,8 @@ def main() -> None:
                        "streams": n_streams,
                        "execution": "concurrent: queries pulled by %d host threads, one CUDA "
                                     "stream each (single_stream holds the one-stream time)"
-                                    % n_streams},
+                                    % n_streams,
+                       "descriptor_limit_fallbacks": dict(R.LIMIT_FALLBACKS)},
             "e2e": {"value": round(e2e_s, 6), "unit": "s", "statistic": "median of timed passes",
                     "results_match_device_run": e2e_match,
                     "h2d_bytes_per_step": h2d_bytes,

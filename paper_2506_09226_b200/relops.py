@@ -23,6 +23,7 @@ once (late materialisation), and no numpy touches a row.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import os
 from dataclasses import dataclass, field
@@ -557,6 +558,7 @@ def local_hash_join(left, right, on: list[tuple[str, str]], how: str = "inner"):
         if overlap:
             raise SchemaError(f"inner join would duplicate columns: {sorted(overlap)}")
     if len(lv.probes) >= L.MAX_PROBES:
+        LIMIT_FALLBACKS["probe_stages_materialized"] += 1
         lv = TableView(lv.materialize())
     rkeys = [r for _, r in on]
     lookup = None
@@ -683,6 +685,8 @@ def _pushdown_join(lv: TableView, rv: TableView, on: tuple[str, str], how: str):
     added = set(need) | {n for st in rv.probes for n in st.payload}
     if (len(need) > L.MAX_PAYLOAD or len(lv.probes) + 1 + len(rv.probes) > L.MAX_PROBES
             or added & set(lv.meta) or len(lv.meta) + len(added) > L.MAX_SLOTS):
+        if not added & set(lv.meta):
+            LIMIT_FALLBACKS["pushdown_join_over_limits"] += 1
         return None
     lookup = Lookup(rbase.select([rname] + [n for n in need if n != rname]), [rname])
     if lookup.lk.kind != L.HT_IDENTITY:
@@ -713,6 +717,12 @@ def _pushdown_join(lv: TableView, rv: TableView, on: tuple[str, str], how: str):
 # ---------------------------------------------------------------------------
 # pipeline construction
 # ---------------------------------------------------------------------------
+
+# Plans that hit a descriptor hard limit (scx.h SCX_MAX_PROBES / _PAYLOAD /
+# _SLOTS) take a slower shape -- an extra materialisation, or a join that is
+# not pushed into the probe scan.  Each such decision is counted here so the
+# bench and tests can report it instead of it happening silently.
+LIMIT_FALLBACKS: collections.Counter = collections.Counter()
 
 # Per-launch timing for the bench's dominant-kernel roofline: while
 # LAUNCH_LOG is a list, every fused-scan launch appends its (start, end) CUDA

@@ -47,6 +47,54 @@ E2E_TABLE_ORDER = ("lineitem", "orders", "customer", "nation", "region", "suppli
 E2E_QUERY_ORDER = ("Q1", "Q6", "Q12", "Q4", "Q18", "Q3", "Q13", "Q22", "Q10", "Q5", "Q7", "Q21",
                    "Q15", "Q14", "Q19", "Q17", "Q8", "Q9", "Q2", "Q11", "Q16", "Q20")
 assert sorted(E2E_QUERY_ORDER) == sorted(QUERIES)
+# single-stream per-query device times at SF100 (ms, round 1): the static
+# longest-first assignment of queries to worker streams and the e2e order
+Q_COST = {'Q1': 2.3, 'Q2': 4.0, 'Q3': 5.3, 'Q4': 1.9, 'Q5': 4.8, 'Q6': 1.0, 'Q7': 5.5, 'Q8': 4.5,
+          'Q9': 9.9, 'Q10': 3.3, 'Q11': 2.0, 'Q12': 2.3, 'Q13': 3.8, 'Q14': 2.2, 'Q15': 2.1,
+          'Q16': 4.9, 'Q17': 4.0, 'Q18': 2.9, 'Q19': 3.0, 'Q20': 5.5, 'Q21': 7.8, 'Q22': 1.8}
+
+
+def query_columns(names) -> dict:
+    """Base columns each plan reads, read off its source: the column-name
+    literals of the plan function and of the queries.py helpers it calls.
+    Only orders the e2e upload (a column a plan reads but this misses is
+    still waited for: Column.data waits on its own upload event)."""
+    import inspect
+    import re
+    from paper_2506_09226_b200 import queries as QM
+    from paper_2506_09226_b200.queries import PLAN_FUNCTIONS
+    funcs = {n: f for n, f in vars(QM).items()
+             if inspect.isfunction(f) and f.__module__ == QM.__name__}
+
+    def lits(f, seen):
+        if f.__name__ in seen:
+            return set()
+        seen.add(f.__name__)
+        src = inspect.getsource(f)
+        out = {m for m in re.findall(r'"([a-z0-9_]+)"', src) if m in names}
+        for n in re.findall(r"\b(_?[a-z0-9_]+)\(", src):
+            if n in funcs:
+                out |= lits(funcs[n], seen)
+        return out
+    return {q: lits(QM_f, set()) for q, QM_f in PLAN_FUNCTIONS.items()}
+
+
+def e2e_order(host: dict) -> tuple[list, list]:
+    """Column-level upload order and the matching query order for the e2e
+    pass: queries by descending device time, each followed by the columns it
+    still lacks, so the expensive queries run while the rest cross PCIe and
+    the last columns to land are read only by cheap queries (the tail after
+    the upload)."""
+    owner = {c: t for t in host for c in host[t]}
+    qcols = query_columns(set(owner))
+    seq, have, qorder = [], set(), []
+    tix = {t: i for i, t in enumerate(E2E_TABLE_ORDER)}
+    for q in sorted(QUERIES, key=lambda x: -Q_COST.get(x, 1.0)):
+        for c in sorted(qcols.get(q, ()) - have, key=lambda c: (tix.get(owner[c], 99), c)):
+            seq.append((owner[c], c))
+            have.add(c)
+        qorder.append(q)
+    return seq, qorder
 
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
            0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -566,6 +614,9 @@ def main() -> None:
     ap.add_argument("--no-configs", action="store_true")
     ap.add_argument("--sweep", default="1,2,4,8,16,32,64",
                     help="config-5 partition sweep sizes (GiB per GPU); empty = skip")
+    ap.add_argument("--table-order", action="store_true",
+                    help="e2e: upload table by table (whole-table waits' order) instead of "
+                         "the column-level first-use order")
     ap.add_argument("--no-pack", action="store_true",
                     help="e2e: send the narrowed columns unpacked")
     ap.add_argument("--shuffle-gib", type=float, default=1.0)
@@ -688,7 +739,7 @@ def main() -> None:
     # static longest-first assignment of queries to streams (by the round-1
     # single-stream per-query times, ms) so every step repeats the same
     # per-stream allocation pattern the warm-up passes already cached
-    q_cost = {'Q1': 2.3, 'Q2': 4.0, 'Q3': 5.3, 'Q4': 1.9, 'Q5': 4.8, 'Q6': 1.0, 'Q7': 5.5, 'Q8': 4.5, 'Q9': 9.9, 'Q10': 3.3, 'Q11': 2.0, 'Q12': 2.3, 'Q13': 3.8, 'Q14': 2.2, 'Q15': 2.1, 'Q16': 4.9, 'Q17': 4.0, 'Q18': 2.9, 'Q19': 3.0, 'Q20': 5.5, 'Q21': 7.8, 'Q22': 1.8}
+    q_cost = Q_COST
     assignment = [[] for _ in range(n_streams)]
     load = [0.0] * n_streams
     for q in sorted(QUERIES, key=lambda x: -q_cost.get(x, 1.0)):
@@ -831,6 +882,9 @@ def main() -> None:
     # its own tables -- PCIe transfer overlapped with query execution
     copy_order = [t for t in E2E_TABLE_ORDER if t in names] + \
         [t for t in names if t not in E2E_TABLE_ORDER]
+    e2e_query_order = E2E_QUERY_ORDER
+    if ep.n == 1 and not args.table_order:
+        copy_order, e2e_query_order = e2e_order(host)
     e2e_ms, e2e_up_ms = [], []
     d2h_bytes = 0
     n_e2e = max(3, min(args.steps, 5))
@@ -847,10 +901,10 @@ def main() -> None:
             if n_streams > 1:
                 # the same worker streams as the device-resident suite, each
                 # query waiting only for its own tables' upload events
-                res = suite_concurrent(dev_tables, ready=ready, order=E2E_QUERY_ORDER)
+                res = suite_concurrent(dev_tables, ready=ready, order=e2e_query_order)
             else:
                 res = {}
-                for q in E2E_QUERY_ORDER:
+                for q in e2e_query_order:
                     ctx = DeviceContext(ep, dev_tables, "default", "default_keys", timed=False,
                                         ready=ready)
                     r = PLAN_FUNCTIONS[q](ctx)
@@ -862,6 +916,10 @@ def main() -> None:
                     torch.cuda.current_stream().wait_event(ev)
             res = suite(dev_tables)
         out = {q: (r.to_reference() if r is not None else None) for q, r in res.items()}
+        if ep.n == 1:
+            # every uploaded column is inside the timed region, read or not
+            for ev in up_events:
+                torch.cuda.current_stream().wait_event(ev)
         e1.record()
         sync_all()
         if i > 1:            # two untimed passes warm the pinned path and the pools

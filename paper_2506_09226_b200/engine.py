@@ -232,7 +232,8 @@ class DeviceContext:
     def table(self, name: str) -> ColumnTable:
         # the query's stream waits for the table's upload events once per
         # context (the dict is shared by concurrent queries: never consumed)
-        if self.ready is not None and name in self.ready and name not in self._waited:
+        if self.ready is not None and name in self.ready and name not in self._waited \
+                and not getattr(self.tables.get(name), "column_ready", False):
             import torch
             evs = self.ready[name]
             for ev in (evs if isinstance(evs, (list, tuple)) else [evs]):
@@ -385,15 +386,20 @@ _COPY_STREAMS: dict = {}
 
 
 def upload_tables_async(host: dict, order=None, stream=None):
-    """Upload pinned host columns on a copy stream, table by table in `order`
-    (first use first), without blocking the compute stream.
+    """Upload pinned host columns on two copy streams in `order` without
+    blocking the compute stream.
 
     ``host``: {table: {column: (HostColumn, pinned torch tensor or
-    codec.PinnedPacked)}} (codec.pin_tables).  Returns
-    (device tables, {table: event}); pass the events as
-    ``DeviceContext(ready=...)`` so each query waits only for the tables it
-    touches while the later tables are still crossing PCIe (H2D overlapped
-    with the queries that can already run).  Single-rank tables only.
+    codec.PinnedPacked)}} (codec.pin_tables).  ``order``: table names (each
+    table's columns in host order) or ``(table, column)`` pairs -- first use
+    first; whatever it leaves out follows in host order.  Every column gets
+    the CUDA event of its own copy (``Column.set_ready``): the first stream
+    that reads a column waits for that event only, so a query starts as soon
+    as the columns it touches have crossed PCIe while the rest are still in
+    flight (H2D overlapped with the queries that can already run).  Returns
+    (device tables, {table: [its column events]}); ``DeviceContext(ready=...)``
+    takes the dict (tables marked ``column_ready`` need no table-level wait).
+    Single-rank tables only.
     """
     import torch
     from .codec import PinnedPacked, scratch_bytes, upload_packed
@@ -407,7 +413,6 @@ def upload_tables_async(host: dict, order=None, stream=None):
     main = torch.cuda.current_stream()
     for cs in streams:
         cs.wait_stream(main)       # buffers below are allocated on `main`
-    tables, events = {}, {}
     # one scratch arena for every packed column's words: the same size each
     # pass, so the caching allocator hands back the same block (per-column
     # scratch allocations cudaMalloc'ed / freed inside timed passes)
@@ -416,51 +421,65 @@ def upload_tables_async(host: dict, order=None, stream=None):
     arena = alloc(max(total, 256), np.uint8)
     for cs in streams:
         arena.record_stream(cs)
+    # the column sequence: explicit pairs / tables first, then the rest
+    seq = []
+    for item in (order or list(host)):
+        if isinstance(item, tuple):
+            if item[0] in host and item[1] in host[item[0]]:
+                seq.append(item)
+        elif item in host:
+            seq.extend((item, c) for c in host[item])
+    seen = set(seq)
+    seq += [(t, c) for t in host for c in host[t] if (t, c) not in seen]
+    cols = {t: {} for t in host}
+    stream_of = {}
+    events = {t: [] for t in host}
     aoff = 0
     k = 0
-    for tname in (order or list(host)):
-        cols = {}
-        used = set()
-        stream_of = {}
-        # column-relative (DIFF) columns go after their reference, on the
-        # reference's copy stream (stream order: the reference is unpacked first)
-        items = list(host[tname].items())
-        is_diff = lambda it: isinstance(it[1][1], PinnedPacked) and it[1][1].col.ref is not None
-        for cname, (hc, pinned) in [it for it in items if not is_diff(it)] + \
-                [it for it in items if is_diff(it)]:
-            ref = pinned.col.ref if isinstance(pinned, PinnedPacked) else None
-            if ref is not None:
-                cs = stream_of[ref]
-            else:
-                cs = streams[k % 2]
-                k += 1
-            stream_of[cname] = cs
-            used.add(id(cs))
-            if isinstance(pinned, PinnedPacked):
-                # packed words cross PCIe, scx_unpack rebuilds the column
-                nb = scratch_bytes(pinned)
-                buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs,
-                                    arena[aoff:aoff + nb],
-                                    cols[ref].data if ref is not None else None)
-                aoff += nb
-            else:
-                buf = alloc(hc.row_count, hc.values.dtype)
-                with torch.cuda.stream(cs):
-                    buf.copy_(pinned, non_blocking=True)
-            col = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
-                         hc.dense and hc.row_count == hc.hi - hc.lo + 1)
-            if hc.sorted:
-                col.sorted = True
-            cols[cname] = col
-        cols = {c: cols[c] for c, _ in items}           # the host table's column order
-        evs = []
-        for cs in streams:
-            if id(cs) in used:
-                ev = torch.cuda.Event(enable_timing=True)
-                ev.record(cs)
-                evs.append(ev)
-        tables[tname] = ColumnTable(cols)
-        events[tname] = evs
+
+    def put(tname, cname):
+        nonlocal aoff, k
+        if cname in cols[tname]:
+            return
+        hc, pinned = host[tname][cname]
+        # a column-relative (DIFF) column is unpacked against its reference:
+        # the reference goes first, and the diff on the reference's copy stream
+        ref = pinned.col.ref if isinstance(pinned, PinnedPacked) else None
+        if ref is not None:
+            put(tname, ref)
+            cs = stream_of[(tname, ref)]
+        else:
+            cs = streams[k % 2]
+            k += 1
+        stream_of[(tname, cname)] = cs
+        if isinstance(pinned, PinnedPacked):
+            # packed words cross PCIe, scx_unpack rebuilds the column
+            nb = scratch_bytes(pinned)
+            buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs,
+                                arena[aoff:aoff + nb],
+                                cols[tname][ref]._data if ref is not None else None)
+            aoff += nb
+        else:
+            buf = alloc(hc.row_count, hc.values.dtype)
+            with torch.cuda.stream(cs):
+                buf.copy_(pinned, non_blocking=True)
+        col = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
+                     hc.dense and hc.row_count == hc.hi - hc.lo + 1)
+        if hc.sorted:
+            col.sorted = True
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(cs)
+        col.set_ready(ev)
+        events[tname].append(ev)
+        cols[tname][cname] = col
+
+    for tname, cname in seq:
+        put(tname, cname)
+    tables = {}
+    for tname in host:
+        t = ColumnTable({c: cols[tname][c] for c in host[tname]})   # host column order
+        t.column_ready = True
+        tables[tname] = t
     return tables, events
 
 

@@ -292,7 +292,7 @@ class Column:
     """
 
     __slots__ = ("kind", "_data", "_host", "scale", "dictionary", "lo", "hi", "dense", "sorted",
-                 "loose")
+                 "loose", "_ready")
 
     def __init__(self, kind: str, data, scale: int = 0, dictionary=None, lo: int = 0,
                  hi: int = -1, dense: bool = False):
@@ -328,10 +328,24 @@ class Column:
         # [lo, hi] proven but loose (an aggregate: rows x per-row range):
         # overflow guards measure the values instead (relops._col_range)
         self.loose = False
+        # (CUDA event, waited stream handles) of an asynchronous upload
+        # (engine.upload_tables_async): the first access to ``data`` from a
+        # stream makes that stream wait for this column's copy -- a query waits
+        # for the columns it reads, not for whole tables
+        self._ready = None
+
+    def set_ready(self, event) -> None:
+        self._ready = (event, set())
 
     @property
     def data(self):
         """Device tensor (uploaded on first use for host-backed result columns)."""
+        if self._ready is not None:
+            ev, waited = self._ready
+            h = _lib.stream_ptr().value or 0
+            if h not in waited:
+                _torch().cuda.current_stream().wait_event(ev)
+                waited.add(h)
         if self._data is None:
             torch = _torch()
             n = len(self._host)

@@ -79,27 +79,57 @@ def query_columns(names) -> dict:
     return {q: lits(QM_f, set()) for q, QM_f in PLAN_FUNCTIONS.items()}
 
 
-def e2e_order(host: dict) -> tuple[list, list]:
-    """Column-level upload order and the matching query order for the e2e
-    pass: queries by descending device time, each followed by the columns it
-    still lacks, so the expensive queries run while the rest cross PCIe and
-    the last columns to land are read only by cheap queries (the tail after
-    the upload)."""
-    owner = {c: t for t in host for c in host[t]}
-    qcols = query_columns(set(owner))
-    seq, have, qorder = [], set(), []
-    tix = {t: i for i, t in enumerate(E2E_TABLE_ORDER)}
-    for q in sorted(QUERIES, key=lambda x: -Q_COST.get(x, 1.0)):
-        for c in sorted(qcols.get(q, ()) - have, key=lambda c: (tix.get(owner[c], 99), c)):
-            seq.append((owner[c], c))
-            have.add(c)
-        qorder.append(q)
-    return seq, qorder
+def _src_bytes(src) -> int:
+    """Bytes one host column sends over PCIe (packed words or the raw array)."""
+    nb = getattr(src, "nbytes", None)
+    if nb is None:
+        nb = src.numel() * src.element_size()
+    return int(nb() if callable(nb) else nb)
 
-REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
-           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
-           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
-           0x100: "display_clock_setting"}
+
+def _e2e_schedule(qorder, qcols, nbytes, cost, rate):
+    """Columns in first-use order of `qorder` and the modelled end of the pass:
+    columns land back to back at `rate` bytes/ms, a query is released when
+    its last column has landed, the GPU runs released work in release order."""
+    seq, have, t, gpu = [], set(), 0.0, 0.0
+    for q in qorder:
+        for c in sorted(qcols[q] - have):
+            seq.append(c)
+            have.add(c)
+            t += nbytes[c] / rate
+        gpu = max(gpu, t) + cost[q]
+    return seq, gpu
+
+
+def e2e_order(host: dict, cost: dict | None = None, rate_gbs: float = 54.0):
+    """Column-level upload order and the matching query order for the e2e
+    pass.  A query starts once the columns it reads have landed, so the pass
+    ends at (upload) + (work released by the last columns): the order is a
+    local search over query orders (adjacent swaps and moves, from the
+    descending-cost order) minimising the modelled end of the pass
+    (_e2e_schedule), with `cost` the queries' measured single-stream device
+    times (ms) and each column's packed bytes over PCIe at `rate_gbs`."""
+    owner = {c: t for t in host for c in host[t]}
+    nbytes = {c: _src_bytes(host[t][c][1]) for c, t in owner.items()}
+    qcols = query_columns(set(owner))
+    cost = {q: (cost or {}).get(q) or Q_COST.get(q, 1.0) for q in QUERIES}
+    rate = rate_gbs * 1e6                  # bytes per ms
+    best = sorted(QUERIES, key=lambda x: -cost[x])
+    best_t = _e2e_schedule(best, qcols, nbytes, cost, rate)[1]
+    improved = True
+    while improved:
+        improved = False
+        for i in range(len(best)):
+            for j in range(len(best)):
+                if i == j:
+                    continue
+                cand = best[:i] + best[i + 1:]
+                cand.insert(j, best[i])
+                t = _e2e_schedule(cand, qcols, nbytes, cost, rate)[1]
+                if t < best_t - 1e-9:
+                    best, best_t, improved = cand, t, True
+    seq = _e2e_schedule(best, qcols, nbytes, cost, rate)[0]
+    return [(owner[c], c) for c in seq], best
 
 
 def peaks() -> dict:
@@ -884,7 +914,8 @@ def main() -> None:
         [t for t in names if t not in E2E_TABLE_ORDER]
     e2e_query_order = E2E_QUERY_ORDER
     if ep.n == 1 and not args.table_order:
-        copy_order, e2e_query_order = e2e_order(host)
+        copy_order, e2e_query_order = e2e_order(
+            host, {q: statistics.mean(v) for q, v in q_ms1.items() if v})
     e2e_ms, e2e_up_ms = [], []
     d2h_bytes = 0
     n_e2e = max(3, min(args.steps, 5))
@@ -995,13 +1026,14 @@ def main() -> None:
         if scans:
             ms, nb, dq, di = max(scans)
             tot_ms = sum(x[0] for x in scans)
-            dtr = None
+            dtr = dl2 = None
             tp = os.path.join(ROOT, "profiles", "roofline_traffic_dominant.json")
             if os.path.exists(tp):
                 with open(tp) as fh:
                     tr = json.load(fh)
                 if float(tr.get("sf", -1)) == float(args.sf) and tr.get("query") == dq:
                     dtr = int(tr["dram_bytes_read"]) + int(tr["dram_bytes_write"])
+                    dl2 = tr.get("l2")
             dom = {"bound": "hbm", "achieved": round(nb / (ms / 1e3) / 1e9, 1),
                    "peak": pk["hbm_gbs"], "unit": "GB/s",
                    "frac": round(nb / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4), "traffic": dtr,
@@ -1009,6 +1041,8 @@ def main() -> None:
                    "alg_bytes_per_launch": nb, "launch_ms": round(ms, 4),
                    "share_of_fused_scan_time": round(ms / tot_ms, 4),
                    "peak_source": pk["source"]}
+            if dl2:
+                dom["l2"] = dl2      # the same launch's L2 counters (ncu --set full)
 
     shuffle = shuffle_bench(ep, args.shuffle_gib) if args.shuffle_gib > 0 else None
 

@@ -27,7 +27,7 @@ def g(name):
     return x * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
 rec = {"sf": 100.0, "query": "$Q", "launch": int("$I"), "kernel": row[h.index("Kernel Name")],
        "dram_bytes_read": int(g("dram__bytes_read.sum")), "dram_bytes_write": int(g("dram__bytes_write.sum")),
-       "gpu_time_ns": g("gpu__time_duration.sum"),
+       "gpu_time_ms": g("gpu__time_duration.sum"),
        "source": "ncu --set full --clock-control none of the bench's dominant launch (tools/gpu_r2ai.sh)"}
 json.dump(rec, open("gpurun_out/roofline_traffic_dominant.json", "w"), indent=1)
 print(rec)

@@ -79,6 +79,12 @@ def query_columns(names) -> dict:
     return {q: lits(QM_f, set()) for q, QM_f in PLAN_FUNCTIONS.items()}
 
 
+REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+           0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+           0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+           0x100: "display_clock_setting"}
+
+
 def _src_bytes(src) -> int:
     """Bytes one host column sends over PCIe (packed words or the raw array)."""
     nb = getattr(src, "nbytes", None)

@@ -1030,7 +1030,7 @@ def main() -> None:
             finally:
                 R.LAUNCH_LOG = None
         if scans:
-            ms, nb, dq, di = max(scans)
+            dms, nb, dq, di = max(scans)
             tot_ms = sum(x[0] for x in scans)
             dtr = dl2 = None
             tp = os.path.join(ROOT, "profiles", "roofline_traffic_dominant.json")
@@ -1040,12 +1040,12 @@ def main() -> None:
                 if float(tr.get("sf", -1)) == float(args.sf) and tr.get("query") == dq:
                     dtr = int(tr["dram_bytes_read"]) + int(tr["dram_bytes_write"])
                     dl2 = tr.get("l2")
-            dom = {"bound": "hbm", "achieved": round(nb / (ms / 1e3) / 1e9, 1),
+            dom = {"bound": "hbm", "achieved": round(nb / (dms / 1e3) / 1e9, 1),
                    "peak": pk["hbm_gbs"], "unit": "GB/s",
-                   "frac": round(nb / (ms / 1e3) / 1e9 / pk["hbm_gbs"], 4), "traffic": dtr,
+                   "frac": round(nb / (dms / 1e3) / 1e9 / pk["hbm_gbs"], 4), "traffic": dtr,
                    "kernel": f"scx_pipe: {dq}'s fused-scan launch #{di} (the longest of the suite)",
-                   "alg_bytes_per_launch": nb, "launch_ms": round(ms, 4),
-                   "share_of_fused_scan_time": round(ms / tot_ms, 4),
+                   "alg_bytes_per_launch": nb, "launch_ms": round(dms, 4),
+                   "share_of_fused_scan_time": round(dms / tot_ms, 4),
                    "peak_source": pk["source"]}
             if dl2:
                 dom["l2"] = dl2      # the same launch's L2 counters (ncu --set full)

@@ -123,3 +123,48 @@ def test_packed_upload_runs_queries_identically(ds):
                                             ready=ready))
         b = P.reference_run(q, plain)
         assert P.result_digest(a) == P.result_digest(b), q
+
+
+@pytest.mark.gpu
+def test_column_ordered_upload_on_worker_streams(ds):
+    """Column-level upload order (bench.e2e_order) with per-column events:
+    queries issued on other streams while the columns are in flight wait for
+    exactly the columns they read and give the device-resident results."""
+    import threading
+    import torch
+    import paper_2506_09226_b200 as P
+    from paper_2506_09226_b200.engine import DeviceContext, load_tables, upload_tables_async
+    from paper_2506_09226_b200.cluster import Endpoint
+    from paper_2506_09226_b200.queries import PLAN_FUNCTIONS
+    import bench
+    host = codec.pin_tables(ds.tables, packed=True)
+    order, qorder = bench.e2e_order(host)
+    assert sorted(order) == sorted((t, c) for t in host for c in host[t])
+    assert sorted(qorder) == sorted(PLAN_FUNCTIONS)
+    plain = load_tables(ds)
+    ep = Endpoint(0, 1, "nccl")
+    dev, ready = upload_tables_async(host, order)
+    assert all(getattr(t, "column_ready", False) for t in dev.values())
+    got, errs = {}, []
+
+    def work(qs):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for q in qs:
+                    got[q] = PLAN_FUNCTIONS[q](DeviceContext(ep, dev, "default", "default_keys",
+                                                             timed=False, ready=ready))
+                    got[q] = got[q].materialize() if got[q] is not None else None
+            s.synchronize()
+        except BaseException as e:      # re-raised below
+            errs.append(e)
+
+    th = [threading.Thread(target=work, args=(qorder[i::3],)) for i in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    if errs:
+        raise errs[0]
+    for q in qorder:
+        assert P.result_digest(got[q]) == P.result_digest(P.reference_run(q, plain)), q

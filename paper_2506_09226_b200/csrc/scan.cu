@@ -188,12 +188,21 @@ __global__ void __launch_bounds__(kBlock) occ_write_kernel(
 }
 
 // ---- finishing a staged stable compaction (jit COMPACT sink) ---------------
-__global__ void region_copy_kernel(const char* src, char* dst, int w, const uint64_t* prefix,
-                                   int64_t region_rows) {
+// One launch moves every output column (blockIdx.z = column): CTA b's staged
+// rows [0, cnt_b) of column j go to rows [prefix_b, prefix_b + cnt_b).
+constexpr int kRegionCols = 16;
+struct RegionCols {
+  const char* src[kRegionCols];
+  char* dst[kRegionCols];
+  int w[kRegionCols];
+};
+
+__global__ void region_copy_kernel(RegionCols R, const uint64_t* prefix, int64_t region_rows) {
+  const int j = blockIdx.z, w = R.w[j];
   const int64_t b = blockIdx.y;
   const uint64_t start = prefix[b], cnt = prefix[b + 1] - start;
-  const char* s = src + (size_t)b * region_rows * w;
-  char* d = dst + (size_t)start * w;
+  const char* s = R.src[j] + (size_t)b * region_rows * w;
+  char* d = R.dst[j] + (size_t)start * w;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
        i += (uint64_t)gridDim.x * blockDim.x) {
     switch (w) {
@@ -214,12 +223,19 @@ int compact_finish(uint64_t* status, int64_t grid, char* stage, int64_t stage_ro
   SCX_CHECK_LAUNCH("small_scan_kernel");
   SCX_CUDA(cudaMemcpyAsync(count, status + grid, 8, cudaMemcpyDeviceToDevice, st));
   char* src = stage;
-  for (int j = 0; j < n_out; ++j) {
-    const int w = dtype_size(outs[j].dtype);
-    region_copy_kernel<<<dim3(16, (unsigned)grid), 256, 0, st>>>(
-        src, reinterpret_cast<char*>(outs[j].ptr), w, status, region_rows);
+  for (int j0 = 0; j0 < n_out; j0 += kRegionCols) {
+    RegionCols R{};
+    const int m = n_out - j0 < kRegionCols ? n_out - j0 : kRegionCols;
+    for (int j = 0; j < m; ++j) {
+      const int w = dtype_size(outs[j0 + j].dtype);
+      R.src[j] = src;
+      R.dst[j] = reinterpret_cast<char*>(outs[j0 + j].ptr);
+      R.w[j] = w;
+      src += (stage_rows * w + 15) & ~int64_t(15);
+    }
+    region_copy_kernel<<<dim3(16, (unsigned)grid, (unsigned)m), 256, 0, st>>>(R, status,
+                                                                             region_rows);
     SCX_CHECK_LAUNCH("region_copy_kernel");
-    src += (stage_rows * w + 15) & ~int64_t(15);
   }
   return SCX_OK;
 }

@@ -197,19 +197,53 @@ struct RegionCols {
   int w[kRegionCols];
 };
 
+// 16 bytes of src starting at byte offset m (0..15) of the aligned pair {a, b}
+__device__ __forceinline__ uint4 byte_window(const uint4 a, const uint4 b, int m) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+  const int q = m >> 2, sh = (m & 3) * 8;
+  uint32_t o[5];
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {     // o[k] = w[q + k], q in 0..3, without local memory
+    uint32_t v = w[k];
+    v = q == 1 ? w[k + 1 < 8 ? k + 1 : 7] : v;
+    v = q == 2 ? w[k + 2 < 8 ? k + 2 : 7] : v;
+    v = q == 3 ? w[k + 3 < 8 ? k + 3 : 7] : v;
+    o[k] = v;
+  }
+  return make_uint4(__funnelshift_r(o[0], o[1], sh), __funnelshift_r(o[1], o[2], sh),
+                    __funnelshift_r(o[2], o[3], sh), __funnelshift_r(o[3], o[4], sh));
+}
+
+// A region is a byte range: [s, s + cnt * w) -> [d, d + cnt * w).  The staged
+// source is 16-byte aligned (region_rows * w and every column's stage are
+// multiples of 16), the destination starts at any byte, so each thread writes
+// one aligned 16-byte destination chunk from a byte window of two aligned
+// source vectors; the first and last chunks (shared with the neighbouring
+// regions) are written byte by byte.
 __global__ void region_copy_kernel(RegionCols R, const uint64_t* prefix, int64_t region_rows) {
   const int j = blockIdx.z, w = R.w[j];
   const int64_t b = blockIdx.y;
-  const uint64_t start = prefix[b], cnt = prefix[b + 1] - start;
-  const char* s = R.src[j] + (size_t)b * region_rows * w;
-  char* d = R.dst[j] + (size_t)start * w;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    switch (w) {
-      case 1: d[i] = s[i]; break;
-      case 2: reinterpret_cast<int16_t*>(d)[i] = reinterpret_cast<const int16_t*>(s)[i]; break;
-      case 4: reinterpret_cast<int32_t*>(d)[i] = reinterpret_cast<const int32_t*>(s)[i]; break;
-      default: reinterpret_cast<int64_t*>(d)[i] = reinterpret_cast<const int64_t*>(s)[i]; break;
+  const uint64_t start = prefix[b], nb = (prefix[b + 1] - start) * (uint64_t)w;
+  if (nb == 0) return;
+  const uint8_t* s = reinterpret_cast<const uint8_t*>(R.src[j]) + (size_t)b * region_rows * w;
+  uint8_t* d = reinterpret_cast<uint8_t*>(R.dst[j]) + (size_t)start * w;
+  const uintptr_t da = reinterpret_cast<uintptr_t>(d), d0 = da & ~uintptr_t(15);
+  const uint64_t nchunks = (da + nb - d0 + 15) / 16;
+  const int m = (int)((16 - (da & 15)) & 15);      // source offset of each chunk, mod 16
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nchunks;
+       c += (uint64_t)gridDim.x * blockDim.x) {
+    const uintptr_t x0 = d0 + c * 16;
+    if (x0 >= da && x0 + 16 <= da + nb) {
+      const uint64_t so = x0 - da;                   // so % 16 == m
+      const uint4* sp = reinterpret_cast<const uint4*>(s + (so - m));
+      const uint4 lo = sp[0];
+      const uint4 hi = m ? sp[1] : lo;
+      *reinterpret_cast<uint4*>(x0) = byte_window(lo, hi, m);
+    } else {
+      for (int i = 0; i < 16; ++i) {
+        const uintptr_t x = x0 + i;
+        if (x >= da && x < da + nb) *reinterpret_cast<uint8_t*>(x) = s[x - da];
+      }
     }
   }
 }
@@ -233,8 +267,8 @@ int compact_finish(uint64_t* status, int64_t grid, char* stage, int64_t stage_ro
       R.w[j] = w;
       src += (stage_rows * w + 15) & ~int64_t(15);
     }
-    region_copy_kernel<<<dim3(16, (unsigned)grid, (unsigned)m), 256, 0, st>>>(R, status,
-                                                                             region_rows);
+    region_copy_kernel<<<dim3(8, (unsigned)grid, (unsigned)m), 256, 0, st>>>(R, status,
+                                                                            region_rows);
     SCX_CHECK_LAUNCH("region_copy_kernel");
   }
   return SCX_OK;

@@ -923,6 +923,7 @@ def main() -> None:
         copy_order, e2e_query_order = e2e_order(
             host, {q: statistics.mean(v) for q, v in q_ms1.items() if v})
     e2e_ms, e2e_up_ms = [], []
+    e2e_qdone = {}
     d2h_bytes = 0
     n_e2e = max(3, min(args.steps, 5))
     for i in range(n_e2e + 2):
@@ -938,7 +939,9 @@ def main() -> None:
             if n_streams > 1:
                 # the same worker streams as the device-resident suite, each
                 # query waiting only for its own tables' upload events
-                res = suite_concurrent(dev_tables, ready=ready, order=e2e_query_order)
+                pq = []
+                res = suite_concurrent(dev_tables, per_query=pq, ready=ready,
+                                       order=e2e_query_order)
             else:
                 res = {}
                 for q in e2e_query_order:
@@ -961,6 +964,8 @@ def main() -> None:
         sync_all()
         if i > 1:            # two untimed passes warm the pinned path and the pools
             e2e_ms.append(e0.elapsed_time(e1))
+            if ep.n == 1 and n_streams > 1:     # when each query's last kernel ended
+                e2e_qdone = {q: round(e0.elapsed_time(b), 2) for q, _, b in pq}
             if ep.n == 1 and up_events:   # when the last column (and its unpack) landed
                 e2e_up_ms.append(max(e0.elapsed_time(ev) for ev in up_events))
         d2h_bytes = sum(v.nbytes for r in out.values() if r for _, v, _ in r.values())
@@ -1132,6 +1137,8 @@ def main() -> None:
                     "narrowed_bytes": narrow_bytes,
                     "passes_ms": [round(x, 2) for x in e2e_ms],
                     "passes_upload_done_ms": [round(x, 2) for x in e2e_up_ms],
+                    "query_order": list(e2e_query_order),
+                    "last_pass_query_done_ms": e2e_qdone,
                     "encoding": "bit-packed host columns (codec.py), unpacked on the device"
                                 if not args.no_pack else "narrowed columns, unpacked"},
             "roofline": dom or roofline,

@@ -408,7 +408,9 @@ def upload_tables_async(host: dict, order=None, stream=None):
     global _COPY_STREAMS
     dev = torch.cuda.current_device()
     if dev not in _COPY_STREAMS:
-        _COPY_STREAMS[dev] = [torch.cuda.Stream(), torch.cuda.Stream()]
+        # high priority: a column's unpack kernel is scheduled ahead of the
+        # queries' pending CTAs (the copy stream's next copy waits behind it)
+        _COPY_STREAMS[dev] = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
     streams = [stream or _COPY_STREAMS[dev][0], _COPY_STREAMS[dev][1]]
     main = torch.cuda.current_stream()
     for cs in streams:

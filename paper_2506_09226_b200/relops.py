@@ -34,7 +34,7 @@ import numpy as np
 from . import _lib as L
 from .expr import (INT64_MAX, INT64_MIN, Atom, ColRef, DerivedKey, IntMeasure, Poly, Pred,
                    as_poly, decimal_exponent, integerise)
-from .table import Column, ColumnTable, HostColumn, SchemaError, alloc
+from .table import Column, ColumnTable, HostColumn, SchemaError, alloc, to_host
 
 AGG_OPS = ("sum", "count", "min", "max", "avg")
 _KEY_KINDS = ("int64", "date32", "dict")
@@ -90,7 +90,7 @@ def _new_i64(n: int, value: int = 0):
 
 
 def _to_host(t) -> np.ndarray:
-    return t.cpu().numpy()
+    return to_host(t)
 
 
 # ---------------------------------------------------------------------------

@@ -283,6 +283,21 @@ def alloc(n: int, np_dtype, device=None):
     return buf[:n] if pad else buf
 
 
+def to_host(t) -> np.ndarray:
+    """D2H read of a device tensor through a pinned (cached) host buffer on the
+    current stream.  A pageable ``.cpu()`` copy goes through the driver's
+    staging buffers and, while an asynchronous upload streams columns in
+    (engine.upload_tables_async), waited behind the in-flight H2D transfers:
+    queries on other streams finished in clusters at column boundaries."""
+    torch = _torch()
+    if t.numel() == 0 or not t.is_cuda:
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    return h.numpy()
+
+
 class Column:
     """Device-resident column (mirror of table.py:46-85).
 
@@ -446,7 +461,7 @@ class Column:
         """Physical values on the host."""
         if self._host is not None:
             return self._host
-        return self.data.cpu().numpy()
+        return to_host(self.data)
 
     @property
     def values(self) -> np.ndarray:

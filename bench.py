@@ -923,7 +923,7 @@ def main() -> None:
         copy_order, e2e_query_order = e2e_order(
             host, {q: statistics.mean(v) for q, v in q_ms1.items() if v})
     e2e_ms, e2e_up_ms = [], []
-    e2e_qdone = {}
+    e2e_qdone, e2e_landed = {}, {}
     d2h_bytes = 0
     n_e2e = max(3, min(args.steps, 5))
     for i in range(n_e2e + 2):
@@ -966,6 +966,10 @@ def main() -> None:
             e2e_ms.append(e0.elapsed_time(e1))
             if ep.n == 1 and n_streams > 1:     # when each query's last kernel ended
                 e2e_qdone = {q: round(e0.elapsed_time(b), 2) for q, _, b in pq}
+            if ep.n == 1:                       # when each column (and its unpack) landed
+                e2e_landed = {f"{t}.{c}": round(e0.elapsed_time(col._ready[0]), 2)
+                              for t, tab in dev_tables.items() for c, col in tab.columns.items()
+                              if col._ready is not None}
             if ep.n == 1 and up_events:   # when the last column (and its unpack) landed
                 e2e_up_ms.append(max(e0.elapsed_time(ev) for ev in up_events))
         d2h_bytes = sum(v.nbytes for r in out.values() if r for _, v, _ in r.values())
@@ -1139,6 +1143,7 @@ def main() -> None:
                     "passes_upload_done_ms": [round(x, 2) for x in e2e_up_ms],
                     "query_order": list(e2e_query_order),
                     "last_pass_query_done_ms": e2e_qdone,
+                    "last_pass_column_landed_ms": e2e_landed,
                     "encoding": "bit-packed host columns (codec.py), unpacked on the device"
                                 if not args.no_pack else "narrowed columns, unpacked"},
             "roofline": dom or roofline,

@@ -23,6 +23,8 @@ from __future__ import annotations
 import ctypes as C
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib as L
@@ -192,6 +194,9 @@ def scratch_bytes(pp: "PinnedPacked") -> int:
     return n
 
 
+_H2D_CHUNK = int(os.environ.get("SCX_H2D_CHUNK_MB", "64")) * (1 << 20) // 4
+
+
 def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, ref_col=None):
     """Device column buffer of ``pc``: H2D of the pinned words (+ bases) on
     ``stream``, then scx_unpack on the same stream.  ``scratch``: a uint8
@@ -216,7 +221,12 @@ def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, 
             else alloc(nb, np.int64)
     with torch.cuda.stream(stream):
         if dw is not None:
-            dw.copy_(src_words, non_blocking=True)
+            # H2D in pieces of _H2D_CHUNK words: the copy engines interleave the
+            # other copy stream's pieces and the queries' D2H result reads with
+            # them instead of queueing behind one multi-GB transfer
+            for a in range(0, nw, _H2D_CHUNK or max(nw, 1)):
+                dw[a:a + (_H2D_CHUNK or nw)].copy_(src_words[a:a + (_H2D_CHUNK or nw)],
+                                                   non_blocking=True)
             if scratch is None:
                 dw.record_stream(stream)
         if db is not None:

@@ -95,16 +95,31 @@ def _src_bytes(src) -> int:
 
 def _e2e_schedule(qorder, qcols, nbytes, cost, rate):
     """Columns in first-use order of `qorder` and the modelled end of the pass:
-    columns land back to back at `rate` bytes/ms, a query is released when
-    its last column has landed, the GPU runs released work in release order."""
-    seq, have, t, gpu = [], set(), 0.0, 0.0
+    columns land back to back at `rate` bytes/ms (one copy stream), a query
+    is released when its last column has landed, the GPU runs released work
+    in release order.  Also returns each query's release time (ms)."""
+    seq, have, t, gpu, rel = [], set(), 0.0, 0.0, {}
     for q in qorder:
         for c in sorted(qcols[q] - have):
             seq.append(c)
             have.add(c)
             t += nbytes[c] / rate
+        rel[q] = t
         gpu = max(gpu, t) + cost[q]
-    return seq, gpu
+    return seq, gpu, rel
+
+
+def e2e_assignment(qorder, rel, cost, n_workers):
+    """Queries to worker streams for the e2e pass: in release order, each to
+    the worker that is free first (list scheduling on the modelled release
+    times), so no released query queues behind a worker's unreleased one."""
+    free = [0.0] * n_workers
+    out = [[] for _ in range(n_workers)]
+    for q in qorder:
+        j = min(range(n_workers), key=lambda w: free[w])
+        out[j].append(q)
+        free[j] = max(free[j], rel.get(q, 0.0)) + cost.get(q, 1.0)
+    return out
 
 
 def e2e_order(host: dict, cost: dict | None = None, rate_gbs: float = 54.0):
@@ -134,8 +149,8 @@ def e2e_order(host: dict, cost: dict | None = None, rate_gbs: float = 54.0):
                 t = _e2e_schedule(cand, qcols, nbytes, cost, rate)[1]
                 if t < best_t - 1e-9:
                     best, best_t, improved = cand, t, True
-    seq = _e2e_schedule(best, qcols, nbytes, cost, rate)[0]
-    return [(owner[c], c) for c in seq], best
+    seq, _, rel = _e2e_schedule(best, qcols, nbytes, cost, rate)
+    return [(owner[c], c) for c in seq], best, rel, cost
 
 
 def peaks() -> dict:
@@ -722,7 +737,7 @@ def main() -> None:
                 per_query.append((q, e0, e1))
         return results
 
-    def suite_concurrent(tabs, per_query=None, ready=None, order=None):
+    def suite_concurrent(tabs, per_query=None, ready=None, order=None, assign=None):
         """The same 22 queries, pulled in order by `n_streams` host threads,
         each issuing on its own CUDA stream: one query's plan building and
         result finishing overlap another's kernels.  The step's end event
@@ -739,7 +754,7 @@ def main() -> None:
                 s = worker_streams[i]
                 with torch.cuda.stream(s):
                     s.wait_event(start)
-                    mine = [q for q in (order or QUERIES) if q in assignment[i]]
+                    mine = [q for q in (order or QUERIES) if q in (assign or assignment)[i]]
                     for q in mine:
                         if per_query is not None:
                             e0 = torch.cuda.Event(enable_timing=True)
@@ -919,9 +934,12 @@ def main() -> None:
     copy_order = [t for t in E2E_TABLE_ORDER if t in names] + \
         [t for t in names if t not in E2E_TABLE_ORDER]
     e2e_query_order = E2E_QUERY_ORDER
+    e2e_assign = None
     if ep.n == 1 and not args.table_order:
-        copy_order, e2e_query_order = e2e_order(
+        copy_order, e2e_query_order, rel, qcost = e2e_order(
             host, {q: statistics.mean(v) for q, v in q_ms1.items() if v})
+        if n_streams > 1:
+            e2e_assign = e2e_assignment(e2e_query_order, rel, qcost, n_streams)
     e2e_ms, e2e_up_ms = [], []
     e2e_qdone, e2e_landed = {}, {}
     d2h_bytes = 0
@@ -941,7 +959,7 @@ def main() -> None:
                 # query waiting only for its own tables' upload events
                 pq = []
                 res = suite_concurrent(dev_tables, per_query=pq, ready=ready,
-                                       order=e2e_query_order)
+                                       order=e2e_query_order, assign=e2e_assign)
             else:
                 res = {}
                 for q in e2e_query_order:
@@ -1142,6 +1160,7 @@ def main() -> None:
                     "passes_ms": [round(x, 2) for x in e2e_ms],
                     "passes_upload_done_ms": [round(x, 2) for x in e2e_up_ms],
                     "query_order": list(e2e_query_order),
+                    "worker_queues": e2e_assign,
                     "last_pass_query_done_ms": e2e_qdone,
                     "last_pass_column_landed_ms": e2e_landed,
                     "encoding": "bit-packed host columns (codec.py), unpacked on the device"

@@ -197,7 +197,8 @@ def scratch_bytes(pp: "PinnedPacked") -> int:
 _H2D_CHUNK = int(os.environ.get("SCX_H2D_CHUNK_MB", "64")) * (1 << 20) // 4
 
 
-def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, ref_col=None):
+def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, ref_col=None,
+                  unpack_stream=None):
     """Device column buffer of ``pc``: H2D of the pinned words (+ bases) on
     ``stream``, then scx_unpack on the same stream.  ``scratch``: a uint8
     device view of >= scratch_bytes() (the caller carves one arena per upload
@@ -233,14 +234,27 @@ def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, 
             db.copy_(src_bases, non_blocking=True)
             if scratch is None:
                 db.record_stream(stream)
+    us = stream
+    if unpack_stream is not None:
+        # the unpack on its own stream, behind this column's copy: the copy
+        # stream goes on with the next column's words
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        unpack_stream.wait_event(ev)
+        us = unpack_stream
+        if scratch is None:
+            for t in (dw, db):
+                if t is not None:
+                    t.record_stream(us)
+    with torch.cuda.stream(us):
         if pc.encoding == DIFF:
             L.call("scx_unpack_diff", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n,
                    pc.k, pc.lo, L.Column_(ref_col.data_ptr(), _scx_of(ref_col), 0),
-                   L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(stream))
+                   L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(us))
         else:
             L.call("scx_unpack", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n, pc.k,
                    pc.lo, pc.encoding, C.c_void_p(db.data_ptr() if db is not None else 0),
-                   L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(stream))
+                   L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(us))
     return buf
 
 

@@ -23,6 +23,8 @@ import json
 import time
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 
 from . import exchange as X
@@ -403,17 +405,21 @@ def upload_tables_async(host: dict, order=None, stream=None):
     """
     import torch
     from .codec import PinnedPacked, scratch_bytes, upload_packed
-    # two copy streams: columns alternate between them (both DMA engines busy);
-    # kept per device so repeated uploads reuse them
+    # SCX_UPLOAD_STREAMS=1 (default): one copy stream lands the columns
+    # strictly in `order` at full PCIe rate, their unpack kernels run on a
+    # separate high-priority stream (the next copy never waits for an unpack,
+    # and an unpack is scheduled ahead of the queries' pending CTAs).  =2: two
+    # copy streams, columns alternating, each unpacked on its copy stream
+    # (columns then land interleaved, out of `order`).  Kept per device.
     global _COPY_STREAMS
     dev = torch.cuda.current_device()
     if dev not in _COPY_STREAMS:
-        # high priority: a column's unpack kernel is scheduled ahead of the
-        # queries' pending CTAs (the copy stream's next copy waits behind it)
-        _COPY_STREAMS[dev] = [torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=-1)]
-    streams = [stream or _COPY_STREAMS[dev][0], _COPY_STREAMS[dev][1]]
+        _COPY_STREAMS[dev] = [torch.cuda.Stream(priority=-1) for _ in range(3)]
+    two = os.environ.get("SCX_UPLOAD_STREAMS", "1") == "2"
+    streams = [stream or _COPY_STREAMS[dev][0]] + ([_COPY_STREAMS[dev][1]] if two else [])
+    unpack_stream = None if two else _COPY_STREAMS[dev][2]
     main = torch.cuda.current_stream()
-    for cs in streams:
+    for cs in streams + ([unpack_stream] if unpack_stream is not None else []):
         cs.wait_stream(main)       # buffers below are allocated on `main`
     # one scratch arena for every packed column's words: the same size each
     # pass, so the caching allocator hands back the same block (per-column
@@ -421,7 +427,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
     total = sum(scratch_bytes(src) for cols in host.values() for _, src in cols.values()
                 if isinstance(src, PinnedPacked))
     arena = alloc(max(total, 256), np.uint8)
-    for cs in streams:
+    for cs in streams + ([unpack_stream] if unpack_stream is not None else []):
         arena.record_stream(cs)
     # the column sequence: explicit pairs / tables first, then the rest
     seq = []
@@ -451,7 +457,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
             put(tname, ref)
             cs = stream_of[(tname, ref)]
         else:
-            cs = streams[k % 2]
+            cs = streams[k % len(streams)]
             k += 1
         stream_of[(tname, cname)] = cs
         if isinstance(pinned, PinnedPacked):
@@ -459,18 +465,21 @@ def upload_tables_async(host: dict, order=None, stream=None):
             nb = scratch_bytes(pinned)
             buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs,
                                 arena[aoff:aoff + nb],
-                                cols[tname][ref]._data if ref is not None else None)
+                                cols[tname][ref]._data if ref is not None else None,
+                                unpack_stream=unpack_stream)
             aoff += nb
+            done_on = unpack_stream or cs
         else:
             buf = alloc(hc.row_count, hc.values.dtype)
             with torch.cuda.stream(cs):
                 buf.copy_(pinned, non_blocking=True)
+            done_on = cs
         col = Column(hc.kind, buf, hc.scale, hc.dictionary, hc.lo, hc.hi,
                      hc.dense and hc.row_count == hc.hi - hc.lo + 1)
         if hc.sorted:
             col.sorted = True
         ev = torch.cuda.Event(enable_timing=True)
-        ev.record(cs)
+        ev.record(done_on)
         col.set_ready(ev)
         events[tname].append(ev)
         cols[tname][cname] = col

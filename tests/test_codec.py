@@ -138,7 +138,7 @@ def test_column_ordered_upload_on_worker_streams(ds):
     from paper_2506_09226_b200.queries import PLAN_FUNCTIONS
     import bench
     host = codec.pin_tables(ds.tables, packed=True)
-    order, qorder = bench.e2e_order(host)
+    order, qorder, _, _ = bench.e2e_order(host)
     assert sorted(order) == sorted((t, c) for t in host for c in host[t])
     assert sorted(qorder) == sorted(PLAN_FUNCTIONS)
     plain = load_tables(ds)

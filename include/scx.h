@@ -424,6 +424,11 @@ int scx_fill_i64(int64_t* p_dev, int64_t n, int64_t stride, int64_t value, void*
 /* p[r * w + j] = pattern_host[j] for r < rows, j < w <= 16: a row-major
  * group table's identities in one pass */
 int scx_fill_rows(int64_t* p_dev, int64_t rows, int w, const int64_t* pattern_host, void* stream);
+/* dst_host[0..nbytes) = src_dev[0..nbytes) by a kernel storing into mapped
+ * pinned host memory (cudaHostAlloc'ed: UVA-mapped): a small result read that
+ * does not queue on a copy engine behind an in-flight upload.  No reference
+ * counterpart (the reference's results are host numpy arrays already). */
+int scx_write_mapped(const void* src_dev, void* dst_host, int64_t nbytes, void* stream);
 
 /* ---- hash partitioning (exchange.py:35-70) --------------------------------
  * bucket(row) = fib_hash(keys) mod n_parts with the reference's u64 wrap:

@@ -150,6 +150,7 @@ _PROTOS = {
     "scx_iota": (C.c_int, [_vp, i64, _vp]),
     "scx_fill_rows": (C.c_int, [_vp, i64, C.c_int, C.POINTER(i64), _vp]),
     "scx_fill_i64": (C.c_int, [_vp, i64, i64, i64, _vp]),
+    "scx_write_mapped": (C.c_int, [_vp, _vp, i64, _vp]),
     "scx_hash_keys": (C.c_int, [C.POINTER(Column_), C.c_int, i64, _vp, _vp]),
     "scx_partition_workspace": (i64, [i64, C.c_int]),
     "scx_partition": (C.c_int, [C.POINTER(Column_), C.c_int, C.POINTER(Column_),

@@ -283,7 +283,41 @@ __global__ void minmax_kernel(scx_column col, int64_t n, int64_t* out) {
   }
 }
 
+
+// ---- small result reads without a copy engine ------------------------------
+// The kernel stores straight into mapped pinned host memory over PCIe: a
+// query's few result bytes reach the host while the copy engines are busy
+// with a multi-GB upload (a D2H cudaMemcpyAsync queued behind it).
+__global__ void write_mapped_kernel(const uint8_t* src, uint8_t* dst, int64_t n) {
+  const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t st = (int64_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)n) & 15) == 0) {
+    for (int64_t i = i0; i < n / 16; i += st)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+  } else {
+    for (int64_t i = i0; i < n; i += st) dst[i] = src[i];
+  }
+}
+
 }  // namespace scx
+
+extern "C" int scx_write_mapped(const void* src_dev, void* dst_host, int64_t nbytes,
+                                void* stream) {
+  using namespace scx;
+  if (nbytes < 0 || (nbytes && (!src_dev || !dst_host))) {
+    set_error("write_mapped: bad arguments");
+    return SCX_EINVAL;
+  }
+  if (nbytes == 0) return SCX_OK;
+  void* dptr = nullptr;
+  SCX_CUDA(cudaHostGetDevicePointer(&dptr, dst_host, 0));
+  const int64_t work = (nbytes + 15) / 16;
+  const int grid = (int)(work < 256 * 64 ? (work + 255) / 256 : 64);
+  write_mapped_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const uint8_t*>(src_dev), reinterpret_cast<uint8_t*>(dptr), nbytes);
+  SCX_CHECK_LAUNCH("write_mapped_kernel");
+  return SCX_OK;
+}
 
 using namespace scx;
 

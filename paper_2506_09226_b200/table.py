@@ -23,6 +23,8 @@ from __future__ import annotations
 from dataclasses import dataclass
 from datetime import date, timedelta
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -283,17 +285,34 @@ def alloc(n: int, np_dtype, device=None):
     return buf[:n] if pad else buf
 
 
+_MAPPED_OK = os.environ.get("SCX_MAPPED_READS", "1") != "0"
+_MAPPED_MAX = 1 << 20
+
+
 def to_host(t) -> np.ndarray:
     """D2H read of a device tensor through a pinned (cached) host buffer on the
     current stream.  A pageable ``.cpu()`` copy goes through the driver's
     staging buffers and, while an asynchronous upload streams columns in
     (engine.upload_tables_async), waited behind the in-flight H2D transfers:
     queries on other streams finished in clusters at column boundaries."""
+    global _MAPPED_OK
     torch = _torch()
     if t.numel() == 0 or not t.is_cuda:
         return t.cpu().numpy()
+    t = t.contiguous()
     h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-    h.copy_(t, non_blocking=True)
+    nb = t.numel() * t.element_size()
+    done = False
+    if _MAPPED_OK and nb <= _MAPPED_MAX:
+        # small reads: a kernel stores into the mapped pinned buffer, no copy
+        # engine (scx_write_mapped)
+        try:
+            _lib.call("scx_write_mapped", t.data_ptr(), h.data_ptr(), nb, _lib.stream_ptr())
+            done = True
+        except _lib.ScxError:
+            _MAPPED_OK = False
+    if not done:
+        h.copy_(t, non_blocking=True)
     torch.cuda.current_stream().synchronize()
     return h.numpy()
 

@@ -98,14 +98,16 @@ def _e2e_schedule(qorder, qcols, nbytes, cost, rate):
     columns land back to back at `rate` bytes/ms (one copy stream), a query
     is released when its last column has landed, the GPU runs released work
     in release order.  Also returns each query's release time (ms)."""
-    seq, have, t, gpu, rel = [], set(), 0.0, 0.0, {}
+    seq, landed, t, rel = [], {}, 0.0, {}
     for q in qorder:
-        for c in sorted(qcols[q] - have):
+        for c in sorted(qcols[q] - landed.keys()):
             seq.append(c)
-            have.add(c)
             t += nbytes[c] / rate
-        rel[q] = t
-        gpu = max(gpu, t) + cost[q]
+            landed[c] = t
+        rel[q] = max([landed[c] for c in qcols[q]] + [0.0])
+    gpu = 0.0
+    for q in sorted(qorder, key=lambda x: rel[x]):
+        gpu = max(gpu, rel[q]) + cost[q]
     return seq, gpu, rel
 
 
@@ -150,6 +152,8 @@ def e2e_order(host: dict, cost: dict | None = None, rate_gbs: float = 54.0):
                 if t < best_t - 1e-9:
                     best, best_t, improved = cand, t, True
     seq, _, rel = _e2e_schedule(best, qcols, nbytes, cost, rate)
+    # the queries in release order (stable): the order the workers run them
+    best = sorted(best, key=lambda q: rel[q])
     return [(owner[c], c) for c in seq], best, rel, cost
 
 

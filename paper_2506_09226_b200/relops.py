@@ -853,7 +853,8 @@ class _Builder:
             pb.kind = st.kind
             pb.key = st.lookup.packing.spec([self.slot[k] for k in st.probe_keys])
             pb.table = st.lookup.lk
-            if (st.lookup.lk.kind == L.HT_BITMAP and _COARSE_BITMAPS
+            if (st.lookup.lk.kind == L.HT_BITMAP
+                    and (_COARSE_BITMAPS or os.environ.get("SCX_COARSE") == "1")
                     and P.n_rows >= _COARSE_MIN_ROWS):
                 # shared-memory coarse level: <= 32 KB of coarse bits shared by
                 # this kernel's bitmap probes

@@ -20,10 +20,9 @@ from __future__ import annotations
 
 import hashlib
 import json
+import os
 import time
 from dataclasses import dataclass, field
-
-import os
 
 import numpy as np
 
@@ -388,8 +387,9 @@ _COPY_STREAMS: dict = {}
 
 
 def upload_tables_async(host: dict, order=None, stream=None):
-    """Upload pinned host columns on two copy streams in `order` without
-    blocking the compute stream.
+    """Upload pinned host columns in `order` on a copy stream (their unpack
+    kernels on a second, high-priority stream) without blocking the compute
+    stream.
 
     ``host``: {table: {column: (HostColumn, pinned torch tensor or
     codec.PinnedPacked)}} (codec.pin_tables).  ``order``: table names (each

@@ -20,10 +20,9 @@ while predicates compile into the fused scan kernel instead of numpy masks.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from datetime import date, timedelta
-
-import os
 
 import numpy as np
 
@@ -290,11 +289,13 @@ _MAPPED_MAX = 1 << 20
 
 
 def to_host(t) -> np.ndarray:
-    """D2H read of a device tensor through a pinned (cached) host buffer on the
-    current stream.  A pageable ``.cpu()`` copy goes through the driver's
-    staging buffers and, while an asynchronous upload streams columns in
-    (engine.upload_tables_async), waited behind the in-flight H2D transfers:
-    queries on other streams finished in clusters at column boundaries."""
+    """D2H read of a device tensor into a pinned (cached) host buffer on the
+    current stream: up to 1 MB by a kernel storing into the mapped buffer
+    (scx_write_mapped, no copy engine), larger reads by an async copy.  A
+    pageable ``.cpu()`` copy -- and any copy-engine D2H -- queued behind the
+    in-flight H2D transfers of an asynchronous upload
+    (engine.upload_tables_async): a query whose columns had landed at 72 ms
+    read its result at 106 ms.  SCX_MAPPED_READS=0 keeps the copy path."""
     global _MAPPED_OK
     torch = _torch()
     if t.numel() == 0 or not t.is_cuda:

@@ -529,6 +529,12 @@ int scx_unpack(const uint32_t* words_dev, int64_t n, int k, int64_t lo, int enco
  * table (l_receiptdate against l_shipdate: 5 bits instead of 12). */
 int scx_unpack_diff(const uint32_t* words_dev, int64_t n, int k, int64_t lo, scx_column ref,
                     scx_column out, void* stream);
+/* key-relative unpack: out[i] = ref[fk[i] - fk_lo] + lo + field(words, i, k),
+ * ref a dense-keyed parent column of ref_n rows (a child date stored against
+ * its parent row's date through the foreign key fk).  Extension of the load
+ * path (codec.py); no reference counterpart. */
+int scx_unpack_fkdiff(const uint32_t* words, int64_t n, int k, int64_t lo, scx_column fk,
+                      int64_t fk_lo, scx_column ref, int64_t ref_n, scx_column out, void* stream);
 
 #ifdef __cplusplus
 }

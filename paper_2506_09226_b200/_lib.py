@@ -179,6 +179,8 @@ _PROTOS = {
     "scx_pack_host": (C.c_int, [_vp, C.c_int, i64, i64, C.c_int, C.c_int, _vp, _vp, C.c_int]),
     "scx_unpack": (C.c_int, [_vp, i64, C.c_int, i64, C.c_int, _vp, Column_, _vp]),
     "scx_unpack_diff": (C.c_int, [_vp, i64, C.c_int, i64, Column_, Column_, _vp]),
+    "scx_unpack_fkdiff": (C.c_int, [_vp, i64, C.c_int, i64, Column_, i64, Column_, i64, Column_,
+                                    _vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

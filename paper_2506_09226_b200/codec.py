@@ -11,6 +11,11 @@ paper's cold run) -- is bound by PCIe, ~48 GB/s against
 * DELTA -- a non-decreasing column (l_orderkey) packs its deltas per 2048-row
            block (1 bit per row at uniform SF100) plus one int64 base per block;
 * IOTA  -- a surrogate key column (lo, lo+1, ...) sends nothing;
+* DIFF  -- a date against another date of the same row (l_shipdate against
+           l_receiptdate: 5 bits);
+* FKDIFF-- a date against its parent row's date through a foreign key into a
+           dense key (l_receiptdate - o_orderdate[l_orderkey - 1]: 8 bits
+           instead of 12; l_commitdate: 6), chosen only where it is narrower;
 * RAW   -- anything that would not shrink (raw float64, k >= the narrowed width).
 
 ``scx_pack_host`` (threaded C++) packs; ``scx_unpack`` rebuilds the narrowed
@@ -32,6 +37,10 @@ from .table import NP_TO_SCX, HostColumn
 
 RAW = -1
 DIFF = 3                 # column-relative: value = ref[i] + lo + field (scx_unpack_diff)
+FKDIFF = 4               # key-relative: value = parent[fk[i] - fk_lo] + lo + field
+# (child table, foreign key, parent table, dense parent key): the key-relative
+# candidates the packer tries (TPC-H's lineitem -> orders, data.py schema)
+FOREIGN_KEYS = (("lineitem", "l_orderkey", "orders", "o_orderkey"),)
 _CHUNK = 1 << 24
 
 
@@ -48,6 +57,9 @@ class PackedColumn:
     words: np.ndarray | None = None      # u32
     bases: np.ndarray | None = None      # i64, DELTA only
     ref: str | None = None               # DIFF: the reference column of the same table
+    fk: str | None = None                # FKDIFF: foreign-key column of this table
+    fk_lo: int = 0                       # FKDIFF: parent row = fk - fk_lo
+    ref_table: str | None = None         # FKDIFF: parent table (ref = its column)
 
     @property
     def dtype(self) -> np.dtype:
@@ -157,10 +169,76 @@ def pack_table(ht, threads: int = 0) -> dict[str, PackedColumn]:
     return out
 
 
-def unpack_host(pc: PackedColumn, ref_values: np.ndarray | None = None) -> np.ndarray:
-    """numpy restatement of scx_unpack / scx_unpack_diff (test infrastructure)."""
+def _pack_fkdiff(hc: HostColumn, fk: HostColumn, parent: HostColumn, fk_lo: int, ref: str,
+                 ref_table: str, fk_name: str, threads: int) -> PackedColumn | None:
+    """value - parent[fk[i] - fk_lo] in FOR bits (None when out of range)."""
+    v = np.asarray(hc.values)
+    n = len(v)
+    pv = np.asarray(parent.values)
+    lo = hi = None
+    for s0 in range(0, n, _CHUNK):
+        idx = np.asarray(fk.values[s0:s0 + _CHUNK]).astype(np.int64) - fk_lo
+        if idx.size and (idx.min() < 0 or idx.max() >= len(pv)):
+            return None
+        d = v[s0:s0 + _CHUNK].astype(np.int64) - pv[idx].astype(np.int64)
+        if d.size:
+            lo = int(d.min()) if lo is None else min(lo, int(d.min()))
+            hi = int(d.max()) if hi is None else max(hi, int(d.max()))
+    if lo is None:
+        return None
+    k = _bits(hi - lo)
+    if k > 32:
+        return None
+    lib = L.load()
+    words = np.empty(int(lib.scx_pack_words(n, k)), dtype=np.uint32)
+    d = v.astype(np.int64) - pv[np.asarray(fk.values).astype(np.int64) - fk_lo].astype(np.int64)
+    L.call("scx_pack_host", d.ctypes.data_as(C.c_void_p), L.SCX_I64, n, lo, k, 0,
+           words.ctypes.data_as(C.c_void_p), None, threads)
+    return PackedColumn(hc, n, FKDIFF, k, lo, words, None, ref, fk_name, fk_lo, ref_table)
+
+
+def pack_tables(tables: dict, threads: int = 0) -> dict[str, dict[str, PackedColumn]]:
+    """pack_table for every table, then each child date column of a
+    FOREIGN_KEYS pair stored against a parent date (FKDIFF) where that is at
+    least 2 bits narrower than its own encoding.  A column another column is
+    stored against (a DIFF reference) may itself become key-relative: it is
+    rebuilt first on the device."""
+    out = {t: pack_table(ht, threads) for t, ht in tables.items()}
+    for child, fk, parent, pk in FOREIGN_KEYS:
+        if child not in tables or parent not in tables:
+            continue
+        ct, pt = tables[child], tables[parent]
+        if fk not in ct.columns or pk not in pt.columns or ct.columns[fk].row_count == 0:
+            continue
+        pkc = pt.columns[pk]
+        if not (pkc.dense and pkc.row_count == pkc.hi - pkc.lo + 1):
+            continue                       # parent row = key - lo needs a dense key
+        pdates = [c for c, hc in pt.columns.items() if hc.kind == "date32"]
+        for c, hc in ct.columns.items():
+            if hc.kind != "date32" or out[child][c].encoding == RAW:
+                continue
+            best = None
+            for r in pdates:
+                pc = _pack_fkdiff(hc, ct.columns[fk], pt.columns[r], pkc.lo, r, parent, fk,
+                                  threads)
+                if pc is not None and (best is None or pc.k < best.k):
+                    best = pc
+            if best is not None and best.k + 2 <= out[child][c].k:
+                out[child][c] = best
+    return out
+
+
+def unpack_host(pc: PackedColumn, ref_values: np.ndarray | None = None,
+                fk_values: np.ndarray | None = None) -> np.ndarray:
+    """numpy restatement of scx_unpack / scx_unpack_diff / scx_unpack_fkdiff
+    (test infrastructure)."""
     if pc.encoding == RAW:
         return np.asarray(pc.meta.values)
+    if pc.encoding == FKDIFF:
+        f = unpack_host(PackedColumn(pc.meta, pc.n, L.PACK_FOR, pc.k, 0, pc.words)).astype(np.int64) \
+            if pc.k else np.zeros(pc.n, dtype=np.int64)
+        par = np.asarray(ref_values).astype(np.int64)[np.asarray(fk_values).astype(np.int64) - pc.fk_lo]
+        return (par + pc.lo + f).astype(pc.dtype)
     if pc.encoding == DIFF:
         f = unpack_host(PackedColumn(pc.meta, pc.n, L.PACK_FOR, pc.k, 0, pc.words)).astype(np.int64) \
             if pc.k else np.zeros(pc.n, dtype=np.int64)
@@ -198,7 +276,7 @@ _H2D_CHUNK = int(os.environ.get("SCX_H2D_CHUNK_MB", "64")) * (1 << 20) // 4
 
 
 def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, ref_col=None,
-                  unpack_stream=None):
+                  unpack_stream=None, fk_col=None):
     """Device column buffer of ``pc``: H2D of the pinned words (+ bases) on
     ``stream``, then scx_unpack on the same stream.  ``scratch``: a uint8
     device view of >= scratch_bytes() (the caller carves one arena per upload
@@ -247,7 +325,12 @@ def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, 
                 if t is not None:
                     t.record_stream(us)
     with torch.cuda.stream(us):
-        if pc.encoding == DIFF:
+        if pc.encoding == FKDIFF:
+            L.call("scx_unpack_fkdiff", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n,
+                   pc.k, pc.lo, L.Column_(fk_col.data_ptr(), _scx_of(fk_col), 0), pc.fk_lo,
+                   L.Column_(ref_col.data_ptr(), _scx_of(ref_col), 0), ref_col.numel(),
+                   L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(us))
+        elif pc.encoding == DIFF:
             L.call("scx_unpack_diff", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n,
                    pc.k, pc.lo, L.Column_(ref_col.data_ptr(), _scx_of(ref_col), 0),
                    L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(us))
@@ -289,9 +372,10 @@ def pin_tables(tables: dict, packed: bool = True, threads: int = 0) -> dict:
     the source is a pinned raw tensor, or a PinnedPacked (packed=True) whose
     words cross PCIe and are unpacked on the device."""
     out = {}
+    packs = pack_tables(tables, threads) if packed else {}
     for t, ht in tables.items():
         cols = {}
-        pt = pack_table(ht, threads) if packed else {}
+        pt = packs[t] if packed else {}
         for c, hc in ht.columns.items():
             pc = pt[c] if packed else PackedColumn(hc, hc.row_count, RAW)
             if pc.encoding == RAW:

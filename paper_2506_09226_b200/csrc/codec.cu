@@ -138,6 +138,21 @@ __global__ void unpack_diff_kernel(const uint32_t* __restrict__ words, int64_t n
     out[i] = (T)(load_i64(r, ref.dtype, i) + lo + (int64_t)(k ? field(words, i, k) : 0));
 }
 
+// key-relative: value = ref[fk[i] - fk_lo] + lo + field -- a date stored
+// against a date of the row's parent through a foreign key into a dense key
+// (l_receiptdate - o_orderdate[l_orderkey - 1] in [2, 151]: 8 bits, not 12)
+template <typename T>
+__global__ void unpack_fkdiff_kernel(const uint32_t* __restrict__ words, int64_t n, int k,
+                                     int64_t lo, scx_column fk, int64_t fk_lo, scx_column ref,
+                                     T* __restrict__ out) {
+  const void* f = reinterpret_cast<const void*>(fk.ptr);
+  const void* r = reinterpret_cast<const void*>(ref.ptr);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (T)(load_i64(r, ref.dtype, load_i64(f, fk.dtype, i) - fk_lo) + lo +
+                 (int64_t)(k ? field(words, i, k) : 0));
+}
+
 template <typename T>
 __global__ void iota_kernel(int64_t n, int64_t lo, T* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -173,6 +188,12 @@ template <typename T> struct DiffL {
   static void run(dim3 g, dim3 b, cudaStream_t st, const uint32_t* w, int64_t n, int k, int64_t lo,
                   scx_column ref, void* out) {
     unpack_diff_kernel<T><<<g, b, 0, st>>>(w, n, k, lo, ref, static_cast<T*>(out));
+  }
+};
+template <typename T> struct FkDiffL {
+  static void run(dim3 g, dim3 b, cudaStream_t st, const uint32_t* w, int64_t n, int k, int64_t lo,
+                  scx_column fk, int64_t fk_lo, scx_column ref, void* out) {
+    unpack_fkdiff_kernel<T><<<g, b, 0, st>>>(w, n, k, lo, fk, fk_lo, ref, static_cast<T*>(out));
   }
 };
 template <typename T> struct IotaL {
@@ -275,5 +296,22 @@ extern "C" int scx_unpack_diff(const uint32_t* words, int64_t n, int k, int64_t 
                                     static_cast<cudaStream_t>(stream), words, n, k, lo, ref,
                                     reinterpret_cast<void*>(out.ptr));
   SCX_CHECK_LAUNCH("unpack_diff_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_unpack_fkdiff(const uint32_t* words, int64_t n, int k, int64_t lo,
+                                 scx_column fk, int64_t fk_lo, scx_column ref, int64_t ref_n,
+                                 scx_column out, void* stream) {
+  if (n < 0 || k < 0 || k > 32 || ref_n < 0 || dtype_size(out.dtype) == 0 ||
+      dtype_size(ref.dtype) == 0 || dtype_size(fk.dtype) == 0 ||
+      (n > 0 && (!out.ptr || !ref.ptr || !fk.ptr)) || (n > 0 && k > 0 && !words)) {
+    set_error("scx_unpack_fkdiff: bad arguments (n=%lld k=%d)", (long long)n, k);
+    return SCX_EINVAL;
+  }
+  if (n == 0) return SCX_OK;
+  codec::launch_typed<codec::FkDiffL>(out.dtype, codec::grid_for(n), codec::kT,
+                                      static_cast<cudaStream_t>(stream), words, n, k, lo, fk,
+                                      fk_lo, ref, reinterpret_cast<void*>(out.ptr));
+  SCX_CHECK_LAUNCH("unpack_fkdiff_kernel");
   return SCX_OK;
 }

@@ -404,7 +404,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
     Single-rank tables only.
     """
     import torch
-    from .codec import PinnedPacked, scratch_bytes, upload_packed
+    from .codec import FKDIFF, PinnedPacked, scratch_bytes, upload_packed
     # SCX_UPLOAD_STREAMS=1 (default): one copy stream lands the columns
     # strictly in `order` at full PCIe rate, their unpack kernels run on a
     # separate high-priority stream (the next copy never waits for an unpack,
@@ -450,23 +450,35 @@ def upload_tables_async(host: dict, order=None, stream=None):
         if cname in cols[tname]:
             return
         hc, pinned = host[tname][cname]
+        pc = pinned.col if isinstance(pinned, PinnedPacked) else None
+        fkd = pc is not None and pc.encoding == FKDIFF
         # a column-relative (DIFF) column is unpacked against its reference:
         # the reference goes first, and the diff on the reference's copy stream
-        ref = pinned.col.ref if isinstance(pinned, PinnedPacked) else None
+        ref = pc.ref if pc is not None and not fkd else None
         if ref is not None:
             put(tname, ref)
             cs = stream_of[(tname, ref)]
         else:
+            if fkd:
+                # key-relative: the foreign key and the parent column first
+                put(tname, pc.fk)
+                put(pc.ref_table, pc.ref)
             cs = streams[k % len(streams)]
             k += 1
         stream_of[(tname, cname)] = cs
         if isinstance(pinned, PinnedPacked):
             # packed words cross PCIe, scx_unpack rebuilds the column
             nb = scratch_bytes(pinned)
-            buf = upload_packed(pinned.col, pinned.words, pinned.bases, cs,
+            if fkd:       # the unpack reads columns that may have landed on another stream
+                us = unpack_stream or cs
+                for dep in (cols[tname][pc.fk], cols[pc.ref_table][pc.ref]):
+                    us.wait_event(dep._ready[0])
+            buf = upload_packed(pc, pinned.words, pinned.bases, cs,
                                 arena[aoff:aoff + nb],
-                                cols[tname][ref]._data if ref is not None else None,
-                                unpack_stream=unpack_stream)
+                                cols[pc.ref_table][pc.ref]._data if fkd else
+                                (cols[tname][ref]._data if ref is not None else None),
+                                unpack_stream=unpack_stream,
+                                fk_col=cols[tname][pc.fk]._data if fkd else None)
             aoff += nb
             done_on = unpack_stream or cs
         else:

@@ -168,3 +168,29 @@ def test_column_ordered_upload_on_worker_streams(ds):
         raise errs[0]
     for q in qorder:
         assert P.result_digest(got[q]) == P.result_digest(P.reference_run(q, plain)), q
+
+
+def test_key_relative_dates_roundtrip(ds):
+    """pack_tables: child dates stored against the parent row's date through
+    the dense foreign key (FKDIFF) where >= 2 bits narrower; a same-row DIFF
+    may reference a key-relative column; every column round-trips."""
+    packs = codec.pack_tables(ds.tables)
+    li, od = ds.tables["lineitem"], ds.tables["orders"]
+    fk = [c for c, pc in packs["lineitem"].items() if pc.encoding == codec.FKDIFF]
+    assert fk, "no key-relative date column chosen"
+    dec = {}
+    for c in fk:
+        pc = packs["lineitem"][c]
+        assert pc.k + 2 <= codec.pack_column(li.columns[c]).k
+        dec[c] = codec.unpack_host(pc, od.columns[pc.ref].values, li.columns[pc.fk].values)
+    for t, ht in ds.tables.items():
+        for c, pc in packs[t].items():
+            if pc.encoding == codec.FKDIFF:
+                got = dec[c]
+            elif pc.encoding == codec.DIFF:
+                got = codec.unpack_host(pc, ht.columns[pc.ref].values)
+            else:
+                got = codec.unpack_host(pc)
+            assert np.array_equal(got, ht.columns[c].values), (t, c, pc.encoding)
+    assert sum(pc.nbytes for p in packs.values() for pc in p.values()) < \
+        sum(codec.pack_table(ht)[c].nbytes for ht in ds.tables.values() for c in ht.columns)

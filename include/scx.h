@@ -535,6 +535,13 @@ int scx_unpack_diff(const uint32_t* words_dev, int64_t n, int k, int64_t lo, scx
  * path (codec.py); no reference counterpart. */
 int scx_unpack_fkdiff(const uint32_t* words, int64_t n, int k, int64_t lo, scx_column fk,
                       int64_t fk_lo, scx_column ref, int64_t ref_n, scx_column out, void* stream);
+/* key-indexed unpack: out[i] = ref[(fk[i] - fk_lo) * fanout + field(words, i, k)],
+ * ref a parent column grouped by a dense key with `fanout` rows per key (a
+ * child value that is one of its parent group's values: l_suppkey among the
+ * partsupp suppliers of l_partkey).  Load-path extension; no reference
+ * counterpart. */
+int scx_unpack_fkidx(const uint32_t* words, int64_t n, int k, scx_column fk, int64_t fk_lo,
+                     int64_t fanout, scx_column ref, int64_t ref_n, scx_column out, void* stream);
 
 #ifdef __cplusplus
 }

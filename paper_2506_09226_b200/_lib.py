@@ -181,6 +181,8 @@ _PROTOS = {
     "scx_unpack_diff": (C.c_int, [_vp, i64, C.c_int, i64, Column_, Column_, _vp]),
     "scx_unpack_fkdiff": (C.c_int, [_vp, i64, C.c_int, i64, Column_, i64, Column_, i64, Column_,
                                     _vp]),
+    "scx_unpack_fkidx": (C.c_int, [_vp, i64, C.c_int, Column_, i64, i64, Column_, i64, Column_,
+                                   _vp]),
 }
 
 EXPORTS = tuple(_PROTOS)

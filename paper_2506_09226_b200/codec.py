@@ -16,6 +16,10 @@ paper's cold run) -- is bound by PCIe, ~48 GB/s against
 * FKDIFF-- a date against its parent row's date through a foreign key into a
            dense key (l_receiptdate - o_orderdate[l_orderkey - 1]: 8 bits
            instead of 12; l_commitdate: 6), chosen only where it is narrower;
+* FKIDX -- a column that is one of its parent group's values, as its index in
+           the group (l_suppkey = the j-th partsupp supplier of l_partkey:
+           2 bits instead of 20), where the parent is grouped by a dense key
+           with a fixed fan-out;
 * RAW   -- anything that would not shrink (raw float64, k >= the narrowed width).
 
 ``scx_pack_host`` (threaded C++) packs; ``scx_unpack`` rebuilds the narrowed
@@ -41,6 +45,11 @@ FKDIFF = 4               # key-relative: value = parent[fk[i] - fk_lo] + lo + fi
 # (child table, foreign key, parent table, dense parent key): the key-relative
 # candidates the packer tries (TPC-H's lineitem -> orders, data.py schema)
 FOREIGN_KEYS = (("lineitem", "l_orderkey", "orders", "o_orderkey"),)
+FKIDX = 5                # key-indexed: value = parent[(fk[i] - fk_lo) * fanout + field]
+# (child, group key, member, parent, parent group key, parent member): the
+# composite foreign keys the packer tries (lineitem (partkey, suppkey) ->
+# partsupp, TPC-H's PARTSUPP relation)
+COMPOSITE_KEYS = (("lineitem", "l_partkey", "l_suppkey", "partsupp", "ps_partkey", "ps_suppkey"),)
 _CHUNK = 1 << 24
 
 
@@ -59,7 +68,8 @@ class PackedColumn:
     ref: str | None = None               # DIFF: the reference column of the same table
     fk: str | None = None                # FKDIFF: foreign-key column of this table
     fk_lo: int = 0                       # FKDIFF: parent row = fk - fk_lo
-    ref_table: str | None = None         # FKDIFF: parent table (ref = its column)
+    ref_table: str | None = None         # FKDIFF / FKIDX: parent table (ref = its column)
+    fanout: int = 1                      # FKIDX: parent rows per key
 
     @property
     def dtype(self) -> np.dtype:
@@ -197,6 +207,47 @@ def _pack_fkdiff(hc: HostColumn, fk: HostColumn, parent: HostColumn, fk_lo: int,
     return PackedColumn(hc, n, FKDIFF, k, lo, words, None, ref, fk_name, fk_lo, ref_table)
 
 
+def _pack_fkidx(hc: HostColumn, fk: HostColumn, pkey: HostColumn, pval: HostColumn,
+                ref: str, ref_table: str, fk_name: str, threads: int) -> PackedColumn | None:
+    """Index of each value within its parent group (None when the parent is
+    not grouped by a dense key with a fixed fan-out, or a value is not among
+    its group's)."""
+    pk = np.asarray(pkey.values)
+    npar = len(pk)
+    if npar == 0 or pkey.hi < pkey.lo:
+        return None
+    nkeys = pkey.hi - pkey.lo + 1
+    if npar % nkeys:
+        return None
+    fan = npar // nkeys
+    for s0 in range(0, npar, _CHUNK):           # grouped: key = lo + row // fanout
+        r = np.arange(s0, min(npar, s0 + _CHUNK), dtype=np.int64)
+        if not np.array_equal(pk[s0:s0 + _CHUNK].astype(np.int64), pkey.lo + r // fan):
+            return None
+    pv = np.asarray(pval.values)
+    v = np.asarray(hc.values)
+    n = len(v)
+    idx = np.empty(n, dtype=np.int64)
+    for s0 in range(0, n, _CHUNK):
+        f = np.asarray(fk.values[s0:s0 + _CHUNK]).astype(np.int64) - pkey.lo
+        if f.size and (f.min() < 0 or f.max() >= nkeys):
+            return None
+        base = f * fan
+        want = v[s0:s0 + _CHUNK]
+        j = np.full(len(f), -1, dtype=np.int64)
+        for g in range(fan - 1, -1, -1):        # first match wins
+            j[pv[base + g] == want] = g
+        if (j < 0).any():
+            return None
+        idx[s0:s0 + len(f)] = j
+    k = _bits(fan - 1)
+    lib = L.load()
+    words = np.empty(int(lib.scx_pack_words(n, k)), dtype=np.uint32)
+    L.call("scx_pack_host", idx.ctypes.data_as(C.c_void_p), L.SCX_I64, n, 0, k, 0,
+           words.ctypes.data_as(C.c_void_p), None, threads)
+    return PackedColumn(hc, n, FKIDX, k, 0, words, None, ref, fk_name, pkey.lo, ref_table, fan)
+
+
 def pack_tables(tables: dict, threads: int = 0) -> dict[str, dict[str, PackedColumn]]:
     """pack_table for every table, then each child date column of a
     FOREIGN_KEYS pair stored against a parent date (FKDIFF) where that is at
@@ -225,6 +276,18 @@ def pack_tables(tables: dict, threads: int = 0) -> dict[str, dict[str, PackedCol
                     best = pc
             if best is not None and best.k + 2 <= out[child][c].k:
                 out[child][c] = best
+    for child, fk, member, parent, pkey, pmember in COMPOSITE_KEYS:
+        if child not in tables or parent not in tables:
+            continue
+        ct, pt = tables[child], tables[parent]
+        if not ({fk, member} <= set(ct.columns) and {pkey, pmember} <= set(pt.columns)):
+            continue
+        if ct.columns[member].row_count == 0 or out[child][member].encoding == RAW:
+            continue
+        pc = _pack_fkidx(ct.columns[member], ct.columns[fk], pt.columns[pkey],
+                         pt.columns[pmember], pmember, parent, fk, threads)
+        if pc is not None and pc.k + 2 <= out[child][member].k:
+            out[child][member] = pc
     return out
 
 
@@ -234,6 +297,11 @@ def unpack_host(pc: PackedColumn, ref_values: np.ndarray | None = None,
     (test infrastructure)."""
     if pc.encoding == RAW:
         return np.asarray(pc.meta.values)
+    if pc.encoding == FKIDX:
+        f = unpack_host(PackedColumn(pc.meta, pc.n, L.PACK_FOR, pc.k, 0, pc.words)).astype(np.int64) \
+            if pc.k else np.zeros(pc.n, dtype=np.int64)
+        row = (np.asarray(fk_values).astype(np.int64) - pc.fk_lo) * pc.fanout + f
+        return np.asarray(ref_values)[row].astype(pc.dtype)
     if pc.encoding == FKDIFF:
         f = unpack_host(PackedColumn(pc.meta, pc.n, L.PACK_FOR, pc.k, 0, pc.words)).astype(np.int64) \
             if pc.k else np.zeros(pc.n, dtype=np.int64)
@@ -325,7 +393,12 @@ def upload_packed(pc: PackedColumn, src_words, src_bases, stream, scratch=None, 
                 if t is not None:
                     t.record_stream(us)
     with torch.cuda.stream(us):
-        if pc.encoding == FKDIFF:
+        if pc.encoding == FKIDX:
+            L.call("scx_unpack_fkidx", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n,
+                   pc.k, L.Column_(fk_col.data_ptr(), _scx_of(fk_col), 0), pc.fk_lo, pc.fanout,
+                   L.Column_(ref_col.data_ptr(), _scx_of(ref_col), 0), ref_col.numel(),
+                   L.Column_(buf.data_ptr(), NP_TO_SCX[pc.dtype], 0), L.stream_ptr(us))
+        elif pc.encoding == FKDIFF:
             L.call("scx_unpack_fkdiff", C.c_void_p(dw.data_ptr() if dw is not None else 0), pc.n,
                    pc.k, pc.lo, L.Column_(fk_col.data_ptr(), _scx_of(fk_col), 0), pc.fk_lo,
                    L.Column_(ref_col.data_ptr(), _scx_of(ref_col), 0), ref_col.numel(),

@@ -153,6 +153,21 @@ __global__ void unpack_fkdiff_kernel(const uint32_t* __restrict__ words, int64_t
                  (int64_t)(k ? field(words, i, k) : 0));
 }
 
+// key-indexed: value = ref[(fk[i] - fk_lo) * fanout + field] -- a column
+// that is one of its parent group's values (l_suppkey = one of the 4
+// partsupp suppliers of l_partkey: 2 bits instead of 20)
+template <typename T>
+__global__ void unpack_fkidx_kernel(const uint32_t* __restrict__ words, int64_t n, int k,
+                                    scx_column fk, int64_t fk_lo, int64_t fanout, scx_column ref,
+                                    T* __restrict__ out) {
+  const void* f = reinterpret_cast<const void*>(fk.ptr);
+  const void* r = reinterpret_cast<const void*>(ref.ptr);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (T)load_i64(r, ref.dtype, (load_i64(f, fk.dtype, i) - fk_lo) * fanout +
+                                           (int64_t)(k ? field(words, i, k) : 0));
+}
+
 template <typename T>
 __global__ void iota_kernel(int64_t n, int64_t lo, T* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -194,6 +209,12 @@ template <typename T> struct FkDiffL {
   static void run(dim3 g, dim3 b, cudaStream_t st, const uint32_t* w, int64_t n, int k, int64_t lo,
                   scx_column fk, int64_t fk_lo, scx_column ref, void* out) {
     unpack_fkdiff_kernel<T><<<g, b, 0, st>>>(w, n, k, lo, fk, fk_lo, ref, static_cast<T*>(out));
+  }
+};
+template <typename T> struct FkIdxL {
+  static void run(dim3 g, dim3 b, cudaStream_t st, const uint32_t* w, int64_t n, int k,
+                  scx_column fk, int64_t fk_lo, int64_t fanout, scx_column ref, void* out) {
+    unpack_fkidx_kernel<T><<<g, b, 0, st>>>(w, n, k, fk, fk_lo, fanout, ref, static_cast<T*>(out));
   }
 };
 template <typename T> struct IotaL {
@@ -313,5 +334,22 @@ extern "C" int scx_unpack_fkdiff(const uint32_t* words, int64_t n, int k, int64_
                                       static_cast<cudaStream_t>(stream), words, n, k, lo, fk,
                                       fk_lo, ref, reinterpret_cast<void*>(out.ptr));
   SCX_CHECK_LAUNCH("unpack_fkdiff_kernel");
+  return SCX_OK;
+}
+
+extern "C" int scx_unpack_fkidx(const uint32_t* words, int64_t n, int k, scx_column fk,
+                                int64_t fk_lo, int64_t fanout, scx_column ref, int64_t ref_n,
+                                scx_column out, void* stream) {
+  if (n < 0 || k < 0 || k > 32 || fanout < 1 || ref_n < 0 || dtype_size(out.dtype) == 0 ||
+      dtype_size(ref.dtype) == 0 || dtype_size(fk.dtype) == 0 ||
+      (n > 0 && (!out.ptr || !ref.ptr || !fk.ptr)) || (n > 0 && k > 0 && !words)) {
+    set_error("scx_unpack_fkidx: bad arguments (n=%lld k=%d)", (long long)n, k);
+    return SCX_EINVAL;
+  }
+  if (n == 0) return SCX_OK;
+  codec::launch_typed<codec::FkIdxL>(out.dtype, codec::grid_for(n), codec::kT,
+                                     static_cast<cudaStream_t>(stream), words, n, k, fk, fk_lo,
+                                     fanout, ref, reinterpret_cast<void*>(out.ptr));
+  SCX_CHECK_LAUNCH("unpack_fkidx_kernel");
   return SCX_OK;
 }

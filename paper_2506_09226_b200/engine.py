@@ -404,7 +404,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
     Single-rank tables only.
     """
     import torch
-    from .codec import FKDIFF, PinnedPacked, scratch_bytes, upload_packed
+    from .codec import FKDIFF, FKIDX, PinnedPacked, scratch_bytes, upload_packed
     # SCX_UPLOAD_STREAMS=1 (default): one copy stream lands the columns
     # strictly in `order` at full PCIe rate, their unpack kernels run on a
     # separate high-priority stream (the next copy never waits for an unpack,
@@ -451,7 +451,7 @@ def upload_tables_async(host: dict, order=None, stream=None):
             return
         hc, pinned = host[tname][cname]
         pc = pinned.col if isinstance(pinned, PinnedPacked) else None
-        fkd = pc is not None and pc.encoding == FKDIFF
+        fkd = pc is not None and pc.encoding in (FKDIFF, FKIDX)
         # a column-relative (DIFF) column is unpacked against its reference:
         # the reference goes first, and the diff on the reference's copy stream
         ref = pc.ref if pc is not None and not fkd else None

@@ -172,8 +172,9 @@ def test_column_ordered_upload_on_worker_streams(ds):
 
 def test_key_relative_dates_roundtrip(ds):
     """pack_tables: child dates stored against the parent row's date through
-    the dense foreign key (FKDIFF) where >= 2 bits narrower; a same-row DIFF
-    may reference a key-relative column; every column round-trips."""
+    the dense foreign key (FKDIFF) where >= 2 bits narrower, l_suppkey as its
+    index among l_partkey's partsupp suppliers (FKIDX); a same-row DIFF may
+    reference a key-relative column; every column round-trips."""
     packs = codec.pack_tables(ds.tables)
     li, od = ds.tables["lineitem"], ds.tables["orders"]
     fk = [c for c, pc in packs["lineitem"].items() if pc.encoding == codec.FKDIFF]
@@ -183,9 +184,13 @@ def test_key_relative_dates_roundtrip(ds):
         pc = packs["lineitem"][c]
         assert pc.k + 2 <= codec.pack_column(li.columns[c]).k
         dec[c] = codec.unpack_host(pc, od.columns[pc.ref].values, li.columns[pc.fk].values)
+    ix = packs["lineitem"]["l_suppkey"]
+    assert ix.encoding == codec.FKIDX and ix.k == 2 and ix.fanout == 4
+    dec["l_suppkey"] = codec.unpack_host(ix, ds.tables["partsupp"].columns["ps_suppkey"].values,
+                                         li.columns["l_partkey"].values)
     for t, ht in ds.tables.items():
         for c, pc in packs[t].items():
-            if pc.encoding == codec.FKDIFF:
+            if pc.encoding in (codec.FKDIFF, codec.FKIDX):
                 got = dec[c]
             elif pc.encoding == codec.DIFF:
                 got = codec.unpack_host(pc, ht.columns[pc.ref].values)

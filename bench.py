@@ -135,6 +135,27 @@ def e2e_order(host: dict, cost: dict | None = None, rate_gbs: float = 54.0):
     owner = {c: t for t in host for c in host[t]}
     nbytes = {c: _src_bytes(host[t][c][1]) for c, t in owner.items()}
     qcols = query_columns(set(owner))
+    # a packed column relative to others (codec DIFF / FKDIFF / FKIDX) lands
+    # only after them: a query reading it waits for its whole dependency closure
+    deps = {}
+    for c, t in owner.items():
+        pc = getattr(host[t][c][1], "col", None)
+        d = set()
+        if pc is not None and pc.ref is not None:
+            d.add(pc.ref)
+        if pc is not None and pc.fk is not None:
+            d.add(pc.fk)
+        deps[c] = {x for x in d if x in owner}
+
+    def closure(cs):
+        out, todo = set(), list(cs)
+        while todo:
+            x = todo.pop()
+            if x not in out:
+                out.add(x)
+                todo.extend(deps.get(x, ()))
+        return out
+    qcols = {q: closure(cs) for q, cs in qcols.items()}
     cost = {q: (cost or {}).get(q) or Q_COST.get(q, 1.0) for q in QUERIES}
     rate = rate_gbs * 1e6                  # bytes per ms
     best = sorted(QUERIES, key=lambda x: -cost[x])

@@ -771,6 +771,7 @@ def main() -> None:
         start = torch.cuda.Event()
         start.record()
         results, errors, lock = {}, [], threading.Lock()
+        pending = list(order or QUERIES)
         done = [torch.cuda.Event() for _ in worker_streams]
 
         def work(i):
@@ -779,7 +780,19 @@ def main() -> None:
                 s = worker_streams[i]
                 with torch.cuda.stream(s):
                     s.wait_event(start)
-                    mine = [q for q in (order or QUERIES) if q in (assign or assignment)[i]]
+                    if assign == "dynamic":
+                        # a shared queue in `order`: each worker takes the next
+                        # query as soon as it is free
+                        def mine_iter():
+                            while True:
+                                with lock:
+                                    if not pending:
+                                        return
+                                    q = pending.pop(0)
+                                yield q
+                        mine = mine_iter()
+                    else:
+                        mine = [q for q in (order or QUERIES) if q in (assign or assignment)[i]]
                     for q in mine:
                         if per_query is not None:
                             e0 = torch.cuda.Event(enable_timing=True)
@@ -964,7 +977,10 @@ def main() -> None:
         copy_order, e2e_query_order, rel, qcost = e2e_order(
             host, {q: statistics.mean(v) for q, v in q_ms1.items() if v})
         if n_streams > 1:
-            e2e_assign = e2e_assignment(e2e_query_order, rel, qcost, n_streams)
+            # SCX_E2E_QUEUE=dynamic: workers pull from one queue in release
+            # order instead of the modelled static queues
+            e2e_assign = ("dynamic" if os.environ.get("SCX_E2E_QUEUE") == "dynamic" else
+                          e2e_assignment(e2e_query_order, rel, qcost, n_streams))
     e2e_ms, e2e_up_ms = [], []
     e2e_qdone, e2e_landed = {}, {}
     d2h_bytes = 0

@@ -979,8 +979,11 @@ def main() -> None:
         if n_streams > 1:
             # SCX_E2E_QUEUE=dynamic: workers pull from one queue in release
             # order instead of the modelled static queues
+            # (SCX_E2E_COST_SCALE: query time under contention / single-stream time)
+            cs = float(os.environ.get("SCX_E2E_COST_SCALE", "1"))
             e2e_assign = ("dynamic" if os.environ.get("SCX_E2E_QUEUE") == "dynamic" else
-                          e2e_assignment(e2e_query_order, rel, qcost, n_streams))
+                          e2e_assignment(e2e_query_order, rel,
+                                         {q: c * cs for q, c in qcost.items()}, n_streams))
     e2e_ms, e2e_up_ms = [], []
     e2e_qdone, e2e_landed = {}, {}
     d2h_bytes = 0
